@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the LJ short-range MD hot path (BASELINE.json metric:
+atom-timesteps/sec, LJ rc = 2.5 sigma, plus % of the HBM roofline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload at N = 1 is BASELINE configs[1]: fcc 64^3 cells = 1,048,576 atoms,
+rho = 0.8442, T = 1.44, rc = 2.5, skin 0.3, neighbor rebuild every 20 steps,
+full neighbor list (``--list half`` for the Newton-3 variant).  A "step" is
+one velocity-Verlet MD step (integrate, rebuild on schedule, force + final
+kick).  Timing: W untimed warm-up steps, then exactly K steps between CUDA
+events on the launching stream, barrier + synchronize on both sides, max over
+ranks.  The working set (Verlet list ~330 MB at 1M atoms) exceeds the 126 MB
+L2, so no explicit L2 flush is done between steps.
+
+Under torchrun (N > 1) every rank runs its own 64^3 domain replica
+(weak scaling, no data-path collective yet -- see DESIGN.md).
+
+``--impl reference`` times the CPU oracle port of the reference
+(oracle/particula_oracle.py: numpy, single-threaded like the reference) on a
+bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "atom-timesteps/sec (LJ, rc=2.5σ)"
+UNIT = "atom-steps/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cells", type=int, default=64, help="fcc cells per axis per GPU")
+    ap.add_argument("--temperature", type=float, default=1.44)
+    ap.add_argument("--rebuild", type=int, default=20)
+    ap.add_argument("--list", choices=["full", "half"], default="full")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def md_kwargs(args, cells):
+    return dict(lattice_cells=cells, density=0.8442, temperature=args.temperature, dt=0.005,
+                cutoff=2.5, skin=0.3, rebuild_stride=args.rebuild, seed=1)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h,
+                                                                    self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        import statistics
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(kw, cells, steps):
+    """Oracle port of the reference MD (numpy, 1 thread) on a bounded sample."""
+    from oracle import particula_oracle as orc
+    cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=steps))
+    drv = orc.MDOracle(cfg)
+    t0 = time.perf_counter()
+    for s in range(1, steps + 1):
+        drv.step(s)
+    dt = time.perf_counter() - t0
+    return drv.n * steps / dt, drv.n, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    kw = md_kwargs(args, args.cells)
+    # size the sample so warmup+steps finish in ~2 minutes of CPU time
+    probe_rate, _, _ = cpu_oracle_rate(kw, 8, 2)
+    budget_atoms = probe_rate * 120.0 / max(1, args.steps + args.warmup)
+    cells = max(6, min(args.cells, int((budget_atoms / 4) ** (1 / 3))))
+    from oracle import particula_oracle as orc
+    cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=args.steps))
+    drv = orc.MDOracle(cfg)
+    for s in range(1, args.warmup + 1):
+        drv.step(s)
+    t0 = time.perf_counter()
+    for s in range(args.warmup + 1, args.warmup + args.steps + 1):
+        drv.step(s)
+    dt = time.perf_counter() - t0
+    value = drv.n * args.steps / dt
+    sample = (f"oracle port (numpy, 1 thread, like the reference) MD on fcc {cells}^3 = "
+              f"{drv.n} atoms, same rho/T/rc/skin/rebuild as the {args.cells}^3 workload")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"LJ fcc {args.cells}^3 x{world}", "sample_atoms": drv.n,
+                       "rebuild_stride": args.rebuild, "list": "full"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    import paper_2109_09056_b200 as pc
+    from paper_2109_09056_b200 import _lib
+
+    kw = md_kwargs(args, args.cells)
+    cfg = pc.md.MDConfig(**kw, steps=args.steps)
+    drv = pc.md.MDDriver(cfg, time_phases=False)
+    n = drv.n
+    W, K = args.warmup, args.steps
+    for s in range(1, W + 1):
+        drv.step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib = _lib.load()
+    drv.force_events = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.pc_launch_count()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for s in range(W + 1, W + K + 1):
+            drv.step(s)
+        ev1.record()
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    launches = lib.pc_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    value = n * world * K / (ms * 1e-3)
+    diag = drv.diagnostics()
+    force_ms = [a.elapsed_time(b) for a, b in drv.force_events]
+    drv.force_events = None
+    kmean = float(drv.cnt[:n].float().mean().item())
+    # algorithmic bytes per force launch per atom: Verlet indices
+    # 4k + row count 4 + pos4 read once 32 (L2-resident afterwards) + FP64
+    # force write 24 + fused final kick v read+write 48
+    bytes_per_atom = 4 * kmean + 4 + 32 + 24 + 48
+    force_avg_s = float(np.mean(force_ms)) * 1e-3
+    achieved = n * bytes_per_atom / force_avg_s / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "force_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("bytes_per_launch_per_atom")
+            traffic = None if traffic is None else traffic * n
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(pc, kw, args.e2e_steps, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, natoms, secs = cpu_oracle_rate(kw, 16, 20)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"oracle port (numpy, 1 thread) 20 MD steps on fcc 16^3 = {natoms} "
+                         f"atoms, same rho/T/rc/skin/rebuild ({secs:.1f} s)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32(LJ magnitude)",
+                "data": "synthetic fcc lattice, seeded Gaussian velocities",
+                "config": {"workload": f"LJ fcc {args.cells}^3 ({n} atoms) per GPU, "
+                                       f"rho=0.8442 T={args.temperature} rc=2.5 skin=0.3 "
+                                       f"rebuild={args.rebuild} {args.list} list",
+                           "atoms_per_gpu": n, "global_atoms": n * world,
+                           "parallelism": f"domain x{world}" if world > 1 else "single domain",
+                           "l2": "working set > L2 (Verlet list ~4k B/atom), no flush",
+                           "mean_neighbors": kmean},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "lj_force_kernel<ELL> (+fused final kick)",
+                             "bytes_per_atom": bytes_per_atom, "peak_kind": peak_kind,
+                             "avg_launch_us": force_avg_s * 1e6},
+                "gpu_launches": int(launches),
+                "clocks": clk.summary(),
+                "e2e": e2e, "cpu_baseline": cpu,
+                "check": {"E_total": diag["E_total"], "temperature": diag["temperature"]}}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(pc, kw, steps, world):
+    """Same metric through the public API with host buffers: pinned host x, v
+    uploaded inside the timed region, then `steps` MD steps each followed by
+    diagnostics() (device reduction + D2H of 5 doubles), as run_md does."""
+    import torch
+    n = 4 * kw["lattice_cells"] ** 3
+    a = (4.0 / kw["density"]) ** (1.0 / 3.0)
+    x = torch.as_tensor(pc.md.fcc_lattice(kw["lattice_cells"], a)).pin_memory()
+    v = torch.as_tensor(pc.md.initial_velocities(n, kw["temperature"], 1.0,
+                                                 kw["seed"])).pin_memory()
+    cfg = pc.md.MDConfig(**kw, steps=steps)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    drv = pc.md.MDDriver(cfg, time_phases=False, state=(x, v))
+    drv.diagnostics()
+    for s in range(1, steps + 1):
+        drv.step(s)
+        drv.diagnostics()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": n * world * steps / (ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": n * 48 / steps, "d2h_bytes_per_step": 40,
+            "steps": steps, "includes": "H2D of x,v + init rebuild/force + per-step "
+                                        "diagnostics D2H"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

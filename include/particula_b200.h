@@ -1,0 +1,228 @@
+/*
+ * particula_b200.h -- C ABI of the B200-native LJ short-range MD hot path.
+ *
+ * Drop-in boundary for the reference package `particula` (arXiv 2109.09056
+ * proxy, /root/reference/pkg/src/particula).  The reference has no FFI of its
+ * own: its "interface" is the set of Python module functions listed below.
+ * Each entry point here replaces the numpy body of one of them; the Python
+ * package `paper_2109_09056_b200` keeps the reference's names, argument
+ * meanings and exceptions and calls these functions through ctypes.
+ *
+ * Conventions
+ *   - every pointer argument named d_* is DEVICE memory owned by the caller
+ *     (torch tensors); the library never allocates or frees caller memory;
+ *   - `stream` is a cudaStream_t passed as void*; all calls are asynchronous
+ *     on that stream unless stated otherwise;
+ *   - return value: PC_OK or a negative status; pc_last_error() holds the
+ *     message (thread-local).  The Python shim maps PC_ERR_VALUE -> ValueError,
+ *     PC_ERR_RUNTIME -> RuntimeError, PC_ERR_OVERLAP -> FloatingPointError
+ *     (ref neighbors.py:107-118, decomp.py:138-140, md.py:118-119);
+ *   - positions are FP64 (x, y, z, tag) quadruples ("pos4", 32 B per particle,
+ *     one DRAM sector per gather); `tag` is an int64 stored bit-for-bit in the
+ *     4th slot (global id in MD, caller index in the list API).
+ */
+#ifndef PARTICULA_B200_H
+#define PARTICULA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PC_OK 0
+#define PC_ERR_VALUE (-1)     /* ValueError            */
+#define PC_ERR_RUNTIME (-2)   /* RuntimeError          */
+#define PC_ERR_OVERLAP (-3)   /* FloatingPointError    */
+#define PC_ERR_CUDA (-4)      /* CUDA launch / runtime */
+#define PC_ERR_CAPACITY (-5)  /* output capacity too small; caller grows + retries */
+
+/* Periodic box, ref geometry.py:10-58.  mi_thresh[a] = smallest d > 0 with
+ * fl(d / length[a]) > 0.5 (the division-free, bit-exact form of
+ * d - L*round(d/L) for |d| < L); +inf on non-periodic axes. */
+typedef struct pc_box {
+  double low[3];
+  double high[3];
+  double length[3];
+  double mi_thresh[3];
+  int32_t periodic[3];
+  int32_t ndim;
+} pc_box;
+
+/* Linked-cell grid: cell = clamp(floor((x - low) / width), 0, nc - 1) per
+ * axis, row-major flat id.  Ref binning.py:58-73 (width = cell_size) and
+ * neighbors.py:56-60 (width = L / nc). */
+typedef struct pc_grid {
+  double low[3];
+  double high[3];
+  double width[3];
+  int32_t nc[3];
+  int32_t ncells;
+  int32_t ndim;       /* coordinates per position actually used (1..3) */
+  int32_t pad;
+} pc_grid;
+
+/* LJ parameters, ref md.py:89-126. */
+typedef struct pc_lj {
+  double epsilon;
+  double sigma;
+  double cutoff2;      /* cutoff*cutoff evaluated in FP64 on the host */
+  double overlap2;     /* (1e-10*sigma)^2 : FloatingPointError below */
+} pc_lj;
+
+/* ---- library ---------------------------------------------------------- */
+const char* pc_last_error(void);
+int pc_version(void);
+/* Kernels launched through this library since load (bench evidence). */
+int64_t pc_launch_count(void);
+int pc_device_sync(void* stream);
+
+/* ---- particle storage (ref aosoa.py) ----------------------------------- */
+/* AoSoA element move: element (i, w) of `src` goes to element (map[i], w) of
+ * `dst`.  Word w of particle i lives at byte
+ *   struct_bytes*(i/V) + word_base[w] + (i%V)*8,
+ * word_base[w] = field byte offset + 8*V*component (ref aosoa.py:63-67).
+ * Replaces the per-field copy_out/copy_in of ref binning.py:90-101. */
+int pc_aosoa_permute(const void* d_src, void* d_dst, const int64_t* d_map,
+                     int64_t n, int32_t V, int64_t struct_bytes,
+                     const int64_t* d_word_base, int32_t nwords, void* stream);
+
+/* dst[k] = src[order[k]] for rows of row_bytes (4 or a multiple of 8). */
+int pc_gather_rows(const void* d_src, void* d_dst, const int32_t* d_order,
+                   int64_t n, int32_t row_bytes, void* stream);
+/* dst[order[k]] = src[k] (row_bytes 4 or a multiple of 8). */
+int pc_scatter_rows(const void* d_src, void* d_dst, const int32_t* d_order,
+                    int64_t n, int32_t row_bytes, void* stream);
+/* One AoSoA field <-> dense (n, ncomp) 8-byte words (copy_out / copy_in of
+ * ref aosoa.py:124-142). */
+int pc_aosoa_field(void* d_buf, int64_t n, int32_t V, int64_t struct_bytes,
+                   int64_t field_off, int32_t ncomp, void* d_dense, int32_t to_dense,
+                   void* stream);
+
+/* ---- binning (ref binning.py:49-101) ------------------------------------ */
+/* Per-particle flat cell id and warp-aggregated atomic cell counts
+ * (ref binning.py:58-73,83 and neighbors.py:56-65).  d_cell_count must be
+ * zeroed by the caller.  check_inside != 0 raises the ValueError of
+ * binning.py:68-69 through d_flag (bit 0). */
+int pc_bin_count(const double* d_x, int64_t n, int32_t x_stride,
+                 const pc_grid* grid, int32_t check_inside, int32_t* d_cell_of,
+                 int64_t* d_axis_idx /* (n, ndim) per-axis cells or NULL */,
+                 int32_t* d_cell_count, int32_t* d_flag, void* stream);
+
+/* Digit "cells" of int64 keys for the LSD passes of bin_by_key
+ * (ref binning.py:49-55): cell = ((key[perm[i]] - kmin) >> shift) & mask. */
+int pc_key_digits(const int64_t* d_keys, const int32_t* d_perm, int64_t n, int64_t kmin,
+                  int32_t shift, int64_t mask, int32_t* d_cell_of, int32_t* d_cell_count,
+                  void* stream);
+
+/* Permutation.is_bijection (ref binning.py:26-33): d_flag bit0 = out of range,
+ * bit1 = duplicate.  d_seen (n int32) zeroed by the caller. */
+int pc_check_bijection(const int64_t* d_map, int64_t n, int32_t* d_seen, int32_t* d_flag,
+                       void* stream);
+
+/* Exclusive prefix sum of n int32 counts into n+1 entries (last = total);
+ * the _i64 variant widens to int64 (CSR offsets, ref neighbors.py:125-128).
+ * d_tmp must hold pc_scan_tmp_bytes(n) bytes. */
+int pc_scan_i32(const int32_t* d_in, int32_t* d_out, int64_t n,
+                void* d_tmp, int64_t tmp_bytes, void* stream);
+int pc_scan_i32_i64(const int32_t* d_in, int64_t* d_out, int64_t n,
+                    void* d_tmp, int64_t tmp_bytes, void* stream);
+int64_t pc_scan_tmp_bytes(int64_t n);
+
+/* Stable counting-sort placement: order[dst] = src with equal cells kept in
+ * ascending src order (ref binning.py:49-55 argsort(kind="stable")).
+ * d_cell_fill (ncells) must be zeroed by the caller. */
+int pc_bin_place(const int32_t* d_cell_of, int64_t n, const int32_t* d_cell_start,
+                 int32_t ncells, int32_t* d_cell_fill, int32_t* d_order_tmp,
+                 int32_t* d_order, void* stream);
+
+/* map[order[k]] = k  (Permutation.map of ref binning.py:13-33). */
+int pc_invert_order(const int32_t* d_order, int64_t n, int64_t* d_map,
+                    void* stream);
+
+/* ---- neighbor lists (ref neighbors.py:49-134) ---------------------------- */
+/* Build from cell-sorted pos4 (d_pos_sorted[k] = particle order[k]) and the
+ * cell offsets of `grid` (ncells+1).  Predicate: min-image r^2 < cutoff2 with
+ * r^2 = (dx*dx + dz*dz) + dy*dy in FP64, no FMA (bit-exact to the reference).
+ * half != 0 keeps only tag_j > tag_i (neighbors.py:121-122).
+ *   mode PC_NBR_COUNT : write d_count[k] only
+ *   mode PC_NBR_CSR   : write row k at d_offsets[k] into d_index
+ *   mode PC_NBR_ELL   : transposed ELL, entry (k, s) at d_index[s*ell_stride+k],
+ *                       s < ell_width; overflow -> d_flag bit 1 (counts still exact)
+ * out_tags != 0 writes tag_j (caller index space), else the sorted index j.
+ * Rows are emitted in ascending sorted index order. */
+#define PC_NBR_COUNT 0
+#define PC_NBR_CSR 1
+#define PC_NBR_ELL 2
+int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_start,
+                 const pc_grid* grid, const pc_box* box, double cutoff2,
+                 int32_t half, int32_t mode, int32_t out_tags,
+                 int32_t* d_count, const int64_t* d_offsets, int32_t* d_index,
+                 int64_t ell_stride, int32_t ell_width, int32_t* d_flag,
+                 void* stream);
+
+/* CSR -> dense (n, width) int64 table, -1 padded (ref neighbors.py:130-134). */
+int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,
+                    int32_t width, int64_t* d_table, void* stream);
+
+/* Sort every CSR row ascending (int32 values), warp per row. */
+int pc_sort_rows(const int64_t* d_offsets, int32_t n, int32_t* d_index,
+                 void* stream);
+
+/* ---- LJ force (ref md.py:89-126) ----------------------------------------- */
+/* Force on rows [0, n_rows) from a neighbor list over pos4 (rows index the
+ * same pos4 array; neighbor values index it too).  FP64 min-image and exact
+ * cutoff test, FP32 LJ magnitude, FP64 force accumulation (exactly
+ * antisymmetric pair forces), FP64 energy partials.
+ * Layout: ell_stride > 0 -> transposed ELL (d_index[s*ell_stride + i]);
+ *         else CSR via d_offsets.
+ * Outputs (any may be NULL):
+ *   d_f3      : double[3][f_stride] planar force
+ *   d_f64     : double (n_rows, 3) row-major force (API path)
+ *   d_pe      : double per-row energy, each pair booked on the smaller tag
+ *   d_v       : double[3][v_stride] planar velocity, fused final half kick
+ *               v += dtm*f (ref md.py:251-257) when non-NULL
+ *   d_partial : double[5*gridDim] per-block (KE after kick, PE, px, py, pz)
+ * Overlap (r^2 < overlap2) sets d_flag bit 2 (FloatingPointError). */
+int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                const int64_t* d_offsets, const int32_t* d_index,
+                int64_t ell_stride, const pc_box* box, const pc_lj* lj,
+                double* d_f3, int64_t f_stride, double* d_f64, double* d_pe,
+                double* d_v, int64_t v_stride, double dtm, double mass,
+                double* d_partial, int32_t* d_flag, void* stream);
+int32_t pc_lj_force_blocks(int32_t n_rows);
+
+/* Half-list Newton-3 variant: rows hold j > i only; f_j -= F via FP32
+ * atomics (not bitwise deterministic).  d_f3 must be zeroed by the caller. */
+int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                     const int32_t* d_index, int64_t ell_stride,
+                     const pc_box* box, const pc_lj* lj, double* d_f3,
+                     int64_t f_stride, double* d_pe_total, int32_t* d_flag,
+                     void* stream);
+
+/* ---- integrate (ref md.py:219-257, geometry.py:40-49) --------------------- */
+/* v += dtm*f; x += dt*v; x = wrap(x) on rows [0,n) -- numpy rounding order. */
+int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride,
+                       const double* d_f3, int64_t f_stride, int32_t n,
+                       double dtm, double dt, const pc_box* box, void* stream);
+/* v += dtm*f, plus the per-block diagnostic partials (KE, 0, px, py, pz). */
+int pc_kick(double* d_v, int64_t v_stride, const double* d_f3, int64_t f_stride,
+            int32_t n, double dtm, double mass, double* d_partial, void* stream);
+
+/* Box.wrap / Box.min_image in place on (rows, d) FP64 arrays
+ * (ref geometry.py:40-49, :51-58). */
+int pc_box_wrap(double* d_x, int64_t rows, int32_t d, const pc_box* box, void* stream);
+int pc_box_min_image(double* d_x, int64_t rows, int32_t d, const pc_box* box, void* stream);
+
+/* lj_pair (ref md.py:89-96) in FP64: e[n], f[n][3] for dx[n][3], r2[n]. */
+int pc_lj_pair(const double* d_dx, const double* d_r2, int64_t n, double eps, double sigma,
+               double* d_e, double* d_f, void* stream);
+
+/* Sum per-block partials (nblocks x 5) into out[5] in a fixed order. */
+int pc_reduce_partials(const double* d_partial, int32_t nblocks, double* d_out,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARTICULA_B200_H */

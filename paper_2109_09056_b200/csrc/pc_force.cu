@@ -1,0 +1,222 @@
+// Lennard-Jones force over a Verlet list (ref md.py:89-126).
+//
+// Thread per row.  Each candidate j is gathered as one 256-bit pos4 load; the
+// displacement, minimum image and the exact-cutoff re-filter run in FP64 with
+// the reference's rounding order, so the set of interacting pairs is the
+// reference's set bit for bit.  The LJ magnitude (rcp, sr6, fmag) is FP32;
+// the force is accumulated in FP64 as f += fmag*dx on the FP64 displacement,
+// so pair forces stay exactly antisymmetric and total momentum is conserved
+// to FP64 rounding (ref test: |P| < 1e-9).  Energies are booked on the
+// smaller tag (md.py:123-125) in FP32 per row and reduced in FP64.
+// The final half kick v += dtm*f (md.py:251-257) and the KE/PE/momentum
+// block partials are fused into the epilogue.
+#include "pc_common.cuh"
+
+namespace pc {
+
+constexpr int kForceThreads = 256;
+
+struct LJConst {
+  double cutoff2, overlap2;
+  float sig2, eps4, eps24;
+};
+
+__device__ __forceinline__ void block_partials(double v0, double v1, double v2, double v3,
+                                               double v4, double* __restrict__ out) {
+  __shared__ double red[kForceThreads / 32][5];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  v2 = warp_sum(v2);
+  v3 = warp_sum(v3);
+  v4 = warp_sum(v4);
+  if (lane == 0) {
+    red[wid][0] = v0; red[wid][1] = v1; red[wid][2] = v2; red[wid][3] = v3; red[wid][4] = v4;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double s = 0.0;
+    for (int w = 0; w < kForceThreads / 32; ++w) s += red[w][threadIdx.x];
+    out[blockIdx.x * 5 + threadIdx.x] = s;
+  }
+}
+
+template <bool ELL>
+__global__ void __launch_bounds__(kForceThreads)
+lj_force_kernel(const double* __restrict__ pos, int n_rows, const int* __restrict__ count,
+                const int64_t* __restrict__ offsets, const int* __restrict__ index,
+                int64_t ell_stride, pc_box b, LJConst c, double* __restrict__ f3,
+                int64_t f_stride, double* __restrict__ f64, double* __restrict__ pe,
+                double* __restrict__ v, int64_t v_stride, double dtm, double mass,
+                double* __restrict__ partial, int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n_rows;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  float ei = 0.f;
+  bool overlap = false;
+  if (live) {
+    const double4 pi = ld_pos4(pos + 4 * (int64_t)i);
+    const int64_t ti = tag_of(pi.w);
+    const int m = count[i];
+    const int* __restrict__ row = ELL ? index + i : index + offsets[i];
+    const int64_t step = ELL ? ell_stride : 1;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) {
+      const int j = __ldg(row + (int64_t)k * step);
+      const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
+      const double dx = min_image(__dsub_rn(pj.x, pi.x), b.length[0], b.mi_thresh[0]);
+      const double dy = min_image(__dsub_rn(pj.y, pi.y), b.length[1], b.mi_thresh[1]);
+      const double dz = min_image(__dsub_rn(pj.z, pi.z), b.length[2], b.mi_thresh[2]);
+      const double r2 = r2_exact(dx, dy, dz);
+      if (r2 < c.cutoff2) {
+        overlap |= (r2 < c.overlap2);
+        const float inv = __frcp_rn((float)r2);
+        const float sr2 = c.sig2 * inv;
+        const float sr6 = sr2 * sr2 * sr2;
+        const double fmag = (double)(c.eps24 * sr6 * (2.f * sr6 - 1.f) * inv);
+        fx = fma(-fmag, dx, fx);
+        fy = fma(-fmag, dy, fy);
+        fz = fma(-fmag, dz, fz);
+        if (tag_of(pj.w) > ti) ei += c.eps4 * sr6 * (sr6 - 1.f);
+      }
+    }
+    if (overlap) atomicOr(flag, kFlagOverlap);
+    if (f3) {
+      f3[i] = fx;
+      f3[f_stride + i] = fy;
+      f3[2 * f_stride + i] = fz;
+    }
+    if (f64) {
+      f64[3 * (int64_t)i + 0] = fx;
+      f64[3 * (int64_t)i + 1] = fy;
+      f64[3 * (int64_t)i + 2] = fz;
+    }
+    if (pe) pe[i] = (double)ei;
+  }
+  if (partial == nullptr && v == nullptr) return;
+  double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0;
+  if (live && v) {
+    // numpy: v[:o] += dtm * f[:o]  -> t = dtm*f (rounded), v = v + t (rounded)
+    double vx = __dadd_rn(v[i], __dmul_rn(dtm, fx));
+    double vy = __dadd_rn(v[v_stride + i], __dmul_rn(dtm, fy));
+    double vz = __dadd_rn(v[2 * v_stride + i], __dmul_rn(dtm, fz));
+    v[i] = vx;
+    v[v_stride + i] = vy;
+    v[2 * v_stride + i] = vz;
+    ke = __dmul_rn(0.5 * mass, r2_exact(vx, vy, vz));
+    px = mass * vx;
+    py = mass * vy;
+    pz = mass * vz;
+  }
+  if (partial) block_partials(ke, live ? (double)ei : 0.0, px, py, pz, partial);
+}
+
+// Half list (Newton's third law): each unordered pair once, f_j -= F through
+// FP64 atomics.  Energies summed per warp into one FP64 accumulator.
+__global__ void __launch_bounds__(kForceThreads)
+lj_force_half_kernel(const double* __restrict__ pos, int n_rows, const int* __restrict__ count,
+                     const int* __restrict__ index, int64_t ell_stride, pc_box b, LJConst c,
+                     double* __restrict__ f3, int64_t f_stride, double* __restrict__ pe_total,
+                     int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  float ei = 0.f;
+  if (i < n_rows) {
+    const double4 pi = ld_pos4(pos + 4 * (int64_t)i);
+    const int m = count[i];
+    bool overlap = false;
+#pragma unroll 2
+    for (int k = 0; k < m; ++k) {
+      const int j = __ldg(index + (int64_t)k * ell_stride + i);
+      const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
+      const double dx = min_image(__dsub_rn(pj.x, pi.x), b.length[0], b.mi_thresh[0]);
+      const double dy = min_image(__dsub_rn(pj.y, pi.y), b.length[1], b.mi_thresh[1]);
+      const double dz = min_image(__dsub_rn(pj.z, pi.z), b.length[2], b.mi_thresh[2]);
+      const double r2 = r2_exact(dx, dy, dz);
+      if (r2 < c.cutoff2) {
+        overlap |= (r2 < c.overlap2);
+        const float inv = __frcp_rn((float)r2);
+        const float sr2 = c.sig2 * inv;
+        const float sr6 = sr2 * sr2 * sr2;
+        const double fmag = (double)(c.eps24 * sr6 * (2.f * sr6 - 1.f) * inv);
+        const double gx = fmag * dx, gy = fmag * dy, gz = fmag * dz;
+        fx -= gx;
+        fy -= gy;
+        fz -= gz;
+        atomicAdd(f3 + j, gx);
+        atomicAdd(f3 + f_stride + j, gy);
+        atomicAdd(f3 + 2 * f_stride + j, gz);
+        ei += c.eps4 * sr6 * (sr6 - 1.f);
+      }
+    }
+    if (overlap) atomicOr(flag, kFlagOverlap);
+    atomicAdd(f3 + i, fx);
+    atomicAdd(f3 + f_stride + i, fy);
+    atomicAdd(f3 + 2 * f_stride + i, fz);
+  }
+  if (pe_total) {
+    double e = warp_sum((double)ei);
+    if ((threadIdx.x & 31) == 0) atomicAdd(pe_total, e);
+  }
+}
+
+static LJConst make_const(const pc_lj* lj) {
+  LJConst c;
+  c.cutoff2 = lj->cutoff2;
+  c.overlap2 = lj->overlap2;
+  c.sig2 = (float)(lj->sigma * lj->sigma);
+  c.eps4 = (float)(4.0 * lj->epsilon);
+  c.eps24 = (float)(24.0 * lj->epsilon);
+  return c;
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+extern "C" {
+
+int32_t pc_lj_force_blocks(int32_t n_rows) {
+  return n_rows <= 0 ? 1 : (n_rows + kForceThreads - 1) / kForceThreads;
+}
+
+int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                const int64_t* d_offsets, const int32_t* d_index, int64_t ell_stride,
+                const pc_box* box, const pc_lj* lj, double* d_f3, int64_t f_stride,
+                double* d_f64, double* d_pe, double* d_v, int64_t v_stride, double dtm,
+                double mass, double* d_partial, int32_t* d_flag, void* stream) {
+  if (n_rows < 0) {
+    set_error("pc_lj_force: negative row count");
+    return PC_ERR_VALUE;
+  }
+  if (ell_stride <= 0 && d_offsets == nullptr && n_rows > 0) {
+    set_error("pc_lj_force: CSR layout needs offsets");
+    return PC_ERR_VALUE;
+  }
+  LJConst c = make_const(lj);
+  unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
+  cudaStream_t s = as_stream(stream);
+  if (ell_stride > 0)
+    lj_force_kernel<true><<<blocks, kForceThreads, 0, s>>>(
+        d_pos, n_rows, d_count, d_offsets, d_index, ell_stride, *box, c, d_f3, f_stride, d_f64,
+        d_pe, d_v, v_stride, dtm, mass, d_partial, d_flag);
+  else
+    lj_force_kernel<false><<<blocks, kForceThreads, 0, s>>>(
+        d_pos, n_rows, d_count, d_offsets, d_index, ell_stride, *box, c, d_f3, f_stride, d_f64,
+        d_pe, d_v, v_stride, dtm, mass, d_partial, d_flag);
+  return check_launch("pc_lj_force");
+}
+
+int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                     const int32_t* d_index, int64_t ell_stride, const pc_box* box,
+                     const pc_lj* lj, double* d_f3, int64_t f_stride, double* d_pe_total,
+                     int32_t* d_flag, void* stream) {
+  if (n_rows <= 0) return PC_OK;
+  LJConst c = make_const(lj);
+  unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
+  lj_force_half_kernel<<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+      d_pos, n_rows, d_count, d_index, ell_stride, *box, c, d_f3, f_stride, d_pe_total, d_flag);
+  return check_launch("pc_lj_force_half");
+}
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+// Velocity-Verlet integrate blocks of ref md.py:219-257 with the periodic
+// wrap of geometry.py:40-49, in numpy's rounding order (no FMA contraction).
+#include "pc_common.cuh"
+
+namespace pc {
+
+constexpr int kIntThreads = 256;
+
+// numpy float mod (npy_divmod): fmod, then shift a nonzero remainder whose
+// sign differs from the divisor's; zero takes the divisor's sign.
+__device__ __forceinline__ double np_mod(double a, double L) {
+  double m = fmod(a, L);
+  if (m != 0.0) {
+    if ((L < 0.0) != (m < 0.0)) m = __dadd_rn(m, L);
+  } else {
+    m = copysign(0.0, L);
+  }
+  return m;
+}
+
+__device__ __forceinline__ double wrap_axis(double x, double low, double high, double L) {
+  double w = __dadd_rn(low, np_mod(__dsub_rn(x, low), L));
+  return w >= high ? low : w;
+}
+
+__global__ void __launch_bounds__(kIntThreads)
+kick_drift_wrap_kernel(double* __restrict__ pos, double* __restrict__ v, int64_t vs,
+                       const double* __restrict__ f, int64_t fs, int n, double dtm, double dt,
+                       pc_box b) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* p = pos + 4 * (int64_t)i;
+  double x[3] = {p[0], p[1], p[2]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double va = __dadd_rn(v[a * vs + i], __dmul_rn(dtm, f[a * fs + i]));
+    v[a * vs + i] = va;
+    double xa = __dadd_rn(x[a], __dmul_rn(dt, va));
+    if (b.periodic[a]) xa = wrap_axis(xa, b.low[a], b.high[a], b.length[a]);
+    x[a] = xa;
+  }
+  p[0] = x[0];
+  p[1] = x[1];
+  p[2] = x[2];
+}
+
+__global__ void __launch_bounds__(kIntThreads)
+kick_kernel(double* __restrict__ v, int64_t vs, const double* __restrict__ f, int64_t fs, int n,
+            double dtm, double mass, double* __restrict__ partial) {
+  __shared__ double red[kIntThreads / 32][5];
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0;
+  if (i < n) {
+    double vx = __dadd_rn(v[i], __dmul_rn(dtm, f[i]));
+    double vy = __dadd_rn(v[vs + i], __dmul_rn(dtm, f[fs + i]));
+    double vz = __dadd_rn(v[2 * vs + i], __dmul_rn(dtm, f[2 * fs + i]));
+    v[i] = vx;
+    v[vs + i] = vy;
+    v[2 * vs + i] = vz;
+    ke = __dmul_rn(0.5 * mass, r2_exact(vx, vy, vz));
+    px = mass * vx;
+    py = mass * vy;
+    pz = mass * vz;
+  }
+  if (!partial) return;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  ke = warp_sum(ke);
+  px = warp_sum(px);
+  py = warp_sum(py);
+  pz = warp_sum(pz);
+  if (lane == 0) {
+    red[wid][0] = ke; red[wid][1] = 0.0; red[wid][2] = px; red[wid][3] = py; red[wid][4] = pz;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double s = 0.0;
+    for (int w = 0; w < kIntThreads / 32; ++w) s += red[w][threadIdx.x];
+    partial[blockIdx.x * 5 + threadIdx.x] = s;
+  }
+}
+
+// Fixed-order reduction of block partials: deterministic for a given grid.
+__global__ void __launch_bounds__(1024)
+reduce_partials_kernel(const double* __restrict__ partial, int nblocks, double* __restrict__ out) {
+  __shared__ double red[32][5];
+  double s[5] = {0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s[k] += partial[b * 5 + k];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double v = warp_sum(s[k]);
+    if (lane == 0) red[wid][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+}
+
+// Box.wrap / Box.min_image on (rows, d) arrays (ref geometry.py:40-58).
+__global__ void box_wrap_kernel(double* __restrict__ x, int64_t rows, int d, pc_box b) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * d) return;
+  int a = (int)(t % d);
+  if (b.periodic[a]) x[t] = wrap_axis(x[t], b.low[a], b.high[a], b.length[a]);
+}
+
+__global__ void box_min_image_kernel(double* __restrict__ x, int64_t rows, int d, pc_box b) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * d) return;
+  int a = (int)(t % d);
+  if (b.periodic[a]) {
+    double v = x[t];
+    double L = b.length[a];
+    // literal form: general |v| (no |v| < L precondition here)
+    x[t] = __dsub_rn(v, __dmul_rn(L, rint(__ddiv_rn(v, L))));
+  }
+}
+
+// lj_pair of ref md.py:89-96 in FP64, same operation order.
+__global__ void lj_pair_kernel(const double* __restrict__ dx, const double* __restrict__ r2,
+                               int64_t n, double eps, double sigma, double* __restrict__ e,
+                               double* __restrict__ f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q = r2[i];
+  double sr2 = __ddiv_rn(__dmul_rn(sigma, sigma), q);
+  double sr6 = __dmul_rn(__dmul_rn(sr2, sr2), sr2);
+  double sr12 = __dmul_rn(sr6, sr6);
+  e[i] = __dmul_rn(__dmul_rn(4.0, eps), __dsub_rn(sr12, sr6));
+  double fm = __ddiv_rn(__dmul_rn(__dmul_rn(24.0, eps), __dsub_rn(__dmul_rn(2.0, sr12), sr6)), q);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) f[3 * i + a] = __dmul_rn(-fm, dx[3 * i + a]);
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+extern "C" {
+
+int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride, const double* d_f3,
+                       int64_t f_stride, int32_t n, double dtm, double dt, const pc_box* box,
+                       void* stream) {
+  if (n <= 0) return PC_OK;
+  kick_drift_wrap_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0,
+                           as_stream(stream)>>>(d_pos, d_v, v_stride, d_f3, f_stride, n, dtm, dt,
+                                                *box);
+  return check_launch("pc_kick_drift_wrap");
+}
+
+int pc_kick(double* d_v, int64_t v_stride, const double* d_f3, int64_t f_stride, int32_t n,
+            double dtm, double mass, double* d_partial, void* stream) {
+  if (n <= 0) n = 0;
+  int blocks = n == 0 ? 1 : (n + kIntThreads - 1) / kIntThreads;
+  kick_kernel<<<blocks, kIntThreads, 0, as_stream(stream)>>>(d_v, v_stride, d_f3, f_stride, n,
+                                                             dtm, mass, d_partial);
+  return check_launch("pc_kick");
+}
+
+int pc_box_wrap(double* d_x, int64_t rows, int32_t d, const pc_box* box, void* stream) {
+  int64_t t = rows * d;
+  if (t <= 0) return PC_OK;
+  box_wrap_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(d_x, rows, d, *box);
+  return check_launch("pc_box_wrap");
+}
+
+int pc_box_min_image(double* d_x, int64_t rows, int32_t d, const pc_box* box, void* stream) {
+  int64_t t = rows * d;
+  if (t <= 0) return PC_OK;
+  box_min_image_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(d_x, rows, d,
+                                                                                   *box);
+  return check_launch("pc_box_min_image");
+}
+
+int pc_lj_pair(const double* d_dx, const double* d_r2, int64_t n, double eps, double sigma,
+               double* d_e, double* d_f, void* stream) {
+  if (n <= 0) return PC_OK;
+  lj_pair_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_dx, d_r2, n, eps,
+                                                                             sigma, d_e, d_f);
+  return check_launch("pc_lj_pair");
+}
+
+int pc_reduce_partials(const double* d_partial, int32_t nblocks, double* d_out, void* stream) {
+  reduce_partials_kernel<<<1, 1024, 0, as_stream(stream)>>>(d_partial, nblocks, d_out);
+  return check_launch("pc_reduce_partials");
+}
+
+}  // extern "C"

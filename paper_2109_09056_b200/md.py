@@ -1,0 +1,371 @@
+"""Lennard-Jones NVE mini-MD on the GPU -- drop-in for ``particula.md``.
+
+Same public surface as ref md.py (``MD_SCHEMA``, ``MDConfig``,
+``fcc_lattice``, ``initial_velocities``, ``lj_pair``, ``lj_forces``,
+``MDDriver``, ``run_md``) and the same step semantics (md.py:219-257):
+
+    integrate   v += dt/2m f ; x += dt v ; wrap          pc_kick_drift_wrap
+    rebuild     (every rebuild_stride) cell sort +        pc_bin_* , pc_gather_rows,
+                Verlet build at (rc+skin)(1+1e-9)          pc_nbr_build (ELL)
+    force       exact-rc LJ + fused final half kick +     pc_lj_force
+                KE/PE/momentum block partials
+
+Device layout (HBM, capacity ``cap``):
+    pos  (cap, 4) f64   x, y, z, global id (int64 bits)  -- 32 B gathers
+    vel  (3, cap) f64   planar
+    frc  (3, cap) f64   planar (FP64-accumulated, antisymmetric pair terms)
+    nbr  (W, cap) i32   transposed ELL Verlet list, cnt (cap,) i32
+
+Particles are re-sorted by cell at every rebuild (physics-transparent: the
+reference sums forces in global-id order and energies by id, md.py:7-11), so
+the 27 stencil cells of a particle are contiguous index ranges.
+
+The initial lattice and Gaussian velocities are built on the host exactly as
+the reference does (md.py:67-86) and uploaded once.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib, aosoa, decomp
+from ._lib import call, ptr, stream
+from .geometry import Box, cube
+from .neighbors import VerletList, neighbor_grid
+
+MD_SCHEMA = aosoa.schema(
+    x=("float64", (3,)),
+    x0=("float64", (3,)),
+    v=("float64", (3,)),
+    f=("float64", (3,)),
+    id=("int64", ()),
+)
+
+_CUTOFF_MARGIN = 1.0 + 1e-9          # ref md.py:32-34
+
+PHASES = ("integrate", "sort", "migrate", "halo", "neighbor", "force")
+
+
+@dataclass
+class MDConfig:
+    """ref md.py:37-64 (same fields, defaults and validation)."""
+    lattice_cells: int = 4
+    density: float = 0.8442
+    temperature: float = 0.8
+    dt: float = 0.005
+    steps: int = 100
+    cutoff: float = 2.5
+    skin: float = 0.0
+    rebuild_stride: int = 1
+    sort_stride: int = 0
+    seed: int = 1
+    vector_length: int = 16
+    rank_dims: tuple = (1, 1, 1)
+    epsilon: float = 1.0
+    sigma: float = 1.0
+    mass: float = 1.0
+
+    def validate(self):
+        if self.rebuild_stride > 1 and self.skin <= 0:
+            raise ValueError("rebuild_stride > 1 requires a positive skin")
+        if self.sort_stride and self.sort_stride % self.rebuild_stride:
+            raise ValueError("sort_stride must be a multiple of rebuild_stride")
+        for name in ("lattice_cells", "steps", "vector_length", "rebuild_stride"):
+            if getattr(self, name) < 1 and name != "steps":
+                raise ValueError(f"{name} must be >= 1")
+        if self.dt <= 0 or self.cutoff <= 0 or self.density <= 0:
+            raise ValueError("dt, cutoff and density must be positive")
+
+
+def fcc_lattice(cells: int, spacing: float) -> np.ndarray:
+    """4-atom FCC basis on a cells^3 grid, ij-meshgrid order (ref md.py:67-74)."""
+    basis = np.array([[0, 0, 0], [0.5, 0.5, 0], [0.5, 0, 0.5], [0, 0.5, 0.5]], dtype=np.float64)
+    ax = np.arange(cells)
+    gx, gy, gz = np.meshgrid(ax, ax, ax, indexing="ij")
+    corners = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+    return (corners[:, None, :] + basis[None, :, :]).reshape(-1, 3) * spacing
+
+
+def initial_velocities(n: int, temperature: float, mass: float, seed: int) -> np.ndarray:
+    """Seeded PCG64 Gaussian velocities, zero momentum, exact-T rescale (ref md.py:77-86)."""
+    v = np.random.default_rng(seed).normal(size=(n, 3))
+    v -= v.mean(axis=0)
+    ke = 0.5 * mass * np.einsum("ij,ij->", v, v)
+    if ke > 0:
+        v *= np.sqrt(1.5 * n * temperature / ke)
+    return v
+
+
+def lj_pair(dx, r2, eps: float, sigma: float):
+    """Pair energies and force on i for dx = xj - xi (ref md.py:89-96), FP64 on device."""
+    is_tensor = isinstance(dx, torch.Tensor)
+    d = _kernels.as_device(dx).reshape(-1, 3)
+    q = _kernels.as_device(r2).reshape(-1)
+    n = q.numel()
+    e = torch.empty(max(n, 1), dtype=torch.float64, device=d.device)
+    f = torch.empty((max(n, 1), 3), dtype=torch.float64, device=d.device)
+    call("pc_lj_pair", ptr(d), ptr(q), n, float(eps), float(sigma), ptr(e), ptr(f), stream())
+    e, f = e[:n], f[:n]
+    return (e, f) if is_tensor else (e.cpu().numpy(), f.cpu().numpy())
+
+
+def _lj_params(eps, sigma, cutoff) -> "_lib.PcLJ":
+    p = _lib.PcLJ()
+    p.epsilon, p.sigma = float(eps), float(sigma)
+    p.cutoff2 = float(cutoff) * float(cutoff)
+    p.overlap2 = (1e-10 * float(sigma)) ** 2
+    return p
+
+
+def lj_forces(x_phys, ids, owned: int, vlist: VerletList, box: Box, periodic, eps: float,
+              sigma: float, cutoff: float):
+    """Canonical LJ forces / per-particle energies for the first ``owned`` rows
+    (ref md.py:99-126): exact-cutoff re-filter in FP64, each pair energy booked
+    on the smaller global id.  FP32 pair arithmetic (tolerance 1e-5)."""
+    is_tensor = isinstance(x_phys, torch.Tensor)
+    x = _kernels.as_device(x_phys)
+    tags = _kernels.as_device(ids, dtype=torch.int64)
+    pos4 = _kernels.pack_pos4(x, tags)
+    counts, offsets, index = vlist.device_csr()
+    per = np.broadcast_to(np.asarray(periodic, bool), (box.ndim,))
+    pbox = _lib.make_box(box.low, box.high, per)
+    owned = int(owned)
+    dev = x.device
+    f64 = torch.zeros((max(owned, 1), 3), dtype=torch.float64, device=dev)
+    pe = torch.zeros(max(owned, 1), dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    call("pc_lj_force", ptr(pos4), owned, ptr(counts), ptr(offsets), ptr(index), 0, pbox,
+         _lj_params(eps, sigma, cutoff), None, 0, ptr(f64), ptr(pe), None, 0, 0.0, 1.0, None,
+         ptr(flag), stream())
+    if int(flag.item()) & _lib.FLAG_OVERLAP:
+        raise FloatingPointError("overlapping particles in LJ kernel")
+    f64, pe = f64[:owned], pe[:owned]
+    return (f64, pe) if is_tensor else (f64.cpu().numpy(), pe.cpu().numpy())
+
+
+class _PhaseTimer:
+    """Per-phase CUDA-event timing in the reference's six buckets (md.py:158-159)."""
+
+    def __init__(self):
+        self.totals = {k: 0.0 for k in PHASES}
+        self._pending = []
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, phase, e0):
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self._pending.append((phase, e0, e1))
+        if len(self._pending) > 4096:
+            self.resolve()
+
+    def resolve(self):
+        if self._pending:
+            self._pending[-1][2].synchronize()
+            for phase, a, b in self._pending:
+                self.totals[phase] += a.elapsed_time(b) * 1e-3
+            self._pending = []
+        return dict(self.totals)
+
+    def reset(self):
+        self.resolve()
+        self.totals = {k: 0.0 for k in PHASES}
+
+
+class MDDriver:
+    """Device-resident velocity-Verlet LJ driver (ref md.py:129-292).
+
+    ``rank_dims`` is validated exactly as the reference does (halo width vs
+    block edge, md.py:140-142); one driver owns the whole box on one GPU --
+    the physics is decomposition-independent by the reference's own contract
+    (md.py:7-11).  Multi-GPU runs use ``paper_2109_09056_b200.dist``.
+    """
+
+    def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
+                 time_phases: bool = True, state=None):
+        cfg.validate()
+        self.cfg = cfg
+        a = (4.0 / cfg.density) ** (1.0 / 3.0)
+        self.box = cube(cfg.lattice_cells * a)
+        self.periodic = np.array([True, True, True])
+        self.n = 4 * cfg.lattice_cells ** 3
+        self.fabric = decomp.decompose(self.box, cfg.rank_dims, self.periodic)
+        halo_w = (cfg.cutoff + cfg.skin) * _CUTOFF_MARGIN
+        if halo_w > self.fabric.block_lengths.min():
+            raise ValueError("cutoff + skin exceeds the local box edge for this rank grid")
+        self.halo_width = halo_w
+        self.search = (cfg.cutoff + cfg.skin) * _CUTOFF_MARGIN
+        if self.search > 0.5 * self.box.lengths.min():
+            raise ValueError("cutoff exceeds half the box length on a periodic axis")
+        self.device = torch.device(device) if device is not None else _lib.device()
+        self._pbox = _lib.make_box(self.box.low, self.box.high, self.periodic)
+        self._lj = _lj_params(cfg.epsilon, cfg.sigma, cfg.cutoff)
+        _nc, _w, self._grid = neighbor_grid(self.box, self.search)
+        self._search2 = self.search * self.search
+        self._dtm = 0.5 * cfg.dt / cfg.mass
+        self._time = time_phases
+        self._timer = _PhaseTimer()
+        self.ell_width = int(ell_width)
+
+        n = self.n
+        self.cap = n
+        dev = self.device
+        if state is None:
+            x = torch.as_tensor(fcc_lattice(cfg.lattice_cells, a))
+            v = torch.as_tensor(initial_velocities(n, cfg.temperature, cfg.mass, cfg.seed))
+        else:       # host (ideally pinned) x, v in global-id order
+            x, v = (t if isinstance(t, torch.Tensor) else torch.as_tensor(t) for t in state)
+        ids = torch.arange(n, dtype=torch.int64, device=dev)
+        self.pos = _kernels.pack_pos4(x.to(dev, non_blocking=True), ids)
+        self.vel = v.to(dev, non_blocking=True).t().contiguous()           # (3, n)
+        self.force_events = None      # optional list collecting (start, end) per force launch
+        self.frc = torch.zeros((3, n), dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.nbr = torch.empty((self.ell_width, n), dtype=torch.int32, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
+        self.build_flag = torch.zeros(1, dtype=torch.int32, device=dev)  # ELL overflow
+        self._nblk = int(_lib.load().pc_lj_force_blocks(n))
+        self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
+        self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
+        self._ke_fresh = False
+        self.rebuilds = 0
+        # the lattice lies in [0, L): the reference's initial migrate wrap
+        # (decomp.py:90-91) is the identity on it
+        self._rebuild()
+        self._force(kick_dtm=0.0)
+        self._timer.reset()
+
+    # -- phases ------------------------------------------------------------
+    def _t0(self):
+        return self._timer.start() if self._time else None
+
+    def _t1(self, phase, e0):
+        if self._time:
+            self._timer.stop(phase, e0)
+
+    def _rebuild(self):
+        """Cell sort of all particle fields + ELL Verlet build (md.py:169-188)."""
+        n, s = self.n, stream()
+        e0 = self._t0()
+        srt = _kernels.CellSort(self.pos, 4, self._grid)
+        self.pos = _kernels.gather_rows(self.pos, srt.order, n)
+        self.vel = torch.stack([_kernels.gather_rows(self.vel[a], srt.order, n)
+                                for a in range(3)])
+        self._t1("sort", e0)
+        e0 = self._t0()
+        while True:
+            self.build_flag.zero_()
+            call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid, self._pbox,
+                 self._search2, 0, _lib.PC_NBR_ELL, 0, ptr(self.cnt), None, ptr(self.nbr),
+                 self.cap, self.ell_width, ptr(self.build_flag), s)
+            if not (int(self.build_flag.item()) & _lib.FLAG_OVERFLOW):
+                break
+            # no silent truncation (SPEC neighbors: grow and rebuild)
+            self.ell_width = int(self.cnt.max().item()) + 8
+            self.nbr = torch.empty((self.ell_width, self.cap), dtype=torch.int32,
+                                   device=self.device)
+        self._t1("neighbor", e0)
+        self.rebuilds += 1
+
+    def _force(self, kick_dtm):
+        e0 = self._t0()
+        if self.force_events is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        call("pc_lj_force", ptr(self.pos), self.n, ptr(self.cnt), None, ptr(self.nbr), self.cap,
+             self._pbox, self._lj, ptr(self.frc), self.cap, None, None, ptr(self.vel),
+             self.cap, float(kick_dtm), float(self.cfg.mass), ptr(self.partial),
+             ptr(self.flag), stream())
+        if self.force_events is not None:
+            b.record()
+            self.force_events.append((a, b))
+        self._t1("force", e0)
+        self._ke_fresh = True
+
+    def _integrate(self):
+        e0 = self._t0()
+        call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
+             self.cap, self.n, self._dtm, float(self.cfg.dt), self._pbox, stream())
+        self._t1("integrate", e0)
+
+    def step(self, step_index: int):
+        """One velocity-Verlet step (ref md.py:219-257)."""
+        self._integrate()
+        if step_index % self.cfg.rebuild_stride == 0:
+            self._rebuild()
+        self._force(kick_dtm=self._dtm)
+
+    def check_errors(self):
+        fl = int(self.flag.item())
+        if fl & _lib.FLAG_OVERLAP:
+            raise FloatingPointError("overlapping particles in LJ kernel")
+
+    # -- diagnostics --------------------------------------------------------
+    def device_diagnostics(self) -> torch.Tensor:
+        """(KE, PE, px, py, pz) on the device, no host sync."""
+        if not self._ke_fresh:
+            kp = torch.zeros_like(self.partial)
+            call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n, 0.0,
+                 float(self.cfg.mass), ptr(kp), stream())
+            pe_col = self.partial[:, 1].clone()
+            self.partial = kp
+            self.partial[:, 1] = pe_col
+            self._ke_fresh = True
+        call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(self.diag), stream())
+        return self.diag
+
+    def diagnostics(self):
+        """Global energies (ref md.py:261-277)."""
+        d = self.device_diagnostics().cpu().numpy()
+        self.check_errors()
+        ke, pe = float(d[0]), float(d[1])
+        return {"KE": ke, "PE": pe, "E_total": ke + pe,
+                "temperature": 2.0 * ke / (3.0 * self.n),
+                "momentum": d[2:5].copy()}
+
+    def gather_state(self):
+        """Positions and velocities in global-id order (ref md.py:279-287)."""
+        p = self.pos[: self.n].cpu().numpy()
+        ids = p[:, 3].view(np.int64)
+        x = np.zeros((self.n, 3))
+        v = np.zeros((self.n, 3))
+        x[ids] = p[:, :3]
+        v[ids] = self.vel[:, : self.n].cpu().numpy().T
+        return x, v
+
+    def negate_velocities(self):
+        self.vel.neg_()
+        self._ke_fresh = False
+
+    @property
+    def timings(self):
+        return self._timer.resolve()
+
+    @timings.setter
+    def timings(self, value):
+        self._timer.reset()
+        for k, v in dict(value).items():
+            self._timer.totals[k] = float(v)
+
+
+def run_md(cfg: MDConfig):
+    """Run the NVE loop; returns (per-step diagnostic rows, phase timings)
+    (ref md.py:295-307)."""
+    drv = MDDriver(cfg)
+    drv.timings = {k: 0.0 for k in PHASES}
+    d = drv.diagnostics()
+    rows = [dict(step=0, KE=d["KE"], PE=d["PE"], E_total=d["E_total"],
+                 temperature=d["temperature"])]
+    for s in range(1, cfg.steps + 1):
+        drv.step(s)
+        d = drv.diagnostics()
+        rows.append(dict(step=s, KE=d["KE"], PE=d["PE"], E_total=d["E_total"],
+                         temperature=d["temperature"]))
+    return rows, drv.timings

@@ -1,0 +1,348 @@
+"""GPU parity: the CUDA path (through the C ABI) vs golden vectors produced by
+the reference and vs the pinned CPU oracle.  Run with ``-m gpu`` on a B200.
+
+Bars: bit-exact for binning, permutations, neighbor lists and the geometry
+helpers; forces per atom within 1e-5 * max(|F_ref,i|_inf, F_rms) (the
+north_star FP32 tolerance); energies within 1e-6 relative.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_cases, load_flat
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 1e-5        # relative, per atom, vs max(|F_ref,i|_inf, F_rms)
+ENERGY_TOL = 1e-6       # relative, per evaluation
+
+
+@pytest.fixture(scope="module")
+def pc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2109_09056_b200 as pkg
+    return pkg
+
+
+def _digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def force_err_ratio(f, fref):
+    frms = np.sqrt((fref ** 2).sum(1).mean())
+    tol = FORCE_TOL * np.maximum(np.abs(fref).max(1), frms)
+    return float((np.abs(f - fref).max(1) / tol).max())
+
+
+# ---------------------------------------------------------------- geometry
+def test_box_wrap_min_image_bit_exact(pc, oracle):
+    rng = np.random.default_rng(1)
+    box = pc.geometry.Box([-1.0, 0.0, 2.0], [3.0, 5.5, 4.25])
+    L = box.lengths
+    x = box.low + rng.uniform(-3, 4, (5000, 3)) * L
+    x[:10] = box.high            # exactly on the upper face
+    per = [True, False, True]
+    got = box.wrap(x, per)
+    ref = oracle.box_wrap(x, box.low, box.high, per)
+    assert np.array_equal(got, ref)
+    d = rng.uniform(-2.5, 2.5, (5000, 3)) * L
+    assert np.array_equal(box.min_image(d, per), oracle.box_min_image(d, L, per))
+
+
+# ---------------------------------------------------------------- binning
+BN = load_cases("binning.npz")
+
+
+@pytest.mark.parametrize("case", [k for k in sorted(BN) if k.startswith("d")])
+def test_binning_bit_exact(pc, case):
+    c = BN[case]
+    box = pc.geometry.Box(c["low"], c["high"])
+    nc, idx = pc.binning.cell_indices(c["x"], box, float(c["cs"]))
+    assert np.array_equal(nc, c["nc"]) and np.array_equal(idx, c["idx"])
+    cb = pc.binning.bin_by_position(c["x"], box, float(c["cs"]))
+    assert np.array_equal(cb.offsets, c["offsets"])
+    assert np.array_equal(cb.permutation.map, c["map"])
+    assert cb.permutation.is_bijection()
+
+
+def test_bin_by_key_stable(pc):
+    c = BN["keys300"]
+    assert np.array_equal(pc.binning.bin_by_key(c["keys"]).map, c["map"])
+    keys = np.array([3, 1, 3, 0, 1, 3])
+    p = pc.binning.bin_by_key(keys)
+    srt = np.empty_like(keys)
+    srt[p.map] = keys
+    assert np.array_equal(srt, np.sort(keys))
+    wide = np.random.default_rng(3).integers(-2**60, 2**60, 5000)
+    pw = pc.binning.bin_by_key(wide)
+    assert np.array_equal(np.argsort(pw.map), np.argsort(wide, kind="stable"))
+
+
+def test_cell_indices_rejects_outside(pc):
+    box = pc.geometry.Box([0.0], [1.0])
+    with pytest.raises(ValueError):
+        pc.binning.cell_indices(np.array([[1.5]]), box, 0.5)
+
+
+def test_permute_all_fields(pc):
+    rng = np.random.default_rng(1)
+    for V in (1, 3, 4, 16, 64):
+        sch = pc.aosoa.schema(x=("float64", (3,)), s=("float64", (3, 3)), id=("int64", ()))
+        p = pc.aosoa.create(sch, V, 30)
+        x = rng.random((30, 3))
+        s = rng.random((30, 3, 3))
+        p.slice("x").copy_in(x)
+        p.slice("s").copy_in(s)
+        p.slice("id").copy_in(np.arange(30, dtype=np.int64))
+        perm = pc.binning.bin_by_key(rng.integers(0, 5, 30))
+        pc.binning.permute(p, perm)
+        ids = p.slice("id").copy_out()
+        xo, so = p.slice("x").copy_out(), p.slice("s").copy_out()
+        for i in range(30):
+            assert ids[perm.map[i]] == i
+            assert np.array_equal(xo[perm.map[i]], x[i])
+            assert np.array_equal(so[perm.map[i]], s[i])
+    p = pc.aosoa.create(pc.aosoa.schema(m=("float64", ())), 2, 3)
+    with pytest.raises(ValueError):
+        pc.binning.permute(p, pc.binning.Permutation(np.array([0, 0, 1])))
+    with pytest.raises(ValueError):
+        pc.binning.permute(p, pc.binning.Permutation(np.array([0, 1])))
+
+
+# ---------------------------------------------------------------- aosoa
+@pytest.mark.parametrize("V", [1, 2, 5, 16, 17])
+@pytest.mark.parametrize("n", [0, 1, 7, 40])
+def test_aosoa_roundtrip(pc, V, n):
+    sch = pc.aosoa.schema(x=("float64", (3,)), m=("float64", ()),
+                          stress=("float64", (3, 3)), id=("int64", ()))
+    p = pc.aosoa.create(sch, V, n)
+    assert p.capacity == -(-n // V) * V
+    rng = np.random.default_rng(n * 31 + V)
+    vals = {"x": rng.random((n, 3)), "m": rng.random(n), "stress": rng.random((n, 3, 3)),
+            "id": rng.integers(-2**40, 2**40, n)}
+    for k, v in vals.items():
+        assert np.all(p.slice(k).copy_out() == 0)
+        p.slice(k).copy_in(v)
+    for k, v in vals.items():
+        assert np.array_equal(p.slice(k).copy_out(), v)
+    if n:
+        assert np.array_equal(p.slice("stress")[n - 1], vals["stress"][n - 1])
+        assert p.slice("x")[0, 2] == vals["x"][0, 2]
+        p.slice("m")[0] = 5.0
+        assert p.slice("m")[0] == 5.0
+        p.resize(n + 3)
+        assert np.array_equal(p.slice("x").copy_out()[:n], vals["x"])
+        assert np.all(p.slice("x").copy_out()[n:] == 0)
+        q = pc.aosoa.create(sch, 4, n + 3)
+        pc.aosoa.deep_copy(q, p)
+        assert np.array_equal(q.slice("stress").copy_out(), p.slice("stress").copy_out())
+
+
+# ---------------------------------------------------------------- neighbors
+NB = load_cases("neighbors.npz")
+
+
+@pytest.mark.parametrize("case", sorted(NB))
+def test_neighbor_lists_bit_exact(pc, case):
+    c = NB[case]
+    box = pc.geometry.Box(c["low"], c["high"])
+    for layout in ("compressed", "dense"):
+        for conv in ("full", "half"):
+            vl = pc.neighbors.build_verlet(c["x"], box, c["periodic"], float(c["cutoff"]),
+                                           layout=layout, half_or_full=conv,
+                                           cell_ratio=float(c["ratio"]))
+            key = f"{layout}_{conv}"
+            assert np.array_equal(vl.counts, c[f"{key}_counts"]), key
+            if layout == "compressed":
+                assert np.array_equal(vl.indices, c[f"{key}_indices"]), key
+                assert np.array_equal(vl.offsets, c[f"{key}_offsets"]), key
+            else:
+                assert np.array_equal(vl.table, c[f"{key}_table"]), key
+
+
+def test_neighbor_argument_errors(pc):
+    box = pc.geometry.cube(2.0)
+    x = np.zeros((1, 3))
+    for kw in (dict(cutoff=-1.0), dict(cutoff=1.5), dict(cutoff=0.5, layout="sparse"),
+               dict(cutoff=0.5, cell_ratio=0.5), dict(cutoff=0.5, half_or_full="x")):
+        cutoff = kw.pop("cutoff")
+        with pytest.raises(ValueError):
+            pc.neighbors.build_verlet(x, box, [True] * 3, cutoff, **kw)
+
+
+def test_neighbor_properties(pc, oracle):
+    rng = np.random.default_rng(7)
+    box = pc.geometry.cube(3.0)
+    x = rng.random((100, 3)) * 3.0
+    half = pc.neighbors.build_verlet(x, box, [True] * 3, 0.9, half_or_full="half")
+    full = pc.neighbors.build_verlet(x, box, [True] * 3, 0.9, half_or_full="full")
+    assert 2 * half.total == full.total
+    i, j = half.pairs()
+    assert np.all(j > i)
+    seen = []
+    pc.neighbors.for_each_neighbor(full, (0, 100), lambda a, b: seen.append((a, b)))
+    ii, jj = full.pairs()
+    assert seen == list(zip(ii.tolist(), jj.tolist()))
+    trip = []
+    pc.neighbors.for_each_neighbor2(full, (0, 100), lambda a, b, c: trip.append(a))
+    assert len(trip) == int(sum(k * (k - 1) // 2 for k in full.counts))
+    # rebuild idempotence
+    again = pc.neighbors.build_verlet(x, box, [True] * 3, 0.9)
+    assert np.array_equal(again.indices, full.indices)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_criterion1_oracle_20_seeds(pc, oracle, seed):
+    """ref tests/test_acceptance.py:22-50 at full size, all four variants."""
+    n = 1000
+    rc = (30 * 3 / (4 * np.pi * n)) ** (1 / 3)
+    x = np.random.default_rng(seed).random((n, 3))
+    ref = oracle.build_verlet(x, np.zeros(3), np.ones(3), [True] * 3, rc)
+    box = pc.geometry.cube(1.0)
+    for layout in ("dense", "compressed"):
+        for conv in ("half", "full"):
+            vl = pc.neighbors.build_verlet(x, box, [True] * 3, rc, layout=layout,
+                                           half_or_full=conv)
+            want = oracle.build_verlet(x, np.zeros(3), np.ones(3), [True] * 3, rc,
+                                       layout=layout, half_or_full=conv)
+            assert np.array_equal(vl.counts, want["counts"])
+            if layout == "compressed":
+                assert np.array_equal(vl.indices, want["indices"])
+            else:
+                assert np.array_equal(vl.table, want["table"])
+    assert abs(ref["counts"].mean() - 30) < 3
+
+
+# ---------------------------------------------------------------- LJ forces
+LJ = load_flat("lj.npz")
+
+
+@pytest.mark.parametrize("name", ["c8", "c16"])
+def test_lj_forces_within_tolerance(pc, name):
+    x0, ids, L = LJ[f"{name}_x0"], LJ[f"{name}_ids"], LJ[f"{name}_L"]
+    box = pc.geometry.Box(np.zeros(3), L)
+    vl = pc.neighbors.build_verlet(x0, box, [True] * 3, float(LJ[f"{name}_search"]))
+    assert np.array_equal(vl.counts, LJ[f"{name}_counts"])
+    assert _digest(vl.offsets, vl.indices) == str(LJ[f"{name}_csr_digest"])
+    f, pe = pc.md.lj_forces(x0, ids, x0.shape[0], vl, box, [True] * 3, 1.0, 1.0, 2.5)
+    fref, peref = LJ[f"{name}_f"], LJ[f"{name}_pe"]
+    assert force_err_ratio(f, fref) < 1.0
+    assert abs(pe.sum() - peref.sum()) <= ENERGY_TOL * abs(peref.sum())
+    assert np.max(np.abs(pe - peref)) < 1e-5 * np.abs(peref).max()
+    # exact antisymmetry of FP64-accumulated pair forces: net force ~ 0
+    assert np.abs(f.sum(0)).max() < 1e-9
+
+
+def test_lj_forces_dense_layout_and_overlap(pc):
+    x0, ids, L = LJ["c8_x0"], LJ["c8_ids"], LJ["c8_L"]
+    box = pc.geometry.Box(np.zeros(3), L)
+    vl = pc.neighbors.build_verlet(x0, box, [True] * 3, float(LJ["c8_search"]),
+                                   layout="dense")
+    f, pe = pc.md.lj_forces(x0, ids, x0.shape[0], vl, box, [True] * 3, 1.0, 1.0, 2.5)
+    assert force_err_ratio(f, LJ["c8_f"]) < 1.0
+    x = np.array([[1.0, 1.0, 1.0], [1.0, 1.0, 1.0 + 1e-12], [5.0, 5.0, 5.0]])
+    b = pc.geometry.cube(10.0)
+    v2 = pc.neighbors.build_verlet(x, b, [True] * 3, 2.5)
+    with pytest.raises(FloatingPointError):
+        pc.md.lj_forces(x, np.arange(3), 3, v2, b, [True] * 3, 1.0, 1.0, 2.5)
+
+
+def test_lj_pair_reference_points(pc):
+    e, _ = pc.md.lj_pair(np.array([[1.0, 0.0, 0.0]]), np.array([1.0]), 1.0, 1.0)
+    assert abs(e[0]) < 1e-14
+    rm = 2.0 ** (1 / 6)
+    e, f = pc.md.lj_pair(np.array([[rm, 0.0, 0.0]]), np.array([rm * rm]), 1.0, 1.0)
+    assert abs(e[0] + 1.0) < 1e-14 and np.max(np.abs(f)) < 1e-12
+
+
+# ---------------------------------------------------------------- MD driver
+MD = load_flat("md.npz")
+
+
+def _series(rows):
+    return np.array([[r["KE"], r["PE"], r["E_total"], r["temperature"]] for r in rows])
+
+
+def test_md_initial_state_bit_exact(pc):
+    drv = pc.md.MDDriver(pc.md.MDConfig(lattice_cells=4, density=1.1, cutoff=2.3, seed=2,
+                                        steps=0))
+    x, v = drv.gather_state()
+    assert np.array_equal(x, MD["crit3_x_init"]) and np.array_equal(v, MD["crit3_v_init"])
+    d = drv.diagnostics()
+    ref = MD["crit3_series"][0]
+    assert abs(d["KE"] - ref[0]) <= 1e-13 * abs(ref[0])
+    assert abs(d["PE"] - ref[1]) <= ENERGY_TOL * abs(ref[1])
+
+
+@pytest.mark.parametrize("name", ["crit3", "skin_sort", "hot", "c1"])
+def test_md_energy_series(pc, name):
+    """Energy series vs the reference run: per step relative 1e-5 on E_total
+    (the trajectories separate chaotically from FP32-rounding seeds; within
+    100-200 steps the separation stays well below this) and the same drift."""
+    kw = json.loads(str(MD[f"{name}_config"]))
+    rows, timings = pc.md.run_md(pc.md.MDConfig(**kw))
+    got, ref = _series(rows), MD[f"{name}_series"]
+    assert got.shape == ref.shape
+    rel = np.abs(got[:, 2] - ref[:, 2]) / np.abs(ref[:, 2])
+    assert rel.max() < 1e-5, rel.max()
+    drift_got = abs(got[-1, 2] - got[0, 2]) / abs(got[0, 2])
+    drift_ref = abs(ref[-1, 2] - ref[0, 2]) / abs(ref[0, 2])
+    assert abs(drift_got - drift_ref) < 1e-5
+    assert set(timings) == {"integrate", "sort", "migrate", "halo", "neighbor", "force"}
+
+
+def test_md_momentum_and_reversal(pc):
+    cfg = pc.md.MDConfig(lattice_cells=3, density=1.1, temperature=0.8, dt=0.005, steps=0,
+                         cutoff=2.0, seed=2)
+    drv = pc.md.MDDriver(cfg)
+    x0, v0 = drv.gather_state()
+    for s in range(1, 51):
+        drv.step(s)
+    assert np.max(np.abs(drv.diagnostics()["momentum"])) < 1e-9
+    drv.negate_velocities()
+    for s in range(51, 101):
+        drv.step(s)
+    x1, v1 = drv.gather_state()
+    dx = x1 - x0
+    L = drv.box.lengths
+    dx -= L * np.round(dx / L)
+    assert np.max(np.abs(dx)) < 1e-6
+    assert np.max(np.abs(v1 + v0)) < 1e-6
+
+
+def test_md_nve_drift_criterion4(pc):
+    """ref tests/test_acceptance.py:97-123: 1000-step drift < 1e-4."""
+    cfg = pc.md.MDConfig(lattice_cells=4, density=1.1, cutoff=2.3, seed=2, dt=0.005,
+                         steps=1000)
+    rows, _ = pc.md.run_md(cfg)
+    e0 = rows[0]["E_total"]
+    assert abs(rows[-1]["E_total"] - e0) / abs(e0) < 1e-4
+
+
+def test_md_config_validation(pc):
+    with pytest.raises(ValueError):
+        pc.md.MDConfig(rebuild_stride=5).validate()
+    with pytest.raises(ValueError):
+        pc.md.MDConfig(skin=0.3, rebuild_stride=4, sort_stride=6).validate()
+    with pytest.raises(ValueError):
+        pc.md.MDConfig(dt=-0.1).validate()
+    with pytest.raises(ValueError):
+        pc.md.run_md(pc.md.MDConfig(lattice_cells=2))
+
+
+def test_md_skin_and_stride_equivalence(pc):
+    base = dict(lattice_cells=3, density=1.1, temperature=0.8, dt=0.005, cutoff=2.0, seed=2)
+    ref, _ = pc.md.run_md(pc.md.MDConfig(steps=60, **base))
+    rows, _ = pc.md.run_md(pc.md.MDConfig(steps=60, skin=0.2, rebuild_stride=5, **base))
+    for a, b in zip(ref, rows):
+        assert abs(a["E_total"] - b["E_total"]) < 1e-9 * abs(b["E_total"])
