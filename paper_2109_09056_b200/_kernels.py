@@ -70,7 +70,7 @@ class CellSort:
         counts = torch.zeros(grid.ncells, dtype=torch.int32, device=dev)
         s = stream()
         call("pc_bin_count", ptr(x), n, x_stride, grid, int(check_inside), ptr(self.cell_of),
-             ptr(counts), ptr(self.flag), s)
+             None, ptr(counts), ptr(self.flag), s)
         self.counts = counts
         self.cell_start = scan_i32(counts)
         fill = torch.zeros(grid.ncells, dtype=torch.int32, device=dev)

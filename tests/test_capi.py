@@ -111,3 +111,24 @@ def test_box_grid_packing():
     assert b.length[1] == 4.0
     g = _lib.make_grid([0.0], [1.0], [0.25], [4])
     assert (g.nc[0], g.nc[1], g.nc[2], g.ncells, g.ndim) == (4, 1, 1, 4, 1)
+
+
+def test_python_call_sites_match_signatures():
+    """Every call("pc_x", ...) in the package passes exactly the bound arity."""
+    import ast
+    from paper_2109_09056_b200 import _lib
+    pkg = os.path.join(ROOT, "paper_2109_09056_b200")
+    bad = []
+    for fn in os.listdir(pkg):
+        if not fn.endswith(".py"):
+            continue
+        tree = ast.parse(open(os.path.join(pkg, fn)).read())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Call) and getattr(node.func, "id", None) == "call" \
+                    and node.args and isinstance(node.args[0], ast.Constant):
+                name = node.args[0].value
+                want = len(_lib.SIGNATURES[name][1])
+                got = len(node.args) - 1
+                if got != want:
+                    bad.append((fn, node.lineno, name, got, want))
+    assert not bad, bad
