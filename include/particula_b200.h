@@ -154,12 +154,28 @@ int pc_invert_order(const int32_t* d_order, int64_t n, int64_t* d_map,
 #define PC_NBR_COUNT 0
 #define PC_NBR_CSR 1
 #define PC_NBR_ELL 2
+#define PC_NBR_SELL 3   /* SELL-32x4: ell_width = entries/row (mult. of 4),
+                           ell_stride = dummy row index used for padding */
 int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_start,
                  const pc_grid* grid, const pc_box* box, double cutoff2,
                  int32_t half, int32_t mode, int32_t out_tags,
                  int32_t* d_count, const int64_t* d_offsets, int32_t* d_index,
                  int64_t ell_stride, int32_t ell_width, int32_t* d_flag,
                  void* stream);
+
+/* MD hot-path build into the SELL-32x4 layout the force kernel reads: entry
+ * k of row a at int word ((a>>5)*(width/4) + k/4)*128 + (a&31)*4 + k%4,
+ * partial quads padded with `dummy` (a row whose position is NaN).  Uses the
+ * shared-memory staged kernel (FP32 prefilter with a bounded band, exact FP64
+ * predicate inside it: bit-identical sets) when every periodic axis has >= 3
+ * cells, else the per-particle kernel.  d_flag bit 1: a row exceeded width
+ * (counts exact, caller grows and rebuilds); bit 4: staging capacity
+ * exceeded (caller rebuilds with pc_nbr_build).  *h_used_staged reports the
+ * kernel chosen. */
+int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_start,
+                      const pc_grid* grid, const pc_box* box, double cutoff2,
+                      int32_t width, int32_t dummy, int32_t* d_count, int32_t* d_index,
+                      int32_t* d_flag, int32_t* h_used_staged, void* stream);
 
 /* CSR -> dense (n, width) int64 table, -1 padded (ref neighbors.py:130-134). */
 int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,
@@ -191,6 +207,20 @@ int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,
                 double* d_v, int64_t v_stride, double dtm, double mass,
                 double* d_partial, int32_t* d_flag, void* stream);
 int32_t pc_lj_force_blocks(int32_t n_rows);
+
+/* MD hot-path force over the SELL-32x4 list of pc_nbr_build_sell: per row one
+ * 128-bit index load per 4 neighbors (software-pipelined) and 4 independent
+ * 256-bit pos4 gathers in flight.  Minimum image is applied only on axes where
+ * the row particle lies within `mi_guard` of a periodic face: for a Verlet
+ * list whose pairs stay closer than mi_guard this is bit-identical to applying
+ * it everywhere (pass +inf to always apply it).  FP64 force accumulation,
+ * fused final half kick (d_v may be NULL), per-block partials (KE after kick,
+ * PE with each pair booked half on either side, px, py, pz). */
+int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                     const int32_t* d_index, int32_t width, const pc_box* box,
+                     const pc_lj* lj, double mi_guard, double* d_f3, int64_t f_stride,
+                     double* d_v, int64_t v_stride, double dtm, double mass,
+                     double* d_partial, int32_t* d_flag, void* stream);
 
 /* Half-list Newton-3 variant: rows hold j > i only; f_j -= F via FP32
  * atomics (not bitwise deterministic).  d_f3 must be zeroed by the caller. */

@@ -88,9 +88,9 @@ class CellSort:
         return m[:self.n]
 
 
-def gather_rows(src, order, n):
-    """dst[k] = src[order[k]] row-wise (any contiguous row layout)."""
-    dst = torch.empty_like(src)
+def gather_rows(src, order, n, out=None):
+    """dst[k] = src[order[k]] for k < n, row-wise (any contiguous row layout)."""
+    dst = torch.empty_like(src) if out is None else out
     row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
     call("pc_gather_rows", ptr(src), ptr(dst), ptr(order), n, row_bytes, stream())
     return dst

@@ -30,6 +30,8 @@ FLAG_OUTSIDE = 1
 FLAG_OVERFLOW = 2
 FLAG_OVERLAP = 4
 FLAG_NONPERIODIC = 8
+FLAG_STAGE = 16
+PC_NBR_SELL = 3
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
@@ -79,6 +81,12 @@ SIGNATURES = {
                                     ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_sort_rows": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
+    "pc_nbr_build_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
+                                         ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_vp,
+                                         c_vp, c_vp, ctypes.POINTER(c_i32), c_vp]),
+    "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, ctypes.POINTER(PcBox),
+                                        ctypes.POINTER(PcLJ), c_dbl, c_vp, c_i64, c_vp, c_i64,
+                                        c_dbl, c_dbl, c_vp, c_vp, c_vp]),
     "pc_lj_force": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i64,
                                    ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_vp, c_i64,
                                    c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),

@@ -24,6 +24,7 @@ constexpr int kFlagOutside = 1;   // ValueError: position outside box
 constexpr int kFlagOverflow = 2;  // neighbor row exceeded ELL width
 constexpr int kFlagOverlap = 4;   // FloatingPointError: r^2 < overlap^2
 constexpr int kFlagNonPeriodic = 8;
+constexpr int kFlagStage = 16;     // staged build: neighborhood exceeded smem
 
 // ---- device helpers ------------------------------------------------------
 // 256-bit read-only gather of one pos4 (x, y, z, tag): one DRAM sector.
@@ -89,6 +90,42 @@ __device__ __forceinline__ int axis_stencil(int c, int nc, int periodic, int out
     out[j + 1] = v;
   }
   return k;
+}
+
+// SELL-32x4 neighbor layout: rows grouped in slices of 32 consecutive rows;
+// each slice owns Q quads; entry k of row a lives at int word
+//   ((a>>5)*Q + (k>>2))*128 + (a&31)*4 + (k&3)
+// so one 128-bit load returns 4 consecutive neighbors of one row and a warp's
+// load of quad q is 512 contiguous bytes.
+__device__ __forceinline__ int64_t sell_word(int a, int k, int Q) {
+  return ((int64_t)(a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3);
+}
+
+// FP64 -> FP32 by truncation through the bit pattern (integer pipe, no F2F);
+// valid for finite values in the FP32 normal range (r^2 of interacting pairs).
+__device__ __forceinline__ float d2f_bits(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v);
+  const unsigned lo = (unsigned)__double2loint(v);
+  const unsigned e = (hi >> 20) & 0x7FFu;
+  const unsigned f = (hi & 0x80000000u) | ((e - 896u) << 23) | ((hi & 0xFFFFFu) << 3) | (lo >> 29);
+  return __uint_as_float(f);
+}
+
+// FP32 -> FP64 exactly through the bit pattern (normal numbers and zero).
+__device__ __forceinline__ double f2d_bits(float v) {
+  const unsigned b = __float_as_uint(v);
+  const unsigned mag = b & 0x7FFFFFFFu;
+  const unsigned hi = mag ? ((b & 0x80000000u) | (((mag >> 23) + 896u) << 20) |
+                             ((b & 0x7FFFFFu) >> 3))
+                          : (b & 0x80000000u);
+  const unsigned lo = b << 29;
+  return __hiloint2double((int)hi, (int)lo);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

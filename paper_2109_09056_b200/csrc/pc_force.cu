@@ -18,7 +18,7 @@ constexpr int kForceThreads = 256;
 
 struct LJConst {
   double cutoff2, overlap2;
-  float sig2, eps4, eps24;
+  float sig2, eps4, eps2, eps24;
 };
 
 __device__ __forceinline__ void block_partials(double v0, double v1, double v2, double v3,
@@ -160,12 +160,117 @@ lj_force_half_kernel(const double* __restrict__ pos, int n_rows, const int* __re
   }
 }
 
+// ---- MD hot path: SELL-32x4 list ------------------------------------------
+// One pair: FP64 displacement (minimum image only where the row particle is
+// near a periodic face, see pc_lj_force_sell), exact FP64 cutoff test, FP32
+// LJ magnitude with bit-pattern conversions (integer pipe, no F2F), FP64
+// accumulation; energy booked half on each side of the pair.
+template <bool MI>
+__device__ __forceinline__ void sell_pair(const double4& pj, const double4& pi, bool nx, bool ny,
+                                          bool nz, const pc_box& b, const LJConst& c, double& fx,
+                                          double& fy, double& fz, double& pe, bool& overlap) {
+  double dx = __dsub_rn(pj.x, pi.x);
+  double dy = __dsub_rn(pj.y, pi.y);
+  double dz = __dsub_rn(pj.z, pi.z);
+  if (MI) {
+    if (nx) dx = min_image(dx, b.length[0], b.mi_thresh[0]);
+    if (ny) dy = min_image(dy, b.length[1], b.mi_thresh[1]);
+    if (nz) dz = min_image(dz, b.length[2], b.mi_thresh[2]);
+  }
+  const double r2 = r2_exact(dx, dy, dz);
+  if (r2 < c.cutoff2) {
+    overlap |= (r2 < c.overlap2);
+    const float inv = rcp_approx(d2f_bits(r2));
+    const float sr2 = c.sig2 * inv;
+    const float sr6 = sr2 * sr2 * sr2;
+    const double fm = f2d_bits(c.eps24 * sr6 * (2.f * sr6 - 1.f) * inv);
+    fx = fma(-fm, dx, fx);
+    fy = fma(-fm, dy, fy);
+    fz = fma(-fm, dz, fz);
+    pe += f2d_bits(c.eps2 * sr6 * (sr6 - 1.f));
+  }
+}
+
+template <bool MI>
+__device__ __forceinline__ void sell_row(const double* __restrict__ pos,
+                                         const int4* __restrict__ row, int mq, int qmax,
+                                         const double4& pi, bool nx, bool ny, bool nz,
+                                         const pc_box& b, const LJConst& c, double& fx,
+                                         double& fy, double& fz, double& pe, bool& overlap) {
+  int4 nxt = make_int4(0, 0, 0, 0);
+  if (mq > 0) nxt = __ldg(row);
+  for (int q = 0; q < qmax; ++q) {
+    const int4 cur = nxt;
+    if (q + 1 < mq) nxt = __ldg(row + (int64_t)(q + 1) * 32);
+    if (q < mq) {
+      const double4 p0 = ld_pos4(pos + 4 * (int64_t)cur.x);
+      const double4 p1 = ld_pos4(pos + 4 * (int64_t)cur.y);
+      const double4 p2 = ld_pos4(pos + 4 * (int64_t)cur.z);
+      const double4 p3 = ld_pos4(pos + 4 * (int64_t)cur.w);
+      sell_pair<MI>(p0, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(p1, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(p2, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(p3, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kForceThreads, 3)
+lj_force_sell_kernel(const double* __restrict__ pos, int n_rows, const int* __restrict__ count,
+                     const int4* __restrict__ nbr, int Q, pc_box b, LJConst c, double guard,
+                     double* __restrict__ f3, int64_t f_stride, double* __restrict__ v,
+                     int64_t v_stride, double dtm, double mass, double* __restrict__ partial,
+                     int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = i < n_rows;
+  double4 pi = make_double4(0.0, 0.0, 0.0, 0.0);
+  int m = 0;
+  if (live) {
+    pi = ld_pos4(pos + 4 * (int64_t)i);
+    m = count[i];
+  }
+  const int mq = (m + 3) >> 2;
+  const int qmax = __reduce_max_sync(0xffffffffu, mq);
+  const bool nx = b.periodic[0] && (pi.x - b.low[0] < guard || b.high[0] - pi.x <= guard);
+  const bool ny = b.periodic[1] && (pi.y - b.low[1] < guard || b.high[1] - pi.y <= guard);
+  const bool nz = b.periodic[2] && (pi.z - b.low[2] < guard || b.high[2] - pi.z <= guard);
+  const int4* row = nbr + (int64_t)(i >> 5) * Q * 32 + lane;
+  double fx = 0.0, fy = 0.0, fz = 0.0, pe = 0.0;
+  bool overlap = false;
+  if (__any_sync(0xffffffffu, live && (nx || ny || nz)))
+    sell_row<true>(pos, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+  else
+    sell_row<false>(pos, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+  if (overlap) atomicOr(flag, kFlagOverlap);
+  double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0;
+  if (live) {
+    f3[i] = fx;
+    f3[f_stride + i] = fy;
+    f3[2 * f_stride + i] = fz;
+    if (v) {
+      const double vx = __dadd_rn(v[i], __dmul_rn(dtm, fx));
+      const double vy = __dadd_rn(v[v_stride + i], __dmul_rn(dtm, fy));
+      const double vz = __dadd_rn(v[2 * v_stride + i], __dmul_rn(dtm, fz));
+      v[i] = vx;
+      v[v_stride + i] = vy;
+      v[2 * v_stride + i] = vz;
+      ke = __dmul_rn(0.5 * mass, r2_exact(vx, vy, vz));
+      px = mass * vx;
+      py = mass * vy;
+      pz = mass * vz;
+    }
+  }
+  if (partial) block_partials(ke, pe, px, py, pz, partial);
+}
+
 static LJConst make_const(const pc_lj* lj) {
   LJConst c;
   c.cutoff2 = lj->cutoff2;
   c.overlap2 = lj->overlap2;
   c.sig2 = (float)(lj->sigma * lj->sigma);
   c.eps4 = (float)(4.0 * lj->epsilon);
+  c.eps2 = (float)(2.0 * lj->epsilon);
   c.eps24 = (float)(24.0 * lj->epsilon);
   return c;
 }
@@ -205,6 +310,23 @@ int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,
         d_pos, n_rows, d_count, d_offsets, d_index, ell_stride, *box, c, d_f3, f_stride, d_f64,
         d_pe, d_v, v_stride, dtm, mass, d_partial, d_flag);
   return check_launch("pc_lj_force");
+}
+
+int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                     const int32_t* d_index, int32_t width, const pc_box* box, const pc_lj* lj,
+                     double mi_guard, double* d_f3, int64_t f_stride, double* d_v,
+                     int64_t v_stride, double dtm, double mass, double* d_partial,
+                     int32_t* d_flag, void* stream) {
+  if (n_rows < 0 || width % 4) {
+    set_error("pc_lj_force_sell: bad rows/width");
+    return PC_ERR_VALUE;
+  }
+  LJConst c = make_const(lj);
+  unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
+  lj_force_sell_kernel<<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+      d_pos, n_rows, d_count, reinterpret_cast<const int4*>(d_index), width / 4, *box, c,
+      mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag);
+  return check_launch("pc_lj_force_sell");
 }
 
 int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,

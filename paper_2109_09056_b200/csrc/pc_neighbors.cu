@@ -56,8 +56,10 @@ nbr_build_kernel(const double* __restrict__ pos, int n, const int* __restrict__ 
               const int v = out_tags ? (int)tj : j;
               if (MODE == PC_NBR_CSR) {
                 index[row + cnt] = v;
+              } else if (MODE == PC_NBR_ELL) {
+                if (cnt < ell_width) index[(int64_t)cnt * ell_stride + i] = v;
               } else if (cnt < ell_width) {
-                index[(int64_t)cnt * ell_stride + i] = v;
+                index[sell_word(i, cnt, ell_width >> 2)] = v;
               }
             }
             ++cnt;
@@ -67,7 +69,175 @@ nbr_build_kernel(const double* __restrict__ pos, int n, const int* __restrict__ 
     }
   }
   count[i] = cnt;
-  if (MODE == PC_NBR_ELL && cnt > ell_width) atomicOr(flag, kFlagOverflow);
+  if (MODE == PC_NBR_SELL) {
+    // pad the last quad with the dummy row (NaN position, never interacts)
+    for (int k = cnt; k < ell_width && (k & 3); ++k)
+      index[sell_word(i, k, ell_width >> 2)] = (int)ell_stride;
+  }
+  if ((MODE == PC_NBR_ELL || MODE == PC_NBR_SELL) && cnt > ell_width)
+    atomicOr(flag, kFlagOverflow);
+}
+
+// ---- staged build (MD hot path) -------------------------------------------
+// One CTA per (x, y) column segment of kSegCells home cells.  The 9 stencil
+// columns' cells z0-1 .. z1 are staged once into shared memory as FP32
+// coordinates relative to the segment centre (periodic image applied per
+// staged cell) plus the particle index, so each home particle scans its 27
+// stencil cells as 9 contiguous shared-memory ranges.  FP32 r^2 decides
+// every candidate outside a rigorously bounded band around cutoff^2; inside
+// the band the reference's FP64 predicate is evaluated on the global FP64
+// positions, so the result is bit-identical to pc_nbr_build / the reference.
+// Requires >= 3 cells on every periodic axis (else the v1 kernel is used).
+constexpr int kSegCells = 4;
+constexpr int kStageCells = kSegCells + 2;
+constexpr int kBuildThreads = 128;
+
+struct StagedParams {
+  double cutoff2;
+  float lo2, hi2;      // FP32 band: r2f < lo2 -> hit, r2f >= hi2 -> miss
+  int Q;               // quads per SELL slice
+  int dummy;           // padding row index
+  int max_stage;       // staged-candidate capacity (float4 entries)
+  int nseg;            // z segments per column
+};
+
+__device__ __forceinline__ bool exact_pair(const double* pos, int a, int j, const pc_box& b,
+                                           double cutoff2) {
+  const double4 pa = ld_pos4(pos + 4 * (int64_t)a);
+  const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
+  const double dx = min_image(__dsub_rn(pj.x, pa.x), b.length[0], b.mi_thresh[0]);
+  const double dy = min_image(__dsub_rn(pj.y, pa.y), b.length[1], b.mi_thresh[1]);
+  const double dz = min_image(__dsub_rn(pj.z, pa.z), b.length[2], b.mi_thresh[2]);
+  return r2_exact(dx, dy, dz) < cutoff2;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBuildThreads)
+nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __restrict__ cell_start,
+                        pc_grid g, pc_box b, StagedParams p, int* __restrict__ count,
+                        int* __restrict__ index, int* __restrict__ flag) {
+  extern __shared__ float4 stage[];
+  __shared__ int cell_off[9][kStageCells + 1];   // staged offset of each cell per column
+  __shared__ int cell_src[9][kStageCells];       // first global index of each staged cell
+  __shared__ double cell_shift[9][kStageCells][3];
+  __shared__ int total;
+
+  const int col = blockIdx.x / p.nseg;
+  const int seg = blockIdx.x - col * p.nseg;
+  const int cx = col / g.nc[1], cy = col - (col / g.nc[1]) * g.nc[1];
+  const int z0 = seg * kSegCells;
+  const int z1 = min(z0 + kSegCells, g.nc[2]);
+  const int nz = z1 - z0 + 2;                    // staged cells per column
+  const double ox = g.low[0] + (cx + 0.5) * g.width[0];
+  const double oy = g.low[1] + (cy + 0.5) * g.width[1];
+  const double oz = g.low[2] + 0.5 * (z0 + z1) * g.width[2];
+
+  // per (column, staged cell): source range and periodic shift
+  if (threadIdx.x < 9 * kStageCells) {
+    const int c = threadIdx.x / kStageCells, k = threadIdx.x - c * kStageCells;
+    int xs = cx + c / 3 - 1, ys = cy + c % 3 - 1, zs = z0 - 1 + k;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    bool ok = k < nz;
+    if (xs < 0) { if (b.periodic[0]) { xs += g.nc[0]; sx = -b.length[0]; } else ok = false; }
+    if (xs >= g.nc[0]) { if (b.periodic[0]) { xs -= g.nc[0]; sx = b.length[0]; } else ok = false; }
+    if (ys < 0) { if (b.periodic[1]) { ys += g.nc[1]; sy = -b.length[1]; } else ok = false; }
+    if (ys >= g.nc[1]) { if (b.periodic[1]) { ys -= g.nc[1]; sy = b.length[1]; } else ok = false; }
+    if (zs < 0) { if (b.periodic[2]) { zs += g.nc[2]; sz = -b.length[2]; } else ok = false; }
+    if (zs >= g.nc[2]) { if (b.periodic[2]) { zs -= g.nc[2]; sz = b.length[2]; } else ok = false; }
+    int cnt = 0, src = 0;
+    if (ok) {
+      const int cell = (xs * g.nc[1] + ys) * g.nc[2] + zs;
+      src = cell_start[cell];
+      cnt = cell_start[cell + 1] - src;
+    }
+    cell_src[c][k] = src;
+    cell_off[c][k + 1] = cnt;   // counts for now, scanned below
+    cell_shift[c][k][0] = sx;
+    cell_shift[c][k][1] = sy;
+    cell_shift[c][k][2] = sz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int c = 0; c < 9; ++c) {
+      cell_off[c][0] = run;
+      for (int k = 0; k < kStageCells; ++k) {
+        run += cell_off[c][k + 1];
+        cell_off[c][k + 1] = run;
+      }
+    }
+    total = run;
+  }
+  __syncthreads();
+  if (total > p.max_stage) {           // dense region: caller falls back to v1
+    if (threadIdx.x == 0) atomicOr(flag, kFlagStage);
+    return;
+  }
+  // stage: FP32 coordinates relative to the segment centre, image applied
+  for (int c = 0; c < 9; ++c) {
+    for (int k = 0; k < nz; ++k) {
+      const int m = cell_off[c][k + 1] - cell_off[c][k];
+      const int src = cell_src[c][k];
+      const int dst = cell_off[c][k];
+      const double sx = cell_shift[c][k][0], sy = cell_shift[c][k][1], sz = cell_shift[c][k][2];
+      for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        const double4 q = ld_pos4(pos + 4 * (int64_t)(src + t));
+        float4 s;
+        s.x = (float)(q.x + sx - ox);
+        s.y = (float)(q.y + sy - oy);
+        s.z = (float)(q.z + sz - oz);
+        s.w = __int_as_float(src + t);
+        stage[dst + t] = s;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int h0 = cell_src[4][1];
+  const int h1 = h0 + (cell_off[4][z1 - z0 + 1] - cell_off[4][1]);
+  const int Q = p.Q;
+  for (int a = h0 + threadIdx.x; a < h1; a += blockDim.x) {
+    const double4 pa = ld_pos4(pos + 4 * (int64_t)a);
+    const float xf = (float)(pa.x - ox), yf = (float)(pa.y - oy), zf = (float)(pa.z - oz);
+    // home cell index within the segment: locate a in column 4's staged cells
+    int k = 1;
+    while (k < z1 - z0 && a >= cell_src[4][k + 1]) ++k;
+    // k is the staged position of the home cell; window = staged cells k-1..k+1
+    int cnt = 0;
+    int b0 = p.dummy, b1 = p.dummy, b2 = p.dummy, b3 = p.dummy;
+    for (int c = 0; c < 9; ++c) {
+      const int s0 = cell_off[c][k - 1], s1 = cell_off[c][k + 2];
+      for (int s = s0; s < s1; ++s) {
+        const float4 q = stage[s];
+        const float dx = q.x - xf, dy = q.y - yf, dz = q.z - zf;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (r2 < p.hi2) {
+          const int j = __float_as_int(q.w);
+          if (j != a && (r2 < p.lo2 || exact_pair(pos, a, j, b, p.cutoff2))) {
+            if (MODE == PC_NBR_SELL && cnt < 4 * Q) {
+              b0 = b1; b1 = b2; b2 = b3; b3 = j;
+              if ((cnt & 3) == 3)
+                reinterpret_cast<int4*>(index)[((int64_t)(a >> 5) * Q + (cnt >> 2)) * 32 +
+                                               (a & 31)] = make_int4(b0, b1, b2, b3);
+            }
+            ++cnt;
+          }
+        }
+      }
+    }
+    if (MODE == PC_NBR_SELL) {
+      if ((cnt & 3) && cnt < 4 * Q) {
+        const int r = cnt & 3;     // valid entries in the open quad, oldest first
+        int4 v = make_int4(p.dummy, p.dummy, p.dummy, p.dummy);
+        if (r == 1) v.x = b3;
+        if (r == 2) { v.x = b2; v.y = b3; }
+        if (r == 3) { v.x = b1; v.y = b2; v.z = b3; }
+        reinterpret_cast<int4*>(index)[((int64_t)(a >> 5) * Q + (cnt >> 2)) * 32 + (a & 31)] = v;
+      }
+      if (cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
+    }
+    count[a] = cnt;
+  }
 }
 
 // Warp per row: ascending order by rank counting (values in a row are
@@ -146,6 +316,15 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
           d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
           d_offsets, d_index, ell_stride, ell_width, d_flag);
       break;
+    case PC_NBR_SELL:
+      if (ell_width % 4) {
+        set_error("pc_nbr_build: SELL width must be a multiple of 4");
+        return PC_ERR_VALUE;
+      }
+      nbr_build_kernel<PC_NBR_SELL><<<blocks, 128, 0, s>>>(
+          d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
+          d_offsets, d_index, ell_stride, ell_width, d_flag);
+      break;
     default:
       set_error("pc_nbr_build: unknown mode %d", mode);
       return PC_ERR_VALUE;
@@ -161,3 +340,54 @@ int pc_sort_rows(const int64_t* d_offsets, int32_t n, int32_t* d_index, void* st
 }
 
 }  // extern "C"
+
+namespace pc {
+static int g_stage_bytes = 0;
+}
+
+extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
+                                 const int32_t* d_cell_start, const pc_grid* grid,
+                                 const pc_box* box, double cutoff2, int32_t width,
+                                 int32_t dummy, int32_t* d_count, int32_t* d_index,
+                                 int32_t* d_flag, int32_t* h_used_staged, void* stream) {
+  using namespace pc;
+  if (n <= 0) return PC_OK;
+  if (width % 4 || width <= 0) {
+    set_error("pc_nbr_build_sell: width must be a positive multiple of 4");
+    return PC_ERR_VALUE;
+  }
+  cudaStream_t s = as_stream(stream);
+  bool staged = grid->ndim == 3;
+  for (int a = 0; a < 3; ++a) staged &= !(box->periodic[a] && grid->nc[a] < 3);
+  if (h_used_staged) *h_used_staged = staged ? 1 : 0;
+  if (!staged) {
+    return pc_nbr_build(d_pos_sorted, n, d_cell_start, grid, box, cutoff2, 0, PC_NBR_SELL, 0,
+                        d_count, nullptr, d_index, dummy, width, d_flag, stream);
+  }
+  // FP32 prefilter band (see header comment of nbr_build_staged_kernel)
+  double U = 0.0;
+  const double wz = grid->width[2] * (kSegCells / 2.0 + 1.0);
+  U = fmax(fmax(1.5 * grid->width[0], 1.5 * grid->width[1]), wz);
+  const double rc = sqrt(cutoff2);
+  const double e23 = ldexp(1.0, -23), e24 = ldexp(1.0, -24);
+  const double err = 2.0 * sqrt(3.0) * rc * (e23 * U + e24 * rc) + 3.0 * e24 * cutoff2;
+  const double margin = 8.0 * err + 1e-12 * cutoff2;
+  StagedParams p;
+  p.cutoff2 = cutoff2;
+  p.lo2 = nextafterf((float)(cutoff2 - margin), -INFINITY);
+  p.hi2 = nextafterf((float)(cutoff2 + margin), INFINITY);
+  p.Q = width / 4;
+  p.dummy = dummy;
+  const int stage_bytes = 64 * 1024;
+  p.max_stage = stage_bytes / (int)sizeof(float4);
+  p.nseg = (grid->nc[2] + kSegCells - 1) / kSegCells;
+  if (g_stage_bytes < stage_bytes) {
+    cudaFuncSetAttribute(nbr_build_staged_kernel<PC_NBR_SELL>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+    g_stage_bytes = stage_bytes;
+  }
+  const int64_t blocks = (int64_t)grid->nc[0] * grid->nc[1] * p.nseg;
+  nbr_build_staged_kernel<PC_NBR_SELL><<<(unsigned)blocks, kBuildThreads, stage_bytes, s>>>(
+      d_pos_sorted, n, d_cell_start, *grid, *box, p, d_count, d_index, d_flag);
+  return check_launch("pc_nbr_build_sell");
+}

@@ -26,7 +26,7 @@ the reference does (md.py:67-86) and uploaded once.
 
 from __future__ import annotations
 
-import time
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -223,12 +223,21 @@ class MDDriver:
         else:       # host (ideally pinned) x, v in global-id order
             x, v = (t if isinstance(t, torch.Tensor) else torch.as_tensor(t) for t in state)
         ids = torch.arange(n, dtype=torch.int64, device=dev)
-        self.pos = _kernels.pack_pos4(x.to(dev, non_blocking=True), ids)
+        # pos has one extra row: the SELL padding target (NaN position, tag -1)
+        self.pos = self._new_pos()
+        self.pos[:n] = _kernels.pack_pos4(x.to(dev, non_blocking=True), ids)
+        self._pos_alt = self._new_pos()
         self.vel = v.to(dev, non_blocking=True).t().contiguous()           # (3, n)
+        self._vel_alt = torch.empty_like(self.vel)
         self.force_events = None      # optional list collecting (start, end) per force launch
         self.frc = torch.zeros((3, n), dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(n, dtype=torch.int32, device=dev)
-        self.nbr = torch.empty((self.ell_width, n), dtype=torch.int32, device=dev)
+        self.ell_width = -(-self.ell_width // 4) * 4
+        self.nbr = self._new_nbr()
+        # minimum image only within this distance of a periodic face (exact:
+        # see pc_lj_force_sell in include/particula_b200.h)
+        self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
+        self.used_staged = None
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
         self.build_flag = torch.zeros(1, dtype=torch.int32, device=dev)  # ELL overflow
         self._nblk = int(_lib.load().pc_lj_force_blocks(n))
@@ -250,27 +259,51 @@ class MDDriver:
         if self._time:
             self._timer.stop(phase, e0)
 
+    def _new_pos(self):
+        p = torch.empty((self.cap + 1, 4), dtype=torch.float64, device=self.device)
+        p[self.cap, :3] = float("nan")
+        p[self.cap, 3] = torch.tensor(-1, dtype=torch.int64).view(torch.float64)
+        return p
+
+    def _new_nbr(self):
+        slices = -(-self.cap // 32)
+        return torch.empty(slices * self.ell_width * 32, dtype=torch.int32, device=self.device)
+
     def _rebuild(self):
-        """Cell sort of all particle fields + ELL Verlet build (md.py:169-188)."""
+        """Cell sort of all particle fields + SELL Verlet build (md.py:169-188)."""
         n, s = self.n, stream()
         e0 = self._t0()
         srt = _kernels.CellSort(self.pos, 4, self._grid)
-        self.pos = _kernels.gather_rows(self.pos, srt.order, n)
-        self.vel = torch.stack([_kernels.gather_rows(self.vel[a], srt.order, n)
-                                for a in range(3)])
+        _kernels.gather_rows(self.pos, srt.order, n, out=self._pos_alt)
+        for a in range(3):
+            _kernels.gather_rows(self.vel[a], srt.order, n, out=self._vel_alt[a])
+        self.pos, self._pos_alt = self._pos_alt, self.pos
+        self.vel, self._vel_alt = self._vel_alt, self.vel
         self._t1("sort", e0)
         e0 = self._t0()
+        used = ctypes.c_int32(0)
+        staged = True
         while True:
             self.build_flag.zero_()
-            call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid, self._pbox,
-                 self._search2, 0, _lib.PC_NBR_ELL, 0, ptr(self.cnt), None, ptr(self.nbr),
-                 self.cap, self.ell_width, ptr(self.build_flag), s)
-            if not (int(self.build_flag.item()) & _lib.FLAG_OVERFLOW):
+            if staged:
+                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                     self._pbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
+                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s)
+            else:
+                call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                     self._pbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
+                     ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s)
+                used.value = 0
+            fl = int(self.build_flag.item())
+            if fl & _lib.FLAG_STAGE:          # dense neighbourhood: per-particle kernel
+                staged = False
+                continue
+            if not (fl & _lib.FLAG_OVERFLOW):
                 break
             # no silent truncation (SPEC neighbors: grow and rebuild)
-            self.ell_width = int(self.cnt.max().item()) + 8
-            self.nbr = torch.empty((self.ell_width, self.cap), dtype=torch.int32,
-                                   device=self.device)
+            self.ell_width = -(-(int(self.cnt[:n].max().item()) + 8) // 4) * 4
+            self.nbr = self._new_nbr()
+        self.used_staged = bool(used.value)
         self._t1("neighbor", e0)
         self.rebuilds += 1
 
@@ -279,10 +312,10 @@ class MDDriver:
         if self.force_events is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-        call("pc_lj_force", ptr(self.pos), self.n, ptr(self.cnt), None, ptr(self.nbr), self.cap,
-             self._pbox, self._lj, ptr(self.frc), self.cap, None, None, ptr(self.vel),
-             self.cap, float(kick_dtm), float(self.cfg.mass), ptr(self.partial),
-             ptr(self.flag), stream())
+        call("pc_lj_force_sell", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
+             self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
+             ptr(self.vel), self.cap, float(kick_dtm), float(self.cfg.mass),
+             ptr(self.partial), ptr(self.flag), stream())
         if self.force_events is not None:
             b.record()
             self.force_events.append((a, b))
@@ -339,6 +372,24 @@ class MDDriver:
         x[ids] = p[:, :3]
         v[ids] = self.vel[:, : self.n].cpu().numpy().T
         return x, v
+
+    def verlet_sets(self):
+        """The current Verlet list (search radius) as a CSR over global ids:
+        (counts, offsets, indices), rows in id order, row entries sorted --
+        the layout of ref neighbors.build_verlet for parity checks."""
+        n, Q = self.n, self.ell_width // 4
+        cnt = self.cnt[:n].to(torch.int64).cpu().numpy()
+        words = self.nbr.cpu().numpy()
+        gid = self.pos[:n, 3].contiguous().view(torch.int64).cpu().numpy()
+        a = np.repeat(np.arange(n), cnt)
+        k = np.arange(a.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        w = ((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)
+        j = words[w]
+        rows_gid, nb_gid = gid[a], gid[j]
+        o = np.lexsort((nb_gid, rows_gid))
+        counts = np.bincount(rows_gid, minlength=n)
+        offsets = np.concatenate(([0], np.cumsum(counts)))
+        return counts, offsets, nb_gid[o]
 
     def negate_velocities(self):
         self.vel.neg_()

@@ -346,3 +346,27 @@ def test_md_skin_and_stride_equivalence(pc):
     rows, _ = pc.md.run_md(pc.md.MDConfig(steps=60, skin=0.2, rebuild_stride=5, **base))
     for a, b in zip(ref, rows):
         assert abs(a["E_total"] - b["E_total"]) < 1e-9 * abs(b["E_total"])
+
+
+@pytest.mark.parametrize("cells,temp", [(16, 1.44), (8, 3.0), (6, 1.44)])
+def test_md_verlet_list_bit_exact(pc, oracle, cells, temp):
+    """The MD engine's SELL list (staged FP32-prefilter build when every axis
+    has >= 3 cells) equals the oracle's list on the same positions, bit-exact,
+    at init and after 25 steps (one rebuild at step 20)."""
+    cfg = pc.md.MDConfig(lattice_cells=cells, density=0.8442, temperature=temp, cutoff=2.5,
+                         skin=0.3, rebuild_stride=20, seed=3, steps=0)
+    drv = pc.md.MDDriver(cfg)
+    for stage in range(2):
+        if stage:
+            for s in range(1, 21):
+                drv.step(s)
+        p = drv.pos[: drv.n].cpu().numpy()
+        ids = p[:, 3].copy().view(np.int64)
+        x = np.empty((drv.n, 3))
+        x[ids] = p[:, :3]
+        counts, offsets, idx = drv.verlet_sets()
+        ref = oracle.build_verlet(x, drv.box.low, drv.box.high, [True] * 3, drv.search)
+        assert np.array_equal(counts, ref["counts"])
+        assert np.array_equal(idx, ref["indices"])
+    nc = int(np.floor(drv.box.lengths[0] / drv.search))
+    assert drv.used_staged == (nc >= 3)
