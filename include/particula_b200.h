@@ -213,9 +213,11 @@ int32_t pc_lj_force_blocks(int32_t n_rows);
  * 256-bit pos4 gathers in flight.  Minimum image is applied only on axes where
  * the row particle lies within `mi_guard` of a periodic face: for a Verlet
  * list whose pairs stay closer than mi_guard this is bit-identical to applying
- * it everywhere (pass +inf to always apply it).  FP64 force accumulation,
- * fused final half kick (d_v may be NULL), per-block partials (KE after kick,
- * PE with each pair booked half on either side, px, py, pz). */
+ * it everywhere (pass +inf to always apply it).  FP64 pair arithmetic and
+ * accumulation, fused final half kick (d_v may be NULL), per-WARP partials
+ * (pc_lj_force_sell_partials(n) rows of KE after kick, PE with each pair
+ * booked half on either side, px, py, pz). */
+int32_t pc_lj_force_sell_partials(int32_t n_rows);
 int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count,
                      const int32_t* d_index, int32_t width, const pc_box* box,
                      const pc_lj* lj, double mi_guard, double* d_f3, int64_t f_stride,

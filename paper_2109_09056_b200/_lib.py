@@ -91,6 +91,7 @@ SIGNATURES = {
                                    ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_vp, c_i64,
                                    c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
     "pc_lj_force_blocks": (c_i32, [c_i32]),
+    "pc_lj_force_sell_partials": (c_i32, [c_i32]),
     "pc_lj_force_half": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i64,
                                         ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_vp,
                                         c_i64, c_vp, c_vp, c_vp]),

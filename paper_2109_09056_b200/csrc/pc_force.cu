@@ -19,6 +19,7 @@ constexpr int kForceThreads = 256;
 struct LJConst {
   double cutoff2, overlap2;
   float sig2, eps4, eps2, eps24;
+  double sig2d, eps2d, eps24d;
 };
 
 __device__ __forceinline__ void block_partials(double v0, double v1, double v2, double v3,
@@ -162,9 +163,21 @@ lj_force_half_kernel(const double* __restrict__ pos, int n_rows, const int* __re
 
 // ---- MD hot path: SELL-32x4 list ------------------------------------------
 // One pair: FP64 displacement (minimum image only where the row particle is
-// near a periodic face, see pc_lj_force_sell), exact FP64 cutoff test, FP32
-// LJ magnitude with bit-pattern conversions (integer pipe, no F2F), FP64
-// accumulation; energy booked half on each side of the pair.
+// near a periodic face, see pc_lj_force_sell), exact FP64 cutoff test, FP64
+// LJ magnitude and accumulation; energy booked half on each side of the pair.
+//
+// Branch-free minimum image for wrapped coordinates (|d| < L): the fast form
+// of pc::min_image without its |d| >= L division fallback.
+__device__ __forceinline__ double min_image_wrapped(double d, double L, double T) {
+  const double a = fabs(d);
+  const double t = copysign(__dsub_rn(a, L), -d);
+  return a >= T ? t : d;
+}
+
+// The pair magnitude is evaluated in FP64 from an approximate reciprocal
+// (MUFU.RCP64H, ~2^-22) refined by one Newton step (~2^-44): no FP32<->FP64
+// conversions, ~11 DFMA-pipe ops, error far below the 1e-5 force tolerance.
+// Force/energy prefactors (24 eps, 2 eps) are applied once per row.
 template <bool MI>
 __device__ __forceinline__ void sell_pair(const double4& pj, const double4& pi, bool nx, bool ny,
                                           bool nz, const pc_box& b, const LJConst& c, double& fx,
@@ -173,21 +186,23 @@ __device__ __forceinline__ void sell_pair(const double4& pj, const double4& pi, 
   double dy = __dsub_rn(pj.y, pi.y);
   double dz = __dsub_rn(pj.z, pi.z);
   if (MI) {
-    if (nx) dx = min_image(dx, b.length[0], b.mi_thresh[0]);
-    if (ny) dy = min_image(dy, b.length[1], b.mi_thresh[1]);
-    if (nz) dz = min_image(dz, b.length[2], b.mi_thresh[2]);
+    if (nx) dx = min_image_wrapped(dx, b.length[0], b.mi_thresh[0]);
+    if (ny) dy = min_image_wrapped(dy, b.length[1], b.mi_thresh[1]);
+    if (nz) dz = min_image_wrapped(dz, b.length[2], b.mi_thresh[2]);
   }
   const double r2 = r2_exact(dx, dy, dz);
   if (r2 < c.cutoff2) {
     overlap |= (r2 < c.overlap2);
-    const float inv = rcp_approx(d2f_bits(r2));
-    const float sr2 = c.sig2 * inv;
-    const float sr6 = sr2 * sr2 * sr2;
-    const double fm = f2d_bits(c.eps24 * sr6 * (2.f * sr6 - 1.f) * inv);
+    double inv;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(r2));
+    inv = fma(inv, fma(-r2, inv, 1.0), inv);
+    const double sr2 = c.sig2d * inv;
+    const double sr6 = sr2 * sr2 * sr2;
+    const double fm = fma(2.0 * sr6, sr6, -sr6) * inv;      // (2 sr12 - sr6) / r2
     fx = fma(-fm, dx, fx);
     fy = fma(-fm, dy, fy);
     fz = fma(-fm, dz, fz);
-    pe += f2d_bits(c.eps2 * sr6 * (sr6 - 1.f));
+    pe = fma(sr6, sr6, pe - sr6);                            // sr12 - sr6
   }
 }
 
@@ -243,6 +258,10 @@ lj_force_sell_kernel(const double* __restrict__ pos, int n_rows, const int* __re
   else
     sell_row<false>(pos, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
   if (overlap) atomicOr(flag, kFlagOverlap);
+  fx *= c.eps24d;
+  fy *= c.eps24d;
+  fz *= c.eps24d;
+  pe *= c.eps2d;
   double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0;
   if (live) {
     f3[i] = fx;
@@ -261,7 +280,18 @@ lj_force_sell_kernel(const double* __restrict__ pos, int n_rows, const int* __re
       pz = mass * vz;
     }
   }
-  if (partial) block_partials(ke, pe, px, py, pz, partial);
+  if (partial) {
+    // per-warp partials: no block barrier, so fast warps retire early
+    ke = warp_sum(ke);
+    pe = warp_sum(pe);
+    px = warp_sum(px);
+    py = warp_sum(py);
+    pz = warp_sum(pz);
+    if (lane == 0) {
+      double* o = partial + (int64_t)(i >> 5) * 5;
+      o[0] = ke; o[1] = pe; o[2] = px; o[3] = py; o[4] = pz;
+    }
+  }
 }
 
 static LJConst make_const(const pc_lj* lj) {
@@ -272,6 +302,9 @@ static LJConst make_const(const pc_lj* lj) {
   c.eps4 = (float)(4.0 * lj->epsilon);
   c.eps2 = (float)(2.0 * lj->epsilon);
   c.eps24 = (float)(24.0 * lj->epsilon);
+  c.sig2d = lj->sigma * lj->sigma;
+  c.eps2d = 2.0 * lj->epsilon;
+  c.eps24d = 24.0 * lj->epsilon;
   return c;
 }
 
@@ -283,6 +316,10 @@ extern "C" {
 
 int32_t pc_lj_force_blocks(int32_t n_rows) {
   return n_rows <= 0 ? 1 : (n_rows + kForceThreads - 1) / kForceThreads;
+}
+
+int32_t pc_lj_force_sell_partials(int32_t n_rows) {
+  return pc_lj_force_blocks(n_rows) * (kForceThreads / 32);
 }
 
 int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,

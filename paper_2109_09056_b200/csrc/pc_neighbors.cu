@@ -193,50 +193,51 @@ nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __rest
   }
   __syncthreads();
 
-  const int h0 = cell_src[4][1];
-  const int h1 = h0 + (cell_off[4][z1 - z0 + 1] - cell_off[4][1]);
+  // Warp-cooperative sweep: warp w owns home cell k = w + 1 (staged position;
+  // window = staged cells k-1..k+1 of every column, 9 contiguous smem ranges
+  // shared by all its particles).  For one home particle at a time the lanes
+  // test 32 candidates at once; hits are compacted into the row with
+  // ballot/popc, so rows list neighbors in staged order.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int Q = p.Q;
-  for (int a = h0 + threadIdx.x; a < h1; a += blockDim.x) {
-    const double4 pa = ld_pos4(pos + 4 * (int64_t)a);
-    const float xf = (float)(pa.x - ox), yf = (float)(pa.y - oy), zf = (float)(pa.z - oz);
-    // home cell index within the segment: locate a in column 4's staged cells
-    int k = 1;
-    while (k < z1 - z0 && a >= cell_src[4][k + 1]) ++k;
-    // k is the staged position of the home cell; window = staged cells k-1..k+1
-    int cnt = 0;
-    int b0 = p.dummy, b1 = p.dummy, b2 = p.dummy, b3 = p.dummy;
-    for (int c = 0; c < 9; ++c) {
-      const int s0 = cell_off[c][k - 1], s1 = cell_off[c][k + 2];
-      for (int s = s0; s < s1; ++s) {
-        const float4 q = stage[s];
-        const float dx = q.x - xf, dy = q.y - yf, dz = q.z - zf;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        if (r2 < p.hi2) {
-          const int j = __float_as_int(q.w);
-          if (j != a && (r2 < p.lo2 || exact_pair(pos, a, j, b, p.cutoff2))) {
-            if (MODE == PC_NBR_SELL && cnt < 4 * Q) {
-              b0 = b1; b1 = b2; b2 = b3; b3 = j;
-              if ((cnt & 3) == 3)
-                reinterpret_cast<int4*>(index)[((int64_t)(a >> 5) * Q + (cnt >> 2)) * 32 +
-                                               (a & 31)] = make_int4(b0, b1, b2, b3);
-            }
-            ++cnt;
+  for (int k = warp + 1; k <= z1 - z0; k += kBuildThreads / 32) {
+    const int hs = cell_off[4][k];                 // staged slot of the first home particle
+    const int hn = cell_off[4][k + 1] - hs;
+    for (int h = 0; h < hn; ++h) {
+      const float4 me = stage[hs + h];
+      const int a = __float_as_int(me.w);
+      int cnt = 0;
+      for (int c = 0; c < 9; ++c) {
+        const int s0 = cell_off[c][k - 1], s1 = cell_off[c][k + 2];
+        for (int s = s0 + lane; s - lane < s1; s += 32) {
+          bool hit = false;
+          int j = 0;
+          if (s < s1) {
+            const float4 q = stage[s];
+            const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            j = __float_as_int(q.w);
+            if (r2 < p.hi2 && j != a)
+              hit = r2 < p.lo2 || exact_pair(pos, a, j, b, p.cutoff2);
           }
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (MODE == PC_NBR_SELL && hit) {
+            const int k2 = cnt + __popc(m & lt);
+            if (k2 < 4 * Q) index[sell_word(a, k2, Q)] = j;
+          }
+          cnt += __popc(m);
         }
       }
-    }
-    if (MODE == PC_NBR_SELL) {
-      if ((cnt & 3) && cnt < 4 * Q) {
-        const int r = cnt & 3;     // valid entries in the open quad, oldest first
-        int4 v = make_int4(p.dummy, p.dummy, p.dummy, p.dummy);
-        if (r == 1) v.x = b3;
-        if (r == 2) { v.x = b2; v.y = b3; }
-        if (r == 3) { v.x = b1; v.y = b2; v.z = b3; }
-        reinterpret_cast<int4*>(index)[((int64_t)(a >> 5) * Q + (cnt >> 2)) * 32 + (a & 31)] = v;
+      if (MODE == PC_NBR_SELL) {
+        // pad the open quad with the dummy row
+        const int kpad = cnt + lane;
+        if (lane < 4 && (kpad & 3) && (kpad >> 2) == (cnt >> 2) && kpad < 4 * Q)
+          index[sell_word(a, kpad, Q)] = p.dummy;
+        if (lane == 0 && cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
       }
-      if (cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
+      if (lane == 0) count[a] = cnt;
     }
-    count[a] = cnt;
   }
 }
 
@@ -378,7 +379,7 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
   p.hi2 = nextafterf((float)(cutoff2 + margin), INFINITY);
   p.Q = width / 4;
   p.dummy = dummy;
-  const int stage_bytes = 64 * 1024;
+  const int stage_bytes = 32 * 1024;
   p.max_stage = stage_bytes / (int)sizeof(float4);
   p.nseg = (grid->nc[2] + kSegCells - 1) / kSegCells;
   if (g_stage_bytes < stage_bytes) {

@@ -240,7 +240,7 @@ class MDDriver:
         self.used_staged = None
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
         self.build_flag = torch.zeros(1, dtype=torch.int32, device=dev)  # ELL overflow
-        self._nblk = int(_lib.load().pc_lj_force_blocks(n))
+        self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))   # per-warp rows
         self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
         self._ke_fresh = False
