@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
+                    help="force-kernel neighbor gather layout")
     return ap.parse_args()
 
 
@@ -187,7 +189,7 @@ def run_ours(args):
 
     kw = md_kwargs(args, args.cells)
     cfg = pc.md.MDConfig(**kw, steps=args.steps)
-    drv = pc.md.MDDriver(cfg, time_phases=False)
+    drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar")
     n = drv.n
     W, K = args.warmup, args.steps
     for s in range(1, W + 1):

@@ -218,7 +218,9 @@ int32_t pc_lj_force_blocks(int32_t n_rows);
  * (pc_lj_force_sell_partials(n) rows of KE after kick, PE with each pair
  * booked half on either side, px, py, pz). */
 int32_t pc_lj_force_sell_partials(int32_t n_rows);
-int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+int pc_lj_force_sell(const double* d_pos, const double* d_planar /* x|y|z planar copy or
+                     NULL: gathers then read 24 B as three 64-bit loads */,
+                     int64_t planar_stride, int32_t n_rows, const int32_t* d_count,
                      const int32_t* d_index, int32_t width, const pc_box* box,
                      const pc_lj* lj, double mi_guard, double* d_f3, int64_t f_stride,
                      double* d_v, int64_t v_stride, double dtm, double mass,
@@ -236,7 +238,12 @@ int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count
 /* v += dtm*f; x += dt*v; x = wrap(x) on rows [0,n) -- numpy rounding order. */
 int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride,
                        const double* d_f3, int64_t f_stride, int32_t n,
-                       double dtm, double dt, const pc_box* box, void* stream);
+                       double dtm, double dt, const pc_box* box,
+                       double* d_planar /* optional x|y|z planar copy, or NULL */,
+                       int64_t planar_stride, void* stream);
+/* planar[a*stride + i] = pos4[i].a for a = x, y, z. */
+int pc_pos_planar(const double* d_pos, int32_t n, double* d_planar, int64_t planar_stride,
+                  void* stream);
 /* v += dtm*f, plus the per-block diagnostic partials (KE, 0, px, py, pz). */
 int pc_kick(double* d_v, int64_t v_stride, const double* d_f3, int64_t f_stride,
             int32_t n, double dtm, double mass, double* d_partial, void* stream);

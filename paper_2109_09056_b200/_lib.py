@@ -84,7 +84,9 @@ SIGNATURES = {
     "pc_nbr_build_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
                                          ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_vp,
                                          c_vp, c_vp, ctypes.POINTER(c_i32), c_vp]),
-    "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, ctypes.POINTER(PcBox),
+    "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
+    "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
+                                        ctypes.POINTER(PcBox),
                                         ctypes.POINTER(PcLJ), c_dbl, c_vp, c_i64, c_vp, c_i64,
                                         c_dbl, c_dbl, c_vp, c_vp, c_vp]),
     "pc_lj_force": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i64,
@@ -96,7 +98,7 @@ SIGNATURES = {
                                         ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_vp,
                                         c_i64, c_vp, c_vp, c_vp]),
     "pc_kick_drift_wrap": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_dbl,
-                                          c_dbl, ctypes.POINTER(PcBox), c_vp]),
+                                          c_dbl, ctypes.POINTER(PcBox), c_vp, c_i64, c_vp]),
     "pc_kick": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i32, c_dbl, c_dbl, c_vp, c_vp]),
     "pc_reduce_partials": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
     "pc_box_wrap": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcBox), c_vp]),

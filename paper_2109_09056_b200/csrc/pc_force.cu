@@ -206,8 +206,26 @@ __device__ __forceinline__ void sell_pair(const double4& pj, const double4& pi, 
   }
 }
 
-template <bool MI>
+// Gather of one candidate: pos4 (one 256-bit load) or planar x/y/z arrays
+// (three 64-bit loads; 24 B instead of 32 B per candidate and 8-B items, so
+// a warp's 32 scattered requests touch fewer L1 lines and wavefronts).
+template <bool PLANAR>
+__device__ __forceinline__ double4 gather(const double* __restrict__ pos,
+                                          const double* __restrict__ pl, int64_t ps, int j) {
+  if (PLANAR) {
+    double4 r;
+    r.x = __ldg(pl + j);
+    r.y = __ldg(pl + ps + j);
+    r.z = __ldg(pl + 2 * ps + j);
+    r.w = 0.0;
+    return r;
+  }
+  return ld_pos4(pos + 4 * (int64_t)j);
+}
+
+template <bool MI, bool PLANAR>
 __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
+                                         const double* __restrict__ pl, int64_t ps,
                                          const int4* __restrict__ row, int mq, int qmax,
                                          const double4& pi, bool nx, bool ny, bool nz,
                                          const pc_box& b, const LJConst& c, double& fx,
@@ -218,10 +236,10 @@ __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
     const int4 cur = nxt;
     if (q + 1 < mq) nxt = __ldg(row + (int64_t)(q + 1) * 32);
     if (q < mq) {
-      const double4 p0 = ld_pos4(pos + 4 * (int64_t)cur.x);
-      const double4 p1 = ld_pos4(pos + 4 * (int64_t)cur.y);
-      const double4 p2 = ld_pos4(pos + 4 * (int64_t)cur.z);
-      const double4 p3 = ld_pos4(pos + 4 * (int64_t)cur.w);
+      const double4 p0 = gather<PLANAR>(pos, pl, ps, cur.x);
+      const double4 p1 = gather<PLANAR>(pos, pl, ps, cur.y);
+      const double4 p2 = gather<PLANAR>(pos, pl, ps, cur.z);
+      const double4 p3 = gather<PLANAR>(pos, pl, ps, cur.w);
       sell_pair<MI>(p0, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
       sell_pair<MI>(p1, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
       sell_pair<MI>(p2, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
@@ -230,8 +248,10 @@ __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
   }
 }
 
+template <bool PLANAR>
 __global__ void __launch_bounds__(kForceThreads, 3)
-lj_force_sell_kernel(const double* __restrict__ pos, int n_rows, const int* __restrict__ count,
+lj_force_sell_kernel(const double* __restrict__ pos, const double* __restrict__ pl, int64_t ps,
+                     int n_rows, const int* __restrict__ count,
                      const int4* __restrict__ nbr, int Q, pc_box b, LJConst c, double guard,
                      double* __restrict__ f3, int64_t f_stride, double* __restrict__ v,
                      int64_t v_stride, double dtm, double mass, double* __restrict__ partial,
@@ -254,9 +274,11 @@ lj_force_sell_kernel(const double* __restrict__ pos, int n_rows, const int* __re
   double fx = 0.0, fy = 0.0, fz = 0.0, pe = 0.0;
   bool overlap = false;
   if (__any_sync(0xffffffffu, live && (nx || ny || nz)))
-    sell_row<true>(pos, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+    sell_row<true, PLANAR>(pos, pl, ps, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe,
+                           overlap);
   else
-    sell_row<false>(pos, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+    sell_row<false, PLANAR>(pos, pl, ps, row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz, pe,
+                            overlap);
   if (overlap) atomicOr(flag, kFlagOverlap);
   fx *= c.eps24d;
   fy *= c.eps24d;
@@ -349,7 +371,8 @@ int pc_lj_force(const double* d_pos, int32_t n_rows, const int32_t* d_count,
   return check_launch("pc_lj_force");
 }
 
-int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+int pc_lj_force_sell(const double* d_pos, const double* d_planar, int64_t planar_stride,
+                     int32_t n_rows, const int32_t* d_count,
                      const int32_t* d_index, int32_t width, const pc_box* box, const pc_lj* lj,
                      double mi_guard, double* d_f3, int64_t f_stride, double* d_v,
                      int64_t v_stride, double dtm, double mass, double* d_partial,
@@ -360,9 +383,16 @@ int pc_lj_force_sell(const double* d_pos, int32_t n_rows, const int32_t* d_count
   }
   LJConst c = make_const(lj);
   unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
-  lj_force_sell_kernel<<<blocks, kForceThreads, 0, as_stream(stream)>>>(
-      d_pos, n_rows, d_count, reinterpret_cast<const int4*>(d_index), width / 4, *box, c,
-      mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag);
+  if (d_planar)
+    lj_force_sell_kernel<true><<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+        d_pos, d_planar, planar_stride, n_rows, d_count, reinterpret_cast<const int4*>(d_index),
+        width / 4, *box, c, mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial,
+        d_flag);
+  else
+    lj_force_sell_kernel<false><<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+        d_pos, d_planar, planar_stride, n_rows, d_count, reinterpret_cast<const int4*>(d_index),
+        width / 4, *box, c, mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial,
+        d_flag);
   return check_launch("pc_lj_force_sell");
 }
 

@@ -26,7 +26,7 @@ __device__ __forceinline__ double wrap_axis(double x, double low, double high, d
 __global__ void __launch_bounds__(kIntThreads)
 kick_drift_wrap_kernel(double* __restrict__ pos, double* __restrict__ v, int64_t vs,
                        const double* __restrict__ f, int64_t fs, int n, double dtm, double dt,
-                       pc_box b) {
+                       pc_box b, double* __restrict__ planar, int64_t ps) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double* p = pos + 4 * (int64_t)i;
@@ -42,6 +42,21 @@ kick_drift_wrap_kernel(double* __restrict__ pos, double* __restrict__ v, int64_t
   p[0] = x[0];
   p[1] = x[1];
   p[2] = x[2];
+  if (planar) {
+    planar[i] = x[0];
+    planar[ps + i] = x[1];
+    planar[2 * ps + i] = x[2];
+  }
+}
+
+__global__ void pos_planar_kernel(const double* __restrict__ pos, int n,
+                                  double* __restrict__ planar, int64_t ps) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = ld_pos4(pos + 4 * (int64_t)i);
+  planar[i] = p.x;
+  planar[ps + i] = p.y;
+  planar[2 * ps + i] = p.z;
 }
 
 __global__ void __launch_bounds__(kIntThreads)
@@ -145,12 +160,20 @@ extern "C" {
 
 int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride, const double* d_f3,
                        int64_t f_stride, int32_t n, double dtm, double dt, const pc_box* box,
-                       void* stream) {
+                       double* d_planar, int64_t planar_stride, void* stream) {
   if (n <= 0) return PC_OK;
   kick_drift_wrap_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0,
                            as_stream(stream)>>>(d_pos, d_v, v_stride, d_f3, f_stride, n, dtm, dt,
-                                                *box);
+                                                *box, d_planar, planar_stride);
   return check_launch("pc_kick_drift_wrap");
+}
+
+int pc_pos_planar(const double* d_pos, int32_t n, double* d_planar, int64_t planar_stride,
+                  void* stream) {
+  if (n <= 0) return PC_OK;
+  pos_planar_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0, as_stream(stream)>>>(
+      d_pos, n, d_planar, planar_stride);
+  return check_launch("pc_pos_planar");
 }
 
 int pc_kick(double* d_v, int64_t v_stride, const double* d_f3, int64_t f_stride, int32_t n,

@@ -189,7 +189,7 @@ class MDDriver:
     """
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
-                 time_phases: bool = True, state=None):
+                 time_phases: bool = True, state=None, planar_gather: bool = True):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -238,6 +238,13 @@ class MDDriver:
         # see pc_lj_force_sell in include/particula_b200.h)
         self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
         self.used_staged = None
+        # planar x|y|z copy (stride cap+1, NaN dummy row) read by the force
+        # gathers: 24 B in 8-B items per candidate instead of one 32-B pos4
+        self.planar_gather = planar_gather
+        self.pl = None
+        if planar_gather:
+            self.pl = torch.empty((3, self.cap + 1), dtype=torch.float64, device=dev)
+            self.pl[:, self.cap] = float("nan")
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
         self.build_flag = torch.zeros(1, dtype=torch.int32, device=dev)  # ELL overflow
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))   # per-warp rows
@@ -279,6 +286,8 @@ class MDDriver:
             _kernels.gather_rows(self.vel[a], srt.order, n, out=self._vel_alt[a])
         self.pos, self._pos_alt = self._pos_alt, self.pos
         self.vel, self._vel_alt = self._vel_alt, self.vel
+        if self.pl is not None:
+            call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self.cap + 1, s)
         self._t1("sort", e0)
         e0 = self._t0()
         used = ctypes.c_int32(0)
@@ -312,7 +321,8 @@ class MDDriver:
         if self.force_events is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-        call("pc_lj_force_sell", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
+        call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n,
+             ptr(self.cnt), ptr(self.nbr),
              self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
              ptr(self.vel), self.cap, float(kick_dtm), float(self.cfg.mass),
              ptr(self.partial), ptr(self.flag), stream())
@@ -325,7 +335,8 @@ class MDDriver:
     def _integrate(self):
         e0 = self._t0()
         call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
-             self.cap, self.n, self._dtm, float(self.cfg.dt), self._pbox, stream())
+             self.cap, self.n, self._dtm, float(self.cfg.dt), self._pbox, ptr(self.pl),
+             self.cap + 1, stream())
         self._t1("integrate", e0)
 
     def step(self, step_index: int):
