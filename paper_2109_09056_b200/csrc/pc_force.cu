@@ -223,6 +223,38 @@ __device__ __forceinline__ double4 gather(const double* __restrict__ pos,
   return ld_pos4(pos + 4 * (int64_t)j);
 }
 
+// Software-pipelined row sweep over the planar positions: while quad q is
+// computed, the positions of quad q+1 and the indices of quad q+2 are in
+// flight (lanes past their own row length gather the NaN dummy row).
+template <bool MI>
+__device__ __forceinline__ void sell_row_pipe(const double* __restrict__ pl, int64_t ps,
+                                              int dummy, const int4* __restrict__ row, int mq,
+                                              int qmax, const double4& pi, bool nx, bool ny,
+                                              bool nz, const pc_box& b, const LJConst& c,
+                                              double& fx, double& fy, double& fz, double& pe,
+                                              bool& overlap) {
+  const int4 d4 = make_int4(dummy, dummy, dummy, dummy);
+  int4 i1 = mq > 0 ? __ldg(row) : d4;
+  int4 i2 = mq > 1 ? __ldg(row + 32) : d4;
+  double4 c0 = gather<true>(nullptr, pl, ps, i1.x), c1 = gather<true>(nullptr, pl, ps, i1.y);
+  double4 c2 = gather<true>(nullptr, pl, ps, i1.z), c3 = gather<true>(nullptr, pl, ps, i1.w);
+  for (int q = 0; q < qmax; ++q) {
+    const int4 i3 = q + 2 < mq ? __ldg(row + (int64_t)(q + 2) * 32) : d4;
+    const double4 n0 = gather<true>(nullptr, pl, ps, i2.x);
+    const double4 n1 = gather<true>(nullptr, pl, ps, i2.y);
+    const double4 n2 = gather<true>(nullptr, pl, ps, i2.z);
+    const double4 n3 = gather<true>(nullptr, pl, ps, i2.w);
+    if (q < mq) {
+      sell_pair<MI>(c0, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(c1, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(c2, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+      sell_pair<MI>(c3, pi, nx, ny, nz, b, c, fx, fy, fz, pe, overlap);
+    }
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    i2 = i3;
+  }
+}
+
 template <bool MI, bool PLANAR>
 __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
                                          const double* __restrict__ pl, int64_t ps,
@@ -230,6 +262,11 @@ __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
                                          const double4& pi, bool nx, bool ny, bool nz,
                                          const pc_box& b, const LJConst& c, double& fx,
                                          double& fy, double& fz, double& pe, bool& overlap) {
+  if (PLANAR) {
+    sell_row_pipe<MI>(pl, ps, (int)(ps - 1), row, mq, qmax, pi, nx, ny, nz, b, c, fx, fy, fz,
+                      pe, overlap);
+    return;
+  }
   int4 nxt = make_int4(0, 0, 0, 0);
   if (mq > 0) nxt = __ldg(row);
   for (int q = 0; q < qmax; ++q) {
@@ -249,7 +286,7 @@ __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
 }
 
 template <bool PLANAR>
-__global__ void __launch_bounds__(kForceThreads, 3)
+__global__ void __launch_bounds__(kForceThreads, PLANAR ? 2 : 3)
 lj_force_sell_kernel(const double* __restrict__ pos, const double* __restrict__ pl, int64_t ps,
                      int n_rows, const int* __restrict__ count,
                      const int4* __restrict__ nbr, int Q, pc_box b, LJConst c, double guard,
