@@ -257,6 +257,37 @@ int pc_box_min_image(double* d_x, int64_t rows, int32_t d, const pc_box* box, vo
 int pc_lj_pair(const double* d_dx, const double* d_r2, int64_t n, double eps, double sigma,
                double* d_e, double* d_f, void* stream);
 
+/* ---- domain decomposition (ref decomp.py) -------------------------------- */
+/* Owning rank of each (n, d) position: ravel(min(floor((x-low)/block), dims-1))
+ * with `fabric` describing the rank grid (width = block lengths, nc = dims);
+ * outside the global box -> d_flag bit 0 (ref decomp.py:58-66). */
+int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
+                int32_t* d_owner, int32_t* d_flag, void* stream);
+/* Wrapped position outside the box on a non-periodic axis -> d_flag bit 3
+ * (ref decomp.py:92-96). */
+int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* box,
+                         int32_t* d_flag, void* stream);
+/* Halo export planning for one source rank (ref decomp.py:143-228): n_off
+ * candidate images in product order (host arrays: destination slot, shift,
+ * destination box lo/hi, each d wide); per particle and slot the best image
+ * (strict <, first wins) is exported iff its squared distance to the box is
+ * < w2.  Writes d_flags[slot*n + i] (int32 0/1) and d_best_off (int8). */
+int pc_halo_plan(const double* d_x, int64_t n, int32_t d, int32_t n_off, const int32_t* h_slot,
+                 const double* h_shift, const double* h_lo, const double* h_hi,
+                 int32_t n_slots, double w2, int32_t* d_flags, int8_t* d_best_off,
+                 void* stream);
+/* Stable compaction: out_idx[pos[i]] = i (and its offset code) where flag[i]. */
+int pc_compact(const int32_t* d_flag, const int32_t* d_pos, int64_t n, int32_t* d_out_idx,
+               const int8_t* d_best_off, int8_t* d_out_off, void* stream);
+/* dst[k] = src[idx[k]] (+ shift[k]) over rows of w doubles (ghost staging,
+ * ref decomp.py:243-246). */
+int pc_gather_shift(const double* d_src, const int32_t* d_idx, int64_t m, int32_t w,
+                    const double* d_shift, double* d_dst, void* stream);
+/* dst[idx[k]] += src[k] over rows of w doubles, idx distinct per call
+ * (one destination's ghost block of ref decomp.py:281-289). */
+int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,
+                   const double* d_src, void* stream);
+
 /* Sum per-block partials (nblocks x 5) into out[5] in a fixed order. */
 int pc_reduce_partials(const double* d_partial, int32_t nblocks, double* d_out,
                        void* stream);

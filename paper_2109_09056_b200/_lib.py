@@ -85,6 +85,15 @@ SIGNATURES = {
                                          ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_vp,
                                          c_vp, c_vp, ctypes.POINTER(c_i32), c_vp]),
     "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
+    "pc_owner_of": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_vp,
+                                   c_vp]),
+    "pc_check_nonperiodic": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcBox), c_vp,
+                                            c_vp]),
+    "pc_halo_plan": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
+                                    c_dbl, c_vp, c_vp, c_vp]),
+    "pc_compact": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "pc_gather_shift": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "pc_scatter_add": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
                                         ctypes.POINTER(PcBox),
                                         ctypes.POINTER(PcLJ), c_dbl, c_vp, c_i64, c_vp, c_i64,

@@ -1,0 +1,207 @@
+// Spatial decomposition kernels: ownership, halo export planning, shifted
+// ghost staging and the reverse (scatter-add) halo.  Replace the numpy bodies
+// of ref decomp.py:58-66 (owner_of), :115-228 (build_halo), :231-260
+// (halo_gather staging) and :263-300 (halo_scatter).
+#include "pc_common.cuh"
+
+namespace pc {
+
+constexpr int kMaxSlots = 26;
+
+// One candidate image of a source rank's particles (ref decomp.py:164-194):
+// destination slot, periodic shift and destination box.
+struct HaloOffset {
+  int slot;            // index of the destination among this rank's distinct dests
+  double shift[3];
+  double lo[3], hi[3];
+};
+
+struct HaloTable {
+  int n_off;                       // offsets in product order (<= 26)
+  int n_slots;                     // distinct destinations
+  int d;                           // dimensionality
+  double w2;
+  HaloOffset off[kMaxSlots];
+};
+
+// owner = ravel(min(floor((x - low) / bl), dims - 1)); outside the global
+// box -> flag bit 0 (ValueError, ref decomp.py:62-63).
+__global__ void owner_kernel(const double* __restrict__ x, int64_t n, int d, pc_grid g,
+                             int* __restrict__ owner, int* __restrict__ flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c[3] = {0, 0, 0};
+  bool outside = false;
+  for (int a = 0; a < d; ++a) {
+    const double v = x[i * d + a];
+    outside |= (v < g.low[a]) || (v > g.high[a]);
+    double q = floor(__ddiv_rn(__dsub_rn(v, g.low[a]), g.width[a]));
+    int ci = (int)q;
+    if (q >= (double)g.nc[a]) ci = g.nc[a] - 1;
+    c[a] = ci;
+  }
+  if (outside) atomicOr(flag, kFlagOutside);
+  owner[i] = (c[0] * g.nc[1] + c[1]) * g.nc[2] + c[2];
+}
+
+// Non-periodic axis: wrapped position outside [low, high] -> flag bit 3
+// (ref decomp.py:92-96).
+__global__ void nonperiodic_check_kernel(const double* __restrict__ x, int64_t n, int d,
+                                         pc_box b, int* __restrict__ flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int a = 0; a < d; ++a) {
+    if (b.periodic[a]) continue;
+    const double v = x[i * d + a];
+    if (v < b.low[a] || v > b.high[a]) atomicOr(flag, kFlagNonPeriodic);
+  }
+}
+
+// Squared distance of x + shift to the closed box, einsum order (x^2+z^2)+y^2
+// for d = 3 (ref decomp.py:115-120).
+__device__ __forceinline__ double dist2_box(const double* x, const HaloOffset& o, int d) {
+  double t[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < d; ++a) {
+    const double p = __dadd_rn(x[a], o.shift[a]);
+    const double below = fmax(__dsub_rn(o.lo[a], p), 0.0);
+    const double above = fmax(__dsub_rn(p, o.hi[a]), 0.0);
+    const double s = __dadd_rn(below, above);
+    t[a] = __dmul_rn(s, s);
+  }
+  if (d == 3) return __dadd_rn(__dadd_rn(t[0], t[2]), t[1]);
+  if (d == 2) return __dadd_rn(t[0], t[1]);
+  return t[0];
+}
+
+// Per particle: best image per destination (strict <, first offset in
+// product order wins ties), export iff best d2 < w^2.  Writes flags[slot][i]
+// (0/1 int32) and the winning offset per slot.
+__global__ void halo_plan_kernel(const double* __restrict__ x, int64_t n, HaloTable t,
+                                 int* __restrict__ flags, int8_t* __restrict__ best_off) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xi[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < t.d; ++a) xi[a] = x[i * t.d + a];
+  double best[kMaxSlots];
+  int bo[kMaxSlots];
+  for (int s = 0; s < t.n_slots; ++s) { best[s] = INFINITY; bo[s] = -1; }
+  for (int k = 0; k < t.n_off; ++k) {
+    const int s = t.off[k].slot;
+    const double d2 = dist2_box(xi, t.off[k], t.d);
+    if (bo[s] < 0 || d2 < best[s]) { best[s] = d2; bo[s] = k; }
+  }
+  for (int s = 0; s < t.n_slots; ++s) {
+    flags[(int64_t)s * n + i] = best[s] < t.w2 ? 1 : 0;
+    best_off[(int64_t)s * n + i] = (int8_t)bo[s];
+  }
+}
+
+// Stable compaction of one slot: idx[pos[i]] = i where flag[i].
+__global__ void compact_kernel(const int* __restrict__ flag, const int* __restrict__ pos,
+                               int64_t n, int* __restrict__ out_idx,
+                               const int8_t* __restrict__ best_off, int8_t* __restrict__ out_off) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  out_idx[pos[i]] = (int)i;
+  out_off[pos[i]] = best_off[i];
+}
+
+// dst[k] = src[idx[k]] (+ shift[k] for the position field): (m, w) doubles.
+__global__ void gather_shift_kernel(const double* __restrict__ src, const int* __restrict__ idx,
+                                    int64_t m, int w, const double* __restrict__ shift,
+                                    double* __restrict__ dst) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t k = t / w;
+  int c = (int)(t - k * w);
+  if (k >= m) return;
+  double v = src[(int64_t)idx[k] * w + c];
+  if (shift) v = __dadd_rn(v, shift[k * w + c]);
+  dst[t] = v;
+}
+
+// dst[idx[k]] += src[k] over (m, w) doubles; idx distinct within one call.
+__global__ void scatter_add_kernel(double* __restrict__ dst, const int* __restrict__ idx,
+                                   int64_t m, int w, const double* __restrict__ src) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t k = t / w;
+  int c = (int)(t - k * w);
+  if (k >= m) return;
+  double* p = dst + (int64_t)idx[k] * w + c;
+  *p = __dadd_rn(*p, src[t]);
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+extern "C" {
+
+int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
+                int32_t* d_owner, int32_t* d_flag, void* stream) {
+  if (n <= 0) return PC_OK;
+  owner_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_x, n, d, *fabric,
+                                                                           d_owner, d_flag);
+  return check_launch("pc_owner_of");
+}
+
+int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* box,
+                         int32_t* d_flag, void* stream) {
+  if (n <= 0) return PC_OK;
+  nonperiodic_check_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_x, n, d, *box, d_flag);
+  return check_launch("pc_check_nonperiodic");
+}
+
+int pc_halo_plan(const double* d_x, int64_t n, int32_t d, int32_t n_off, const int32_t* h_slot,
+                 const double* h_shift, const double* h_lo, const double* h_hi, int32_t n_slots,
+                 double w2, int32_t* d_flags, int8_t* d_best_off, void* stream) {
+  if (n <= 0) return PC_OK;
+  if (n_off > kMaxSlots || n_slots > kMaxSlots || d < 1 || d > 3) {
+    set_error("pc_halo_plan: too many offsets or bad dimension");
+    return PC_ERR_VALUE;
+  }
+  HaloTable t;
+  t.n_off = n_off;
+  t.n_slots = n_slots;
+  t.d = d;
+  t.w2 = w2;
+  for (int k = 0; k < n_off; ++k) {
+    t.off[k].slot = h_slot[k];
+    for (int a = 0; a < 3; ++a) {
+      t.off[k].shift[a] = a < d ? h_shift[k * d + a] : 0.0;
+      t.off[k].lo[a] = a < d ? h_lo[k * d + a] : 0.0;
+      t.off[k].hi[a] = a < d ? h_hi[k * d + a] : 0.0;
+    }
+  }
+  halo_plan_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(d_x, n, t, d_flags,
+                                                                               d_best_off);
+  return check_launch("pc_halo_plan");
+}
+
+int pc_compact(const int32_t* d_flag, const int32_t* d_pos, int64_t n, int32_t* d_out_idx,
+               const int8_t* d_best_off, int8_t* d_out_off, void* stream) {
+  if (n <= 0) return PC_OK;
+  compact_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_flag, d_pos, n, d_out_idx, d_best_off, d_out_off);
+  return check_launch("pc_compact");
+}
+
+int pc_gather_shift(const double* d_src, const int32_t* d_idx, int64_t m, int32_t w,
+                    const double* d_shift, double* d_dst, void* stream) {
+  int64_t t = m * w;
+  if (t <= 0) return PC_OK;
+  gather_shift_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_src, d_idx, m, w, d_shift, d_dst);
+  return check_launch("pc_gather_shift");
+}
+
+int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,
+                   const double* d_src, void* stream) {
+  int64_t t = m * w;
+  if (t <= 0) return PC_OK;
+  scatter_add_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(d_dst, d_idx,
+                                                                                 m, w, d_src);
+  return check_launch("pc_scatter_add");
+}
+
+}  // extern "C"
