@@ -189,8 +189,18 @@ def run_ours(args):
 
     kw = md_kwargs(args, args.cells)
     cfg = pc.md.MDConfig(**kw, steps=args.steps)
-    drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar")
-    n = drv.n
+    if world > 1:
+        # weak scaling: a 64^3-cell block per GPU, spatial decomposition with
+        # ghost halo over NCCL (paper_2109_09056_b200.dist)
+        from paper_2109_09056_b200.dist import DistMD, rank_dims_for
+        dims = rank_dims_for(world)
+        cfg.rank_dims = dims
+        drv = DistMD(cfg, cells=[args.cells * d for d in dims], local_init=True)
+        eng = drv.engine
+    else:
+        drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar")
+        eng = drv
+    n = drv.n                      # global atoms
     W, K = args.warmup, args.steps
     for s in range(1, W + 1):
         drv.step(s)
@@ -198,7 +208,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     lib = _lib.load()
-    drv.force_events = []
+    eng.force_events = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = lib.pc_launch_count()
     with ClockSampler(local) as clk:
@@ -215,17 +225,19 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         ms = float(t.item())
-    value = n * world * K / (ms * 1e-3)
+    value = n * K / (ms * 1e-3)
     diag = drv.diagnostics()
-    force_ms = [a.elapsed_time(b) for a, b in drv.force_events]
-    drv.force_events = None
-    kmean = float(drv.cnt[:n].float().mean().item())
+    force_ms = [a.elapsed_time(b) for a, b in eng.force_events]
+    eng.force_events = None
+    n_rows = eng.n_total if world > 1 else n          # rows this rank's force kernel sweeps
+    n_local = eng.n_owned if world > 1 else n
+    kmean = float(eng.cnt[:n_rows].float().sum().item()) / max(1, n_local)
     # algorithmic bytes per force launch per atom: Verlet indices
     # 4k + row count 4 + pos4 read once 32 (L2-resident afterwards) + FP64
     # force write 24 + fused final kick v read+write 48
     bytes_per_atom = 4 * kmean + 4 + 32 + 24 + 48
     force_avg_s = float(np.mean(force_ms)) * 1e-3
-    achieved = n * bytes_per_atom / force_avg_s / 1e9
+    achieved = n_local * bytes_per_atom / force_avg_s / 1e9
     peak, peak_kind = measured_peak()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "force_traffic.json")
@@ -235,7 +247,7 @@ def run_ours(args):
             traffic = None if traffic is None else traffic * n
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         e2e = run_e2e(pc, kw, args.e2e_steps, world)
 
     cpu = None

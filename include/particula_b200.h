@@ -161,7 +161,9 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
                  int32_t half, int32_t mode, int32_t out_tags,
                  int32_t* d_count, const int64_t* d_offsets, int32_t* d_index,
                  int64_t ell_stride, int32_t ell_width, int32_t* d_flag,
-                 void* stream);
+                 void* stream,
+                 const double* d_posb /* binning positions (NULL: d_pos_sorted) */,
+                 const pc_box* box_exact /* min-image box of the predicate (NULL: box) */);
 
 /* MD hot-path build into the SELL-32x4 layout the force kernel reads: entry
  * k of row a at int word ((a>>5)*(width/4) + k/4)*128 + (a&31)*4 + k%4,
@@ -171,11 +173,15 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
  * cells, else the per-particle kernel.  d_flag bit 1: a row exceeded width
  * (counts exact, caller grows and rebuilds); bit 4: staging capacity
  * exceeded (caller rebuilds with pc_nbr_build).  *h_used_staged reports the
- * kernel chosen. */
+ * kernel chosen.  Decomposed domains bin owned+ghost particles by d_posb
+ * (ghosts shifted by their periodic image into the local frame) on a local
+ * grid/box while the FP64 predicate uses the raw positions and the global
+ * box_exact, exactly the reference's ghost convention (md.py:181-188). */
 int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_start,
                       const pc_grid* grid, const pc_box* box, double cutoff2,
                       int32_t width, int32_t dummy, int32_t* d_count, int32_t* d_index,
-                      int32_t* d_flag, int32_t* h_used_staged, void* stream);
+                      int32_t* d_flag, int32_t* h_used_staged, void* stream,
+                      const double* d_posb, const pc_box* box_exact);
 
 /* CSR -> dense (n, width) int64 table, -1 padded (ref neighbors.py:130-134). */
 int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,
@@ -283,6 +289,12 @@ int pc_compact(const int32_t* d_flag, const int32_t* d_pos, int64_t n, int32_t* 
  * ref decomp.py:243-246). */
 int pc_gather_shift(const double* d_src, const int32_t* d_idx, int64_t m, int32_t w,
                     const double* d_shift, double* d_dst, void* stream);
+/* Per-step halo refresh: buf[k] = pos4[rows[k]].xyz (pack) and
+ * pos4[rows[k]].xyz = buf[k] (+ planar copy) (unpack), buf (m, 3) f64. */
+int pc_halo_pack(const double* d_pos, const int32_t* d_rows, int64_t m, double* d_buf,
+                 void* stream);
+int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double* d_pos,
+                   double* d_planar, int64_t planar_stride, void* stream);
 /* dst[idx[k]] += src[k] over rows of w doubles, idx distinct per call
  * (one destination's ghost block of ref decomp.py:281-289). */
 int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,

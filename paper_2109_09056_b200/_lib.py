@@ -79,11 +79,13 @@ SIGNATURES = {
     "pc_invert_order": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "pc_nbr_build": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
                                     ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_i32,
-                                    c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+                                    c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp,
+                                    ctypes.POINTER(PcBox)]),
     "pc_sort_rows": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
     "pc_nbr_build_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
                                          ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_vp,
-                                         c_vp, c_vp, ctypes.POINTER(c_i32), c_vp]),
+                                         c_vp, c_vp, ctypes.POINTER(c_i32), c_vp, c_vp,
+                                         ctypes.POINTER(PcBox)]),
     "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
     "pc_owner_of": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_vp,
                                    c_vp]),
@@ -94,6 +96,8 @@ SIGNATURES = {
     "pc_compact": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "pc_gather_shift": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "pc_scatter_add": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "pc_halo_pack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "pc_halo_unpack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
                                         ctypes.POINTER(PcBox),
                                         ctypes.POINTER(PcLJ), c_dbl, c_vp, c_i64, c_vp, c_i64,

@@ -130,6 +130,36 @@ __global__ void scatter_add_kernel(double* __restrict__ dst, const int* __restri
   *p = __dadd_rn(*p, src[t]);
 }
 
+// Per-step halo refresh (ref md.py:192-200 / decomp.py:231-260 with the
+// plan cached): pack the raw x, y, z of exported rows into a contiguous send
+// buffer; unpack a received buffer into the ghost rows (+ planar copy).
+__global__ void halo_pack_kernel(const double* __restrict__ pos, const int* __restrict__ rows,
+                                 int64_t m, double* __restrict__ buf) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const double4 p = ld_pos4(pos + 4 * (int64_t)rows[k]);
+  buf[3 * k] = p.x;
+  buf[3 * k + 1] = p.y;
+  buf[3 * k + 2] = p.z;
+}
+
+__global__ void halo_unpack_kernel(const double* __restrict__ buf, const int* __restrict__ rows,
+                                   int64_t m, double* __restrict__ pos,
+                                   double* __restrict__ planar, int64_t ps) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int r = rows[k];
+  const double x = buf[3 * k], y = buf[3 * k + 1], z = buf[3 * k + 2];
+  pos[4 * (int64_t)r] = x;
+  pos[4 * (int64_t)r + 1] = y;
+  pos[4 * (int64_t)r + 2] = z;
+  if (planar) {
+    planar[r] = x;
+    planar[ps + r] = y;
+    planar[2 * ps + r] = z;
+  }
+}
+
 }  // namespace pc
 
 using namespace pc;
@@ -193,6 +223,22 @@ int pc_gather_shift(const double* d_src, const int32_t* d_idx, int64_t m, int32_
   gather_shift_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(
       d_src, d_idx, m, w, d_shift, d_dst);
   return check_launch("pc_gather_shift");
+}
+
+int pc_halo_pack(const double* d_pos, const int32_t* d_rows, int64_t m, double* d_buf,
+                 void* stream) {
+  if (m <= 0) return PC_OK;
+  halo_pack_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(d_pos, d_rows, m,
+                                                                               d_buf);
+  return check_launch("pc_halo_pack");
+}
+
+int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double* d_pos,
+                   double* d_planar, int64_t planar_stride, void* stream) {
+  if (m <= 0) return PC_OK;
+  halo_unpack_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_buf, d_rows, m, d_pos, d_planar, planar_stride);
+  return check_launch("pc_halo_unpack");
 }
 
 int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,

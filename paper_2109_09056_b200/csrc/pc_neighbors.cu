@@ -16,17 +16,18 @@ nbr_build_kernel(const double* __restrict__ pos, int n, const int* __restrict__ 
                  pc_grid g, pc_box b, double cutoff2, int half, int out_tags,
                  int* __restrict__ count, const int64_t* __restrict__ offsets,
                  int* __restrict__ index, int64_t ell_stride, int ell_width,
-                 int* __restrict__ flag) {
+                 int* __restrict__ flag, const double* __restrict__ posb, pc_box e) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double4 pi = ld_pos4(pos + 4 * (int64_t)i);
+  const double4 bi = ld_pos4(posb + 4 * (int64_t)i);
   const int64_t ti = tag_of(pi.w);
   int sx[3], sy[3], sz[3];
-  int nx = axis_stencil(cell_coord(pi.x, g.low[0], g.width[0], g.nc[0]), g.nc[0],
+  int nx = axis_stencil(cell_coord(bi.x, g.low[0], g.width[0], g.nc[0]), g.nc[0],
                         b.periodic[0], sx);
-  int ny = axis_stencil(cell_coord(pi.y, g.low[1], g.width[1], g.nc[1]), g.nc[1],
+  int ny = axis_stencil(cell_coord(bi.y, g.low[1], g.width[1], g.nc[1]), g.nc[1],
                         b.periodic[1], sy);
-  int nz = axis_stencil(cell_coord(pi.z, g.low[2], g.width[2], g.nc[2]), g.nc[2],
+  int nz = axis_stencil(cell_coord(bi.z, g.low[2], g.width[2], g.nc[2]), g.nc[2],
                         b.periodic[2], sz);
   int64_t row = 0;
   if (MODE == PC_NBR_CSR) row = offsets[i];
@@ -46,9 +47,9 @@ nbr_build_kernel(const double* __restrict__ pos, int n, const int* __restrict__ 
         for (int j = jb; j < je; ++j) {
           if (j == i) continue;
           const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
-          const double dx = min_image(__dsub_rn(pj.x, pi.x), b.length[0], b.mi_thresh[0]);
-          const double dy = min_image(__dsub_rn(pj.y, pi.y), b.length[1], b.mi_thresh[1]);
-          const double dz = min_image(__dsub_rn(pj.z, pi.z), b.length[2], b.mi_thresh[2]);
+          const double dx = min_image(__dsub_rn(pj.x, pi.x), e.length[0], e.mi_thresh[0]);
+          const double dy = min_image(__dsub_rn(pj.y, pi.y), e.length[1], e.mi_thresh[1]);
+          const double dz = min_image(__dsub_rn(pj.z, pi.z), e.length[2], e.mi_thresh[2]);
           if (r2_exact(dx, dy, dz) < cutoff2) {
             const int64_t tj = tag_of(pj.w);
             if (half && !(tj > ti)) continue;
@@ -115,7 +116,8 @@ template <int MODE>
 __global__ void __launch_bounds__(kBuildThreads)
 nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __restrict__ cell_start,
                         pc_grid g, pc_box b, StagedParams p, int* __restrict__ count,
-                        int* __restrict__ index, int* __restrict__ flag) {
+                        int* __restrict__ index, int* __restrict__ flag,
+                        const double* __restrict__ posb, pc_box e) {
   extern __shared__ float4 stage[];
   __shared__ int cell_off[9][kStageCells + 1];   // staged offset of each cell per column
   __shared__ int cell_src[9][kStageCells];       // first global index of each staged cell
@@ -181,7 +183,7 @@ nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __rest
       const int dst = cell_off[c][k];
       const double sx = cell_shift[c][k][0], sy = cell_shift[c][k][1], sz = cell_shift[c][k][2];
       for (int t = threadIdx.x; t < m; t += blockDim.x) {
-        const double4 q = ld_pos4(pos + 4 * (int64_t)(src + t));
+        const double4 q = ld_pos4(posb + 4 * (int64_t)(src + t));
         float4 s;
         s.x = (float)(q.x + sx - ox);
         s.y = (float)(q.y + sy - oy);
@@ -219,7 +221,7 @@ nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __rest
             const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
             j = __float_as_int(q.w);
             if (r2 < p.hi2 && j != a)
-              hit = r2 < p.lo2 || exact_pair(pos, a, j, b, p.cutoff2);
+              hit = r2 < p.lo2 || exact_pair(pos, a, j, e, p.cutoff2);
           }
           const unsigned m = __ballot_sync(0xffffffffu, hit);
           if (MODE == PC_NBR_SELL && hit) {
@@ -289,8 +291,10 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
                  const pc_grid* grid, const pc_box* box, double cutoff2, int32_t half,
                  int32_t mode, int32_t out_tags, int32_t* d_count, const int64_t* d_offsets,
                  int32_t* d_index, int64_t ell_stride, int32_t ell_width, int32_t* d_flag,
-                 void* stream) {
+                 void* stream, const double* d_posb, const pc_box* box_exact) {
   if (n <= 0) return PC_OK;
+  const double* posb = d_posb ? d_posb : d_pos_sorted;
+  const pc_box ebox = box_exact ? *box_exact : *box;
   if (mode == PC_NBR_CSR && d_offsets == nullptr) {
     set_error("pc_nbr_build: CSR mode needs offsets");
     return PC_ERR_VALUE;
@@ -305,17 +309,17 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
     case PC_NBR_COUNT:
       nbr_build_kernel<PC_NBR_COUNT><<<blocks, 128, 0, s>>>(
           d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
-          d_offsets, d_index, ell_stride, ell_width, d_flag);
+          d_offsets, d_index, ell_stride, ell_width, d_flag, posb, ebox);
       break;
     case PC_NBR_CSR:
       nbr_build_kernel<PC_NBR_CSR><<<blocks, 128, 0, s>>>(
           d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
-          d_offsets, d_index, ell_stride, ell_width, d_flag);
+          d_offsets, d_index, ell_stride, ell_width, d_flag, posb, ebox);
       break;
     case PC_NBR_ELL:
       nbr_build_kernel<PC_NBR_ELL><<<blocks, 128, 0, s>>>(
           d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
-          d_offsets, d_index, ell_stride, ell_width, d_flag);
+          d_offsets, d_index, ell_stride, ell_width, d_flag, posb, ebox);
       break;
     case PC_NBR_SELL:
       if (ell_width % 4) {
@@ -324,7 +328,7 @@ int pc_nbr_build(const double* d_pos_sorted, int32_t n, const int32_t* d_cell_st
       }
       nbr_build_kernel<PC_NBR_SELL><<<blocks, 128, 0, s>>>(
           d_pos_sorted, n, d_cell_start, *grid, *box, cutoff2, half, out_tags, d_count,
-          d_offsets, d_index, ell_stride, ell_width, d_flag);
+          d_offsets, d_index, ell_stride, ell_width, d_flag, posb, ebox);
       break;
     default:
       set_error("pc_nbr_build: unknown mode %d", mode);
@@ -350,7 +354,8 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
                                  const int32_t* d_cell_start, const pc_grid* grid,
                                  const pc_box* box, double cutoff2, int32_t width,
                                  int32_t dummy, int32_t* d_count, int32_t* d_index,
-                                 int32_t* d_flag, int32_t* h_used_staged, void* stream) {
+                                 int32_t* d_flag, int32_t* h_used_staged, void* stream,
+                                 const double* d_posb, const pc_box* box_exact) {
   using namespace pc;
   if (n <= 0) return PC_OK;
   if (width % 4 || width <= 0) {
@@ -363,7 +368,8 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
   if (h_used_staged) *h_used_staged = staged ? 1 : 0;
   if (!staged) {
     return pc_nbr_build(d_pos_sorted, n, d_cell_start, grid, box, cutoff2, 0, PC_NBR_SELL, 0,
-                        d_count, nullptr, d_index, dummy, width, d_flag, stream);
+                        d_count, nullptr, d_index, dummy, width, d_flag, stream, d_posb,
+                        box_exact);
   }
   // FP32 prefilter band (see header comment of nbr_build_staged_kernel)
   double U = 0.0;
@@ -389,6 +395,7 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
   }
   const int64_t blocks = (int64_t)grid->nc[0] * grid->nc[1] * p.nseg;
   nbr_build_staged_kernel<PC_NBR_SELL><<<(unsigned)blocks, kBuildThreads, stage_bytes, s>>>(
-      d_pos_sorted, n, d_cell_start, *grid, *box, p, d_count, d_index, d_flag);
+      d_pos_sorted, n, d_cell_start, *grid, *box, p, d_count, d_index, d_flag,
+      d_posb ? d_posb : d_pos_sorted, box_exact ? *box_exact : *box);
   return check_launch("pc_nbr_build_sell");
 }

@@ -1,0 +1,692 @@
+"""Multi-GPU LJ MD by spatial domain decomposition (one rank per GPU).
+
+The reference simulates its ranks in one process (ref decomp.py:1-8, md.py
+MDDriver with ``rank_dims``): every rank owns a block of a uniform Cartesian
+split, carries ghost copies of the particles within the halo width
+``(rc + skin)(1 + 1e-9)`` of its block, migrates particles at every neighbor
+rebuild and refreshes ghost positions on every other step, with the cached
+halo plan (md.py:169-200).  This module is the same algorithm with one rank
+per GPU:
+
+* ``DomainEngine`` -- one rank's device-resident state and phases.  Owned and
+  ghost particles share one array sorted by a local linked-cell grid that
+  covers the block plus its halo (``binpos``: ghosts shifted by their
+  periodic image); the FP64 pair predicate and the forces use the raw
+  positions with the global minimum image, exactly the reference's ghost
+  convention (md.py:181-188), so the neighbor sets are the single-domain ones.
+* phases produce per-destination float64 row blocks ("outboxes") and consume
+  per-source blocks ("inboxes") in ascending source order -- the reference's
+  deterministic delivery (decomp.py:5-7).
+* ``NCCLTransport`` moves the blocks between processes (``torch.distributed``
+  send/recv batched per exchange, counts first via all_gather; NCCL over
+  NVLink/NVSwitch on a B200 box, gloo in the CPU tests);
+  ``FabricMD`` runs all ranks in one process on one device (the reference's
+  in-process fabric) by routing the blocks directly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from ._lib import call, ptr, stream
+from .decomp import DomainFabric, decompose
+from .geometry import Box
+from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, fcc_lattice, \
+    initial_velocities
+
+MIG_W = 7     # migrate row: x, y, z, vx, vy, vz, gid (int64 bits)
+HALO_W = 7    # halo row: x, y, z, gid bits, shift x, y, z
+
+
+def rank_dims_for(world: int):
+    """Rank grid of BASELINE configs: 1 -> 1x1x1, 2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2."""
+    table = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+    if world in table:
+        return table[world]
+    dims = [1, 1, 1]
+    w, a = world, 0
+    for p in (2, 3, 5, 7):
+        while w % p == 0:
+            dims[a % 3] *= p
+            w //= p
+            a += 1
+    if w != 1:
+        dims[0] *= w
+    return tuple(dims)
+
+
+def _as_f64(t):
+    return t.view(torch.float64) if t.dtype == torch.int64 else t
+
+
+class DomainEngine:
+    """One rank's particles and kernels (owned + ghost rows in one array)."""
+
+    def __init__(self, cfg: MDConfig, fabric: DomainFabric, rank: int, x, v, gid, device,
+                 ell_width: int = 128, planar_gather: bool = True, time_phases: bool = False):
+        self.cfg = cfg
+        self.fabric = fabric
+        self.rank = rank
+        self.device = torch.device(device)
+        gb = fabric.global_box
+        self.box = gb
+        self.periodic = np.array(fabric.periodic)
+        self.search = (cfg.cutoff + cfg.skin) * _CUTOFF_MARGIN
+        self.halo_width = self.search
+        if self.halo_width > fabric.block_lengths.min():
+            raise ValueError("cutoff + skin exceeds the local box edge for this rank grid")
+        self._gbox = _lib.make_box(gb.low, gb.high, self.periodic)
+        self._lj = _lj_params(cfg.epsilon, cfg.sigma, cfg.cutoff)
+        self._dtm = 0.5 * cfg.dt / cfg.mass
+        self._search2 = self.search * self.search
+        self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
+        self.ell_width = -(-int(ell_width) // 4) * 4
+        self.planar_gather = planar_gather
+        self._time = time_phases
+        self.timer = _PhaseTimer()
+        self._local_grid()
+        self._offsets = self._halo_offsets()
+        n = int(x.shape[0])
+        self.cap = 0
+        self._alloc(max(64, int(n * 1.6) + 64))
+        self.n_owned, self.n_total = n, n
+        if n:
+            self.pos[:n, :3] = x.to(self.device, torch.float64)
+            self.pos[:n, 3] = gid.to(self.device, torch.int64).view(torch.float64)
+            self.vel[:, :n] = v.to(self.device, torch.float64).t()
+        self.is_ghost = torch.zeros(self.cap, dtype=torch.int32, device=self.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.build_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.export_rows = {}     # dest -> int32 sorted rows (per-step pack)
+        self.ghost_blocks = []    # [(src, int32 sorted rows)] ascending src
+        self.rebuilds = 0
+        self.force_events = None  # optional [(start, end)] CUDA events per force launch
+
+    # ---- geometry -----------------------------------------------------------
+    def _local_grid(self):
+        """Cells >= search over the block + halo on decomposed axes; the full
+        periodic length on undecomposed axes (self-images by min image)."""
+        f, gb = self.fabric, self.fabric.global_box
+        lb = f.local_box(self.rank)
+        lo, hi, per = np.zeros(3), np.zeros(3), np.zeros(3, bool)
+        for a in range(3):
+            if f.rank_dims[a] == 1:
+                lo[a], hi[a], per[a] = gb.low[a], gb.high[a], bool(self.periodic[a])
+            else:
+                lo[a], hi[a] = lb.low[a] - self.halo_width, lb.high[a] + self.halo_width
+        ext = hi - lo
+        nc = np.maximum(1, np.floor(ext / self.search).astype(np.int64))
+        self.lbox_lo, self.lbox_hi, self.lbox_per = lo, hi, per
+        self._lbox = _lib.make_box(lo, hi, per)
+        self._grid = _lib.make_grid(lo, hi, ext / nc, nc)
+
+    def _halo_offsets(self):
+        f = self.fabric
+        d = 3
+        L = f.global_box.lengths
+        me = f.coords_of(self.rank)
+        out = []
+        for off in itertools.product((-1, 0, 1), repeat=d):
+            if not any(off):
+                continue
+            tgt = me + np.array(off)
+            shift = np.zeros(d)
+            ok = True
+            for a in range(d):
+                if 0 <= tgt[a] < f.rank_dims[a]:
+                    continue
+                if not f.periodic[a]:
+                    ok = False
+                    break
+                if tgt[a] < 0:
+                    tgt[a] += f.rank_dims[a]
+                    shift[a] = L[a]
+                else:
+                    tgt[a] -= f.rank_dims[a]
+                    shift[a] = -L[a]
+            if not ok:
+                continue
+            dest = f.rank_of(tgt)
+            if dest != self.rank:
+                out.append((dest, shift))
+        dests = sorted(set(dst for dst, _ in out))
+        slot = {dst: k for k, dst in enumerate(dests)}
+        h_slot = np.array([slot[dst] for dst, _ in out], np.int32)
+        h_shift = np.ascontiguousarray(np.stack([s for _, s in out])) if out else np.zeros((0, 3))
+        lo = np.stack([f.local_box(dst).low for dst, _ in out]) if out else np.zeros((0, 3))
+        hi = np.stack([f.local_box(dst).high for dst, _ in out]) if out else np.zeros((0, 3))
+        return {"dests": dests, "slot": h_slot, "shift": h_shift.astype(np.float64),
+                "lo": np.ascontiguousarray(lo, np.float64),
+                "hi": np.ascontiguousarray(hi, np.float64)}
+
+    # ---- storage -------------------------------------------------------------
+    def _alloc(self, cap):
+        dev = self.device
+        old = None
+        if self.cap:
+            old = (self.pos, self.vel, self.n_total)
+        self.cap = int(cap)
+        self.pos = torch.zeros((self.cap + 1, 4), dtype=torch.float64, device=dev)
+        self.pos[self.cap, :3] = float("nan")
+        self.pos[self.cap, 3] = torch.tensor(-1, dtype=torch.int64).view(torch.float64)
+        self.binpos = torch.zeros_like(self.pos)
+        self.vel = torch.zeros((3, self.cap), dtype=torch.float64, device=dev)
+        self.frc = torch.zeros((3, self.cap), dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(self.cap, dtype=torch.int32, device=dev)
+        slices = -(-self.cap // 32)
+        self.nbr = torch.empty(slices * self.ell_width * 32, dtype=torch.int32, device=dev)
+        self.pl = None
+        if self.planar_gather:
+            self.pl = torch.empty((3, self.cap + 1), dtype=torch.float64, device=dev)
+            self.pl[:, self.cap] = float("nan")
+        self._nblk = int(_lib.load().pc_lj_force_sell_partials(self.cap))
+        self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
+        self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
+        if old is not None:
+            p, v, n = old
+            self.pos[:n] = p[:n]
+            self.vel[:, :n] = v[:, :n]
+
+    def _ensure(self, n):
+        if n > self.cap:
+            keep_ghost = None
+            self._alloc(int(n * 1.3) + 64)
+            self.is_ghost = torch.zeros(self.cap, dtype=torch.int32, device=self.device)
+            del keep_ghost
+
+    def _t0(self):
+        return self.timer.start() if self._time else None
+
+    def _t1(self, phase, e0):
+        if self._time:
+            self.timer.stop(phase, e0)
+
+    # ---- phases --------------------------------------------------------------
+    def integrate(self):
+        e0 = self._t0()
+        call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
+             self.cap, self.n_total, self._dtm, float(self.cfg.dt), self._gbox, ptr(self.pl),
+             self.cap + 1, stream())
+        self._t1("integrate", e0)
+
+    def _owned_rows(self):
+        """Rows of owned particles in current order (drop ghosts, decomp.py:86-88)."""
+        n = self.n_total
+        if self.n_total == self.n_owned:
+            return None
+        own = (1 - self.is_ghost[:n]).contiguous()
+        pos = _kernels.scan_i32(own)
+        m = int(pos[n].item())
+        rows = torch.empty(max(m, 1), dtype=torch.int32, device=self.device)
+        dummy = torch.zeros(max(n, 1), dtype=torch.int8, device=self.device)
+        dummy_o = torch.empty(max(m, 1), dtype=torch.int8, device=self.device)
+        call("pc_compact", ptr(own), ptr(pos), n, ptr(rows), ptr(dummy), ptr(dummy_o), stream())
+        return rows[:m]
+
+    def migrate_out(self):
+        """Drop ghosts, wrap (done in integrate), owners, stable grouping by
+        owner; returns {dest: (m, 7) rows} for dest != self (decomp.py:77-99)."""
+        e0 = self._t0()
+        rows = self._owned_rows()
+        if rows is not None:
+            n = rows.numel()
+            p = torch.empty((n + 1, 4), dtype=torch.float64, device=self.device)
+            _kernels.gather_rows(self.pos, rows, n, out=p)
+            vv = torch.empty((3, max(n, 1)), dtype=torch.float64, device=self.device)
+            for a in range(3):
+                _kernels.gather_rows(self.vel[a], rows, n, out=vv[a])
+            self.pos[:n] = p[:n]
+            self.vel[:, :n] = vv[:, :n]
+            self.n_owned = self.n_total = n
+        n = self.n_owned
+        x = self.pos[:n, :3].contiguous()
+        owner = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if n:
+            call("pc_owner_of", ptr(x), n, 3, self.fabric.pc_grid(), ptr(owner), ptr(flag),
+                 stream())
+            if int(flag.item()):
+                raise ValueError("position outside global box")
+        from .decomp import _group_by
+        order, starts = _group_by(owner[:n], self.fabric.n_ranks)
+        self._mig_order, self._mig_starts = order, starts
+        out = {}
+        for dst in range(self.fabric.n_ranks):
+            a, b = int(starts[dst]), int(starts[dst + 1])
+            if dst == self.rank or b == a:
+                continue
+            out[dst] = self._pack_mig(order[a:b])
+        self._t1("migrate", e0)
+        return out
+
+    def _pack_mig(self, rows):
+        m = rows.numel()
+        buf = torch.empty((m, MIG_W), dtype=torch.float64, device=self.device)
+        rows = rows.contiguous()
+        p = torch.empty((m, 4), dtype=torch.float64, device=self.device)
+        _kernels.gather_rows(self.pos, rows, m, out=p)
+        buf[:, 0:3] = p[:, 0:3]
+        buf[:, 6] = p[:, 3]
+        for a in range(3):
+            tmp = torch.empty(m, dtype=torch.float64, device=self.device)
+            _kernels.gather_rows(self.vel[a], rows, m, out=tmp)
+            buf[:, 3 + a] = tmp
+        return buf
+
+    def migrate_in(self, inbox):
+        """Arrivals by ascending source rank, own stayers at position rank."""
+        e0 = self._t0()
+        order, starts = self._mig_order, self._mig_starts
+        blocks = []
+        for src in range(self.fabric.n_ranks):
+            if src == self.rank:
+                a, b = int(starts[src]), int(starts[src + 1])
+                if b > a:
+                    blocks.append(self._pack_mig(order[a:b]))
+            elif src in inbox and inbox[src].shape[0]:
+                blocks.append(inbox[src])
+        rows = torch.cat(blocks) if blocks else torch.empty((0, MIG_W), dtype=torch.float64,
+                                                             device=self.device)
+        n = rows.shape[0]
+        self._ensure(n + 1)
+        self.pos[:n, :3] = rows[:, 0:3]
+        self.pos[:n, 3] = rows[:, 6]
+        self.vel[:, :n] = rows[:, 3:6].t()
+        self.n_owned = self.n_total = n
+        self.is_ghost[: self.cap].zero_()
+        self._t1("migrate", e0)
+
+    def halo_out(self):
+        """Export plan (best image per destination, d^2 < w^2) and the ghost
+        payload per destination (decomp.py:143-228, 231-246)."""
+        e0 = self._t0()
+        n = self.n_owned
+        o = self._offsets
+        self._exports = {}
+        out = {}
+        ns = len(o["dests"])
+        if ns == 0 or n == 0:
+            self._t1("halo", e0)
+            return out
+        x = self.pos[:n, :3].contiguous()
+        flags = torch.empty((ns, n), dtype=torch.int32, device=self.device)
+        best = torch.empty((ns, n), dtype=torch.int8, device=self.device)
+        call("pc_halo_plan", ptr(x), n, 3, len(o["slot"]),
+             o["slot"].ctypes.data_as(ctypes.c_void_p), o["shift"].ctypes.data_as(ctypes.c_void_p),
+             o["lo"].ctypes.data_as(ctypes.c_void_p), o["hi"].ctypes.data_as(ctypes.c_void_p),
+             ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
+        table = torch.as_tensor(o["shift"]).to(self.device)
+        for k, dst in enumerate(o["dests"]):
+            pos = _kernels.scan_i32(flags[k])
+            m = int(pos[n].item())
+            if m == 0:
+                continue
+            ix = torch.empty(m, dtype=torch.int32, device=self.device)
+            oc = torch.empty(m, dtype=torch.int8, device=self.device)
+            call("pc_compact", ptr(flags[k]), ptr(pos), n, ptr(ix), ptr(best[k]), ptr(oc),
+                 stream())
+            self._exports[dst] = ix
+            buf = torch.empty((m, HALO_W), dtype=torch.float64, device=self.device)
+            p = torch.empty((m, 4), dtype=torch.float64, device=self.device)
+            _kernels.gather_rows(self.pos, ix, m, out=p)
+            buf[:, 0:4] = p
+            buf[:, 4:7] = table[oc.to(torch.int64)]
+            out[dst] = buf
+        self._t1("halo", e0)
+        return out
+
+    def halo_in(self, inbox):
+        """Ghosts after owned rows by ascending source (decomp.py:247-260)."""
+        e0 = self._t0()
+        n = self.n_owned
+        blocks = [(src, inbox[src]) for src in sorted(inbox) if inbox[src].shape[0]]
+        g = sum(b.shape[0] for _, b in blocks)
+        self._ensure(n + g + 1)
+        self.binpos[:n] = self.pos[:n]
+        at = n
+        self._ghost_src = []
+        for src, b in blocks:
+            m = b.shape[0]
+            self.pos[at:at + m] = b[:, 0:4]
+            self.binpos[at:at + m, :3] = b[:, 0:3] + b[:, 4:7]
+            self.binpos[at:at + m, 3] = b[:, 3]
+            self.vel[:, at:at + m] = 0.0
+            self._ghost_src.append((src, at, m))
+            at += m
+        self.is_ghost[: self.cap].zero_()
+        self.is_ghost[n:at] = 1
+        self.n_total = at
+        self._t1("halo", e0)
+
+    def sort_and_build(self):
+        """Stable cell sort of owned + ghost rows on the local grid, then the
+        SELL Verlet build of all rows (ghost rows emptied)."""
+        n = self.n_total
+        s = stream()
+        e0 = self._t0()
+        srt = _kernels.CellSort(self.binpos[:n], 4, self._grid)
+        order = srt.order
+        new_pos = torch.empty_like(self.pos)
+        new_pos[self.cap] = self.pos[self.cap]
+        _kernels.gather_rows(self.pos, order, n, out=new_pos)
+        new_bin = torch.empty_like(self.binpos)
+        _kernels.gather_rows(self.binpos, order, n, out=new_bin)
+        new_vel = torch.zeros_like(self.vel)
+        for a in range(3):
+            _kernels.gather_rows(self.vel[a], order, n, out=new_vel[a])
+        new_g = torch.zeros_like(self.is_ghost)
+        _kernels.gather_rows(self.is_ghost, order, n, out=new_g)
+        self.pos, self.binpos, self.vel, self.is_ghost = new_pos, new_bin, new_vel, new_g
+        inv = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        call("pc_invert_order", ptr(order), n, ptr(inv), s)
+        inv32 = inv[:n].to(torch.int32)
+        self.export_rows = {dst: inv32[ix.to(torch.int64)].contiguous()
+                            for dst, ix in getattr(self, "_exports", {}).items()}
+        self.ghost_blocks = [(src, inv32[at:at + m].contiguous())
+                             for src, at, m in getattr(self, "_ghost_src", [])]
+        if self.pl is not None:
+            call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self.cap + 1, s)
+        self._t1("sort", e0)
+        e0 = self._t0()
+        used = ctypes.c_int32(0)
+        staged = True
+        while True:
+            self.build_flag.zero_()
+            if staged:
+                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                     self._lbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
+                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s,
+                     ptr(self.binpos), self._gbox)
+            else:
+                call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                     self._lbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
+                     ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s,
+                     ptr(self.binpos), self._gbox)
+            fl = int(self.build_flag.item())
+            if fl & _lib.FLAG_STAGE:
+                staged = False
+                continue
+            if not (fl & _lib.FLAG_OVERFLOW):
+                break
+            self.ell_width = -(-(int(self.cnt[:n].max().item()) + 8) // 4) * 4
+            slices = -(-self.cap // 32)
+            self.nbr = torch.empty(slices * self.ell_width * 32, dtype=torch.int32,
+                                   device=self.device)
+        self.cnt[:n] *= (1 - self.is_ghost[:n])          # ghost rows carry no list
+        self.used_staged = bool(used.value)
+        self.rebuilds += 1
+        self._t1("neighbor", e0)
+
+    def refresh_out(self):
+        """Per-step ghost refresh payload (raw x, y, z of exported rows)."""
+        e0 = self._t0()
+        out = {}
+        for dst, rows in self.export_rows.items():
+            m = rows.numel()
+            buf = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+            call("pc_halo_pack", ptr(self.pos), ptr(rows), m, ptr(buf), stream())
+            out[dst] = buf
+        self._t1("halo", e0)
+        return out
+
+    def refresh_in(self, inbox):
+        e0 = self._t0()
+        for src, rows in self.ghost_blocks:
+            buf = inbox[src]
+            call("pc_halo_unpack", ptr(buf), ptr(rows), rows.numel(), ptr(self.pos),
+                 ptr(self.pl), self.cap + 1, stream())
+        self._t1("halo", e0)
+
+    def force(self, kick_dtm):
+        e0 = self._t0()
+        ev = self.force_events
+        if ev is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n_total,
+             ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
+             self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
+             float(self.cfg.mass), ptr(self.partial), ptr(self.flag), stream())
+        if ev is not None:
+            b.record()
+            ev.append((a, b))
+        self._t1("force", e0)
+
+    def local_diagnostics(self):
+        nb = int(_lib.load().pc_lj_force_sell_partials(self.n_total))
+        call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
+        return self.diag
+
+    def owned_state(self):
+        """(gid, x, v) of owned rows (host numpy)."""
+        n = self.n_total
+        g = self.is_ghost[:n].cpu().numpy().astype(bool)
+        p = self.pos[:n].cpu().numpy()
+        v = self.vel[:, :n].cpu().numpy().T
+        ids = p[:, 3].copy().view(np.int64)
+        return ids[~g], p[~g, :3], v[~g]
+
+
+def _route(outboxes):
+    """In-process delivery: inbox[dst][src] = outbox[src][dst]."""
+    inboxes = [dict() for _ in outboxes]
+    for src, ob in enumerate(outboxes):
+        for dst, buf in ob.items():
+            inboxes[dst][src] = buf
+    return inboxes
+
+
+class _StepLogic:
+    """Shared step schedule (ref md.py:219-257) over phase callbacks."""
+
+    def _rebuild_all(self):
+        self._exchange("migrate_out", "migrate_in", MIG_W)
+        self._exchange("halo_out", "halo_in", HALO_W)
+        for e in self._engines():
+            e.sort_and_build()
+
+    def step(self, step_index: int):
+        for e in self._engines():
+            e.integrate()
+        if step_index % self.cfg.rebuild_stride == 0:
+            self._rebuild_all()
+        else:
+            self._exchange("refresh_out", "refresh_in", 3)
+        for e in self._engines():
+            e.force(self._dtm)
+
+    def _init_forces(self):
+        self._rebuild_all()
+        for e in self._engines():
+            e.force(0.0)
+
+
+class FabricMD(_StepLogic):
+    """All ranks of a rank grid in one process on one device -- the
+    reference's in-process fabric (md.py MDDriver with rank_dims), with GPU
+    kernels doing every data-sized step."""
+
+    def __init__(self, cfg: MDConfig, device=None):
+        cfg.validate()
+        self.cfg = cfg
+        a = (4.0 / cfg.density) ** (1.0 / 3.0)
+        self.box = Box(np.zeros(3), np.full(3, cfg.lattice_cells * a))
+        self.periodic = np.array([True, True, True])
+        self.fabric = decompose(self.box, cfg.rank_dims, self.periodic)
+        self.n = 4 * cfg.lattice_cells ** 3
+        self._dtm = 0.5 * cfg.dt / cfg.mass
+        dev = device if device is not None else _lib.device()
+        x = torch.as_tensor(fcc_lattice(cfg.lattice_cells, a))
+        v = torch.as_tensor(initial_velocities(self.n, cfg.temperature, cfg.mass, cfg.seed))
+        ids = torch.arange(self.n, dtype=torch.int64)
+        self.engines = []
+        for r in range(self.fabric.n_ranks):
+            if r == 0:
+                self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev))
+            else:
+                z = torch.zeros((0, 3), dtype=torch.float64)
+                self.engines.append(DomainEngine(cfg, self.fabric, r, z, z,
+                                                 torch.zeros(0, dtype=torch.int64), dev))
+        self._init_forces()
+
+    def _engines(self):
+        return self.engines
+
+    def _exchange(self, out_name, in_name, width):
+        outs = [getattr(e, out_name)() for e in self.engines]
+        for e, inbox in zip(self.engines, _route(outs)):
+            getattr(e, in_name)(inbox)
+
+    def diagnostics(self):
+        tot = sum(e.local_diagnostics().cpu().numpy() for e in self.engines)
+        ke, pe = float(tot[0]), float(tot[1])
+        return {"KE": ke, "PE": pe, "E_total": ke + pe,
+                "temperature": 2.0 * ke / (3.0 * self.n), "momentum": tot[2:5].copy()}
+
+    def gather_state(self):
+        x = np.zeros((self.n, 3))
+        v = np.zeros((self.n, 3))
+        for e in self.engines:
+            ids, xs, vs = e.owned_state()
+            x[ids] = xs
+            v[ids] = vs
+        return x, v
+
+
+class NCCLTransport:
+    """Per-destination row blocks between processes with torch.distributed:
+    send counts first (all_gather of the count vector), then one batched
+    isend/irecv per peer pair.  Works with nccl (GPU) and gloo (CPU tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+        # gloo moves host tensors only: stage device blocks through the host
+        # (used to run several ranks on one GPU in tests); NCCL sends device
+        # memory directly over NVLink
+        self.host_staged = dist.get_backend(group) == "gloo"
+
+    def _wire(self, t):
+        return t.cpu() if self.host_staged else t
+
+    def counts(self, outbox, device):
+        send = torch.zeros(self.world, dtype=torch.int64)
+        for dst, buf in outbox.items():
+            send[dst] = buf.shape[0]
+        send = send if self.host_staged else send.to(device)
+        allc = [torch.zeros_like(send) for _ in range(self.world)]
+        self.dist.all_gather(allc, send, group=self.group)
+        return torch.stack(allc).cpu().numpy()        # [src, dst]
+
+    def exchange(self, outbox, width, device, dtype=torch.float64):
+        c = self.counts(outbox, device)
+        ops, inbox = [], {}
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            m_out = int(c[self.rank, peer])
+            m_in = int(c[peer, self.rank])
+            if m_out:
+                ops.append(self.dist.P2POp(self.dist.isend,
+                                           self._wire(outbox[peer].contiguous()), peer,
+                                           group=self.group))
+            if m_in:
+                buf = torch.empty((m_in, width), dtype=dtype,
+                                  device="cpu" if self.host_staged else device)
+                inbox[peer] = buf
+                ops.append(self.dist.P2POp(self.dist.irecv, buf, peer, group=self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        if self.host_staged:
+            inbox = {k: v.to(device) for k, v in inbox.items()}
+        return inbox
+
+    def allreduce(self, t):
+        w = self._wire(t)
+        self.dist.all_reduce(w, group=self.group)
+        if w is not t:
+            t.copy_(w)
+        return t
+
+
+class DistMD(_StepLogic):
+    """One rank per GPU under torch.distributed (launch with torchrun)."""
+
+    def __init__(self, cfg: MDConfig, cells=None, transport=None, device=None,
+                 local_init: bool = False, time_phases: bool = False):
+        import torch.distributed as dist
+        cfg.validate()
+        self.cfg = cfg
+        self.transport = transport if transport is not None else NCCLTransport()
+        world, rank = self.transport.world, self.transport.rank
+        dims = tuple(cfg.rank_dims) if int(np.prod(cfg.rank_dims)) == world \
+            else rank_dims_for(world)
+        cells = np.array(cells if cells is not None else [cfg.lattice_cells] * 3, np.int64)
+        a = (4.0 / cfg.density) ** (1.0 / 3.0)
+        self.box = Box(np.zeros(3), cells * a)
+        self.periodic = np.array([True, True, True])
+        self.fabric = decompose(self.box, dims, self.periodic)
+        self.n = int(4 * np.prod(cells))
+        self._dtm = 0.5 * cfg.dt / cfg.mass
+        self.device = torch.device(device) if device is not None else _lib.device()
+        x, v, ids = self._initial(cells, a, rank, local_init)
+        self.engine = DomainEngine(cfg, self.fabric, rank, x, v, ids, self.device,
+                                   time_phases=time_phases)
+        self._init_forces()
+        del dist
+
+    def _initial(self, cells, a, rank, local_init):
+        """Reference-identical global init (md.py:67-86) kept by owner, or a
+        per-rank lattice block with per-rank seeded velocities (local_init,
+        for runs too large to build one global velocity stream)."""
+        cfg = self.cfg
+        if not local_init:
+            if len(set(cells.tolist())) != 1:
+                raise ValueError("global init needs a cubic lattice; use local_init")
+            x = fcc_lattice(int(cells[0]), a)
+            v = initial_velocities(self.n, cfg.temperature, cfg.mass, cfg.seed)
+            ids = np.arange(self.n, dtype=np.int64)
+            owner = self.fabric.owner_of(x) if self.n else np.zeros(0, np.int64)
+            keep = owner == rank
+            return (torch.as_tensor(x[keep]), torch.as_tensor(v[keep]),
+                    torch.as_tensor(ids[keep]))
+        dims = self.fabric.rank_dims
+        c = self.fabric.coords_of(rank)
+        per = cells // dims
+        lo = c * per
+        hi = np.where(c == dims - 1, cells, lo + per)
+        gx, gy, gz = np.meshgrid(*[np.arange(lo[k], hi[k]) for k in range(3)], indexing="ij")
+        corner = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+        basis = np.array([[0, 0, 0], [0.5, 0.5, 0], [0.5, 0, 0.5], [0, 0.5, 0.5]])
+        x = (corner[:, None, :] + basis[None]).reshape(-1, 3) * a
+        flat = (corner[:, 0] * cells[1] + corner[:, 1]) * cells[2] + corner[:, 2]
+        ids = (flat[:, None] * 4 + np.arange(4)[None]).reshape(-1).astype(np.int64)
+        v = initial_velocities(x.shape[0], cfg.temperature, cfg.mass,
+                               cfg.seed * 1000003 + rank)
+        return torch.as_tensor(x), torch.as_tensor(v), torch.as_tensor(ids)
+
+    def _engines(self):
+        return [self.engine]
+
+    def _exchange(self, out_name, in_name, width):
+        out = getattr(self.engine, out_name)()
+        inbox = self.transport.exchange(out, width, self.device)
+        getattr(self.engine, in_name)(inbox)
+
+    def diagnostics(self):
+        d = self.engine.local_diagnostics().clone()
+        self.transport.allreduce(d)
+        t = d.cpu().numpy()
+        ke, pe = float(t[0]), float(t[1])
+        return {"KE": ke, "PE": pe, "E_total": ke + pe,
+                "temperature": 2.0 * ke / (3.0 * self.n), "momentum": t[2:5].copy()}

@@ -280,7 +280,7 @@ class MDDriver:
         """Cell sort of all particle fields + SELL Verlet build (md.py:169-188)."""
         n, s = self.n, stream()
         e0 = self._t0()
-        srt = _kernels.CellSort(self.pos, 4, self._grid)
+        srt = _kernels.CellSort(self.pos[:n], 4, self._grid)     # excludes the dummy row
         _kernels.gather_rows(self.pos, srt.order, n, out=self._pos_alt)
         for a in range(3):
             _kernels.gather_rows(self.vel[a], srt.order, n, out=self._vel_alt[a])
@@ -297,11 +297,12 @@ class MDDriver:
             if staged:
                 call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
                      self._pbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
-                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s)
+                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s, None, None)
             else:
                 call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
                      self._pbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
-                     ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s)
+                     ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s, None,
+                     None)
                 used.value = 0
             fl = int(self.build_flag.item())
             if fl & _lib.FLAG_STAGE:          # dense neighbourhood: per-particle kernel

@@ -166,7 +166,7 @@ def build_verlet(positions, box: Box, periodic, cutoff: float, layout: str = "co
     cnt_sorted = torch.empty(n, dtype=torch.int32, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     call("pc_nbr_build", ptr(sorted4), n, ptr(srt.cell_start), grid, pbox, cutoff2, half,
-         _lib.PC_NBR_COUNT, 1, ptr(cnt_sorted), None, None, 0, 0, ptr(flag), s)
+         _lib.PC_NBR_COUNT, 1, ptr(cnt_sorted), None, None, 0, 0, ptr(flag), s, None, None)
     # counts in caller order -> CSR offsets; the fill writes row k at the
     # offset of its caller index, then rows are sorted ascending
     call("pc_scatter_rows", ptr(cnt_sorted), ptr(counts), ptr(srt.order), n, 4, s)
@@ -175,7 +175,7 @@ def build_verlet(positions, box: Box, periodic, cutoff: float, layout: str = "co
     off_sorted = _kernels.gather_rows(offsets[:n], srt.order, n)
     index = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
     call("pc_nbr_build", ptr(sorted4), n, ptr(srt.cell_start), grid, pbox, cutoff2, half,
-         _lib.PC_NBR_CSR, 1, ptr(cnt_sorted), ptr(off_sorted), ptr(index), 0, 0, ptr(flag), s)
+         _lib.PC_NBR_CSR, 1, ptr(cnt_sorted), ptr(off_sorted), ptr(index), 0, 0, ptr(flag), s, None, None)
     call("pc_sort_rows", ptr(offsets), n, ptr(index), s)
     return _finish(layout, half_or_full, cutoff, counts[:n], offsets, index[:total], n, total)
 

@@ -1,0 +1,85 @@
+"""Multi-process exchange protocol of the multi-GPU engine, on CPU with gloo
+(world size 2 and 3): counts first, then batched point-to-point blocks,
+delivered per source -- the transport dist.DistMD uses over NCCL."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_09056_b200.dist import NCCLTransport
+        t = NCCLTransport()
+        # rank r sends (r+1)*(d+1) rows to every d != r, rows encode (src, dst, k)
+        out = {}
+        for d in range(world):
+            if d == rank:
+                continue
+            m = (rank + 1) * (d + 1)
+            rows = torch.zeros((m, 3), dtype=torch.float64)
+            rows[:, 0] = rank
+            rows[:, 1] = d
+            rows[:, 2] = torch.arange(m, dtype=torch.float64)
+            out[d] = rows
+        if rank == world - 1:
+            out.pop(0, None)          # a rank that sends nothing to rank 0
+        inbox = t.exchange(out, 3, torch.device("cpu"))
+        got = {s: b.numpy().copy() for s, b in inbox.items()}
+        red = t.allreduce(torch.tensor([float(rank), 1.0], dtype=torch.float64))
+        q.put((rank, got, red.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_transport_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, got, red = q.get(timeout=120)
+        res[rank] = (got, red)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (got, red) in res.items():
+        assert red.tolist() == [sum(range(world)), float(world)]
+        for src in range(world):
+            if src == rank or (src == world - 1 and rank == 0):
+                assert src not in got
+                continue
+            m = (src + 1) * (rank + 1)
+            b = got[src]
+            assert b.shape == (m, 3)
+            assert np.all(b[:, 0] == src) and np.all(b[:, 1] == rank)
+            assert np.array_equal(b[:, 2], np.arange(m))
+
+
+def test_rank_dims_for():
+    from paper_2109_09056_b200.dist import rank_dims_for
+    assert rank_dims_for(1) == (1, 1, 1)
+    assert rank_dims_for(2) == (2, 1, 1)
+    assert rank_dims_for(4) == (2, 2, 1)
+    assert rank_dims_for(8) == (2, 2, 2)
+    assert int(np.prod(rank_dims_for(6))) == 6
