@@ -53,6 +53,16 @@ nbr_build_kernel(const double* __restrict__ pos, int n, const int* __restrict__ 
           if (r2_exact(dx, dy, dz) < cutoff2) {
             const int64_t tj = tag_of(pj.w);
             if (half && !(tj > ti)) continue;
+            if (posb != pos) {
+              // decomposed domain: accept only the ghost image adjacent to i in
+              // the local frame (another image of the same particle is ~L away)
+              const double4 bj = ld_pos4(posb + 4 * (int64_t)j);
+              const double lim = sqrt(cutoff2) * (1.0 + 1e-9);
+              if ((!b.periodic[0] && fabs(bj.x - bi.x) > lim) ||
+                  (!b.periodic[1] && fabs(bj.y - bi.y) > lim) ||
+                  (!b.periodic[2] && fabs(bj.z - bi.z) > lim))
+                continue;
+            }
             if (MODE != PC_NBR_COUNT) {
               const int v = out_tags ? (int)tj : j;
               if (MODE == PC_NBR_CSR) {

@@ -154,9 +154,15 @@ class DomainEngine:
             dest = f.rank_of(tgt)
             if dest != self.rank:
                 out.append((dest, shift))
-        dests = sorted(set(dst for dst, _ in out))
-        slot = {dst: k for k, dst in enumerate(dests)}
-        h_slot = np.array([slot[dst] for dst, _ in out], np.int32)
+        # One slot per image (not per destination as in the API's build_halo):
+        # when a block is narrower than twice the halo width a particle can be
+        # needed on both sides of a neighbour's block.  The reference covers
+        # that with one raw-position ghost + global min image (md.py:181-182);
+        # binning ghosts in the local frame needs every image within the
+        # width.  Duplicate images never pair twice: the build's binpos
+        # prefilter only accepts the image adjacent to the row particle.
+        dests = [dst for dst, _ in out]
+        h_slot = np.arange(len(out), dtype=np.int32)
         h_shift = np.ascontiguousarray(np.stack([s for _, s in out])) if out else np.zeros((0, 3))
         lo = np.stack([f.local_box(dst).low for dst, _ in out]) if out else np.zeros((0, 3))
         hi = np.stack([f.local_box(dst).high for dst, _ in out]) if out else np.zeros((0, 3))
@@ -321,7 +327,8 @@ class DomainEngine:
              o["lo"].ctypes.data_as(ctypes.c_void_p), o["hi"].ctypes.data_as(ctypes.c_void_p),
              ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
         table = torch.as_tensor(o["shift"]).to(self.device)
-        for k, dst in enumerate(o["dests"]):
+        per_dest = {}
+        for k, dst in enumerate(o["dests"]):           # offsets in product order
             pos = _kernels.scan_i32(flags[k])
             m = int(pos[n].item())
             if m == 0:
@@ -330,12 +337,17 @@ class DomainEngine:
             oc = torch.empty(m, dtype=torch.int8, device=self.device)
             call("pc_compact", ptr(flags[k]), ptr(pos), n, ptr(ix), ptr(best[k]), ptr(oc),
                  stream())
+            per_dest.setdefault(dst, []).append((ix, table[k].expand(m, 3)))
+        for dst in sorted(per_dest):
+            ix = torch.cat([a for a, _ in per_dest[dst]]).contiguous()
+            sh = torch.cat([b for _, b in per_dest[dst]])
+            m = ix.numel()
             self._exports[dst] = ix
             buf = torch.empty((m, HALO_W), dtype=torch.float64, device=self.device)
             p = torch.empty((m, 4), dtype=torch.float64, device=self.device)
             _kernels.gather_rows(self.pos, ix, m, out=p)
             buf[:, 0:4] = p
-            buf[:, 4:7] = table[oc.to(torch.int64)]
+            buf[:, 4:7] = sh
             out[dst] = buf
         self._t1("halo", e0)
         return out
