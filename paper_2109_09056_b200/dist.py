@@ -151,6 +151,10 @@ class DomainEngine:
                     shift[a] = -L[a]
             if not ok:
                 continue
+            # undecomposed periodic axes wrap inside the local grid: an image
+            # shifted along one of them would duplicate the local self-image
+            if any(shift[a] != 0 and f.rank_dims[a] == 1 for a in range(d)):
+                continue
             dest = f.rank_of(tgt)
             if dest != self.rank:
                 out.append((dest, shift))
