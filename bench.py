@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--path", choices=["tile", "sell"], default="tile",
+                    help="MD force/list path: tile-staged (default) or per-particle SELL")
     ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
                     help="force-kernel neighbor gather layout")
     return ap.parse_args()
@@ -198,7 +200,8 @@ def run_ours(args):
         drv = DistMD(cfg, cells=[args.cells * d for d in dims], local_init=True)
         eng = drv.engine
     else:
-        drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar")
+        drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar",
+                             tile=args.path == "tile")
         eng = drv
     n = drv.n                      # global atoms
     W, K = args.warmup, args.steps
@@ -232,10 +235,17 @@ def run_ours(args):
     n_rows = eng.n_total if world > 1 else n          # rows this rank's force kernel sweeps
     n_local = eng.n_owned if world > 1 else n
     kmean = float(eng.cnt[:n_rows].float().sum().item()) / max(1, n_local)
-    # algorithmic bytes per force launch per atom: Verlet indices
-    # 4k + row count 4 + pos4 read once 32 (L2-resident afterwards) + FP64
-    # force write 24 + fused final kick v read+write 48
-    bytes_per_atom = 4 * kmean + 4 + 32 + 24 + 48
+    # algorithmic bytes per force launch per atom: list entries
+    # (2 B tile slots / 4 B SELL indices) x k + row count 4 + position read
+    # once (24 planar / 32 pos4; L2-resident afterwards) + FP64 force write 24
+    # + fused final kick v read+write 48
+    mode = getattr(eng, "mode", "sell")
+    if mode == "tile":
+        bytes_per_atom = 2 * kmean + 4 + 24 + 24 + 48
+        kname = "tile_force_kernel (smem-staged, 16-bit slots, +fused final kick)"
+    else:
+        bytes_per_atom = 4 * kmean + 4 + 32 + 24 + 48
+        kname = "lj_force_sell_kernel (+fused final kick)"
     force_avg_s = float(np.mean(force_ms)) * 1e-3
     achieved = n_local * bytes_per_atom / force_avg_s / 1e9
     peak, peak_kind = measured_peak()
@@ -270,7 +280,7 @@ def run_ours(args):
                            "mean_neighbors": kmean},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                              "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "lj_force_kernel<ELL> (+fused final kick)",
+                             "kernel": kname,
                              "bytes_per_atom": bytes_per_atom, "peak_kind": peak_kind,
                              "avg_launch_us": force_avg_s * 1e6},
                 "gpu_launches": int(launches),

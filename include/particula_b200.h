@@ -183,6 +183,37 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
                       int32_t* d_flag, int32_t* h_used_staged, void* stream,
                       const double* d_posb, const pc_box* box_exact);
 
+/* ---- tile-staged MD hot path (pc_tile.cu) -------------------------------- */
+/* A tile = kTileZ (8) consecutive z-cells of one (x, y) column of `grid`; its
+ * home rows are one contiguous index range.  Its 27-cell neighbourhood is
+ * enumerated column by column, cell by cell ("slots", < 65536), identically in
+ * the build and the force kernel.  Lists: per tile, 32-row slices; entry k of
+ * tile row u at uint16 ((slice0[tile] + u/32)*(width/4) + k/4)*128 + (u%32)*4
+ * + k%4, the open quad padded with the row's own slot. */
+int32_t pc_tile_count(const pc_grid* grid);
+/* slices[tile] = ceil(home rows / 32); the caller scans them into slice0. */
+int pc_tile_slices(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_slices,
+                   void* stream);
+/* Verlet build into tile slot lists: the reference's FP64 predicate decided
+ * through the FP32 band prefilter of pc_nbr_build_sell, warp-cooperative
+ * ballot/popc compaction.  d_flag bit 1: row overflow (counts exact), bit 4:
+ * staging capacity exceeded (caller falls back to pc_nbr_build_sell). */
+int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_cell_start,
+                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_exact,
+                  double cutoff2, int32_t width, int32_t max_stage, const int32_t* d_slice0,
+                  int32_t* d_count, uint16_t* d_list, int32_t* d_flag, void* stream);
+int32_t pc_tile_force_partials(const pc_grid* grid);
+/* LJ force over tile slot lists: the tile's FP64 neighbourhood (planar x|y|z)
+ * is staged in shared memory once, rows gather by LDS.64; FP32 band decides
+ * the cutoff except within 1e-5 relative of rc^2 (exact FP64 there); FP32 LJ
+ * magnitude, FP64 accumulation, fused final kick, per-warp partials. */
+int pc_tile_force(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,
+                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_global,
+                  const pc_lj* lj, double mi_guard, int32_t width, int32_t max_stage,
+                  const int32_t* d_slice0, const int32_t* d_count, const uint16_t* d_list,
+                  double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride, double dtm,
+                  double mass, double* d_partial, int32_t* d_flag, void* stream);
+
 /* CSR -> dense (n, width) int64 table, -1 padded (ref neighbors.py:130-134). */
 int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,
                     int32_t width, int64_t* d_table, void* stream);

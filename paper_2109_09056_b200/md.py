@@ -189,7 +189,8 @@ class MDDriver:
     """
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
-                 time_phases: bool = True, state=None, planar_gather: bool = True):
+                 time_phases: bool = True, state=None, planar_gather: bool = True,
+                 tile: bool = True, max_stage: int = 2048):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -238,6 +239,12 @@ class MDDriver:
         # see pc_lj_force_sell in include/particula_b200.h)
         self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
         self.used_staged = None
+        # tile-staged path (pc_tile.cu): shared-memory neighbourhoods + 16-bit
+        # slot lists; falls back to the SELL path for small or dense grids
+        self.tile = bool(tile)
+        self.max_stage = int(max_stage)
+        self.mode = "sell"
+        self._tlist = None
         # planar x|y|z copy (stride cap+1, NaN dummy row) read by the force
         # gathers: 24 B in 8-B items per candidate instead of one 32-B pos4
         self.planar_gather = planar_gather
@@ -290,6 +297,13 @@ class MDDriver:
             call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self.cap + 1, s)
         self._t1("sort", e0)
         e0 = self._t0()
+        self._cell_start = srt.cell_start
+        if self.tile and self._tile_build(srt.cell_start):
+            self._t1("neighbor", e0)
+            self.rebuilds += 1
+            return
+        self.mode = "sell"
+        self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))
         used = ctypes.c_int32(0)
         staged = True
         while True:
@@ -317,16 +331,56 @@ class MDDriver:
         self._t1("neighbor", e0)
         self.rebuilds += 1
 
+    def _tile_build(self, cell_start) -> bool:
+        """Tile slot-list build (pc_tile.cu); False when this grid or density
+        does not fit the tile path (the SELL path then runs)."""
+        g = self._grid
+        if min(g.nc[0], g.nc[1], g.nc[2]) < 3 or self.pl is None:
+            return False
+        lib, s = _lib.load(), stream()
+        nt = int(lib.pc_tile_count(g))
+        slices = torch.empty(nt, dtype=torch.int32, device=self.device)
+        call("pc_tile_slices", ptr(cell_start), g, ptr(slices), s)
+        self._slice0 = _kernels.scan_i32(slices)
+        total = int(self._slice0[nt].item())
+        while True:
+            need = total * self.ell_width * 32
+            if self._tlist is None or self._tlist.numel() < need:
+                self._tlist = torch.empty(int(need * 1.1) + 64, dtype=torch.int16,
+                                          device=self.device)
+            self.build_flag.zero_()
+            call("pc_tile_build", ptr(self.pos), None, ptr(cell_start), g, self._pbox,
+                 self._pbox, self._search2, self.ell_width, self.max_stage, ptr(self._slice0),
+                 ptr(self.cnt), ptr(self._tlist), ptr(self.build_flag), s)
+            fl = int(self.build_flag.item())
+            if fl & _lib.FLAG_STAGE:
+                return False
+            if not (fl & _lib.FLAG_OVERFLOW):
+                break
+            self.ell_width = -(-(int(self.cnt[: self.n].max().item()) + 8) // 4) * 4
+        self.mode = "tile"
+        self._nblk = int(lib.pc_tile_force_partials(g))
+        if self._nblk > self.partial.shape[0]:
+            self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=self.device)
+        return True
+
     def _force(self, kick_dtm):
         e0 = self._t0()
         if self.force_events is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-        call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n,
-             ptr(self.cnt), ptr(self.nbr),
-             self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
-             ptr(self.vel), self.cap, float(kick_dtm), float(self.cfg.mass),
-             ptr(self.partial), ptr(self.flag), stream())
+        if self.mode == "tile":
+            call("pc_tile_force", ptr(self.pl), self.cap + 1, ptr(self._cell_start), self._grid,
+                 self._pbox, self._pbox, self._lj, self._mi_guard, self.ell_width,
+                 self.max_stage, ptr(self._slice0), ptr(self.cnt), ptr(self._tlist),
+                 ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
+                 float(self.cfg.mass), ptr(self.partial), ptr(self.flag), stream())
+        else:
+            call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n,
+                 ptr(self.cnt), ptr(self.nbr),
+                 self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
+                 ptr(self.vel), self.cap, float(kick_dtm), float(self.cfg.mass),
+                 ptr(self.partial), ptr(self.flag), stream())
         if self.force_events is not None:
             b.record()
             self.force_events.append((a, b))
@@ -391,17 +445,62 @@ class MDDriver:
         the layout of ref neighbors.build_verlet for parity checks."""
         n, Q = self.n, self.ell_width // 4
         cnt = self.cnt[:n].to(torch.int64).cpu().numpy()
-        words = self.nbr.cpu().numpy()
         gid = self.pos[:n, 3].contiguous().view(torch.int64).cpu().numpy()
         a = np.repeat(np.arange(n), cnt)
         k = np.arange(a.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
-        w = ((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)
-        j = words[w]
+        if self.mode == "tile":
+            j = self._tile_decode(a, k, Q)
+        else:
+            words = self.nbr.cpu().numpy()
+            w = ((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)
+            j = words[w]
         rows_gid, nb_gid = gid[a], gid[j]
         o = np.lexsort((nb_gid, rows_gid))
         counts = np.bincount(rows_gid, minlength=n)
         offsets = np.concatenate(([0], np.cumsum(counts)))
         return counts, offsets, nb_gid[o]
+
+    def _tile_decode(self, rows, ks, Q):
+        """Host replica of the tile slot enumeration (pc_tile.cuh) to map
+        tile slot lists back to particle rows (test/inspection only)."""
+        g = self._grid
+        nc = [g.nc[0], g.nc[1], g.nc[2]]
+        tz = 8
+        nseg = -(-nc[2] // tz)
+        cs = self._cell_start.cpu().numpy().astype(np.int64)
+        slice0 = self._slice0.cpu().numpy().astype(np.int64)
+        lst = self._tlist.cpu().numpy().view(np.uint16)
+        per = [bool(self._pbox.periodic[i]) for i in range(3)]
+        out = np.empty(rows.size, np.int64)
+        for t in range(nc[0] * nc[1] * nseg):
+            col, seg = divmod(t, nseg)
+            cx, cy = divmod(col, nc[1])
+            z0, z1 = seg * tz, min(seg * tz + tz, nc[2])
+            slots = []
+            for c in range(9):
+                xs, ys = cx + c // 3 - 1, cy + c % 3 - 1
+                for kk in range(z1 - z0 + 2):
+                    zs = z0 - 1 + kk
+                    v = [xs, ys, zs]
+                    ok = True
+                    for ax in range(3):
+                        if not 0 <= v[ax] < nc[ax]:
+                            if per[ax]:
+                                v[ax] %= nc[ax]
+                            else:
+                                ok = False
+                    if ok:
+                        cell = (v[0] * nc[1] + v[1]) * nc[2] + v[2]
+                        slots.extend(range(cs[cell], cs[cell + 1]))
+            slots = np.asarray(slots, np.int64)
+            h0 = cs[(cx * nc[1] + cy) * nc[2] + z0]
+            h1 = cs[(cx * nc[1] + cy) * nc[2] + z1]
+            sel = (rows >= h0) & (rows < h1)
+            u = rows[sel] - h0
+            kk = ks[sel]
+            w = ((slice0[t] + (u >> 5)) * Q + (kk >> 2)) * 128 + (u & 31) * 4 + (kk & 3)
+            out[sel] = slots[lst[w].astype(np.int64)]
+        return out
 
     def negate_velocities(self):
         self.vel.neg_()
