@@ -196,8 +196,10 @@ int pc_tile_slices(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_
                    void* stream);
 /* Verlet build into tile slot lists: the reference's FP64 predicate decided
  * through the FP32 band prefilter of pc_nbr_build_sell, warp-cooperative
- * ballot/popc compaction.  d_flag bit 1: row overflow (counts exact), bit 4:
- * staging capacity exceeded (caller falls back to pc_nbr_build_sell). */
+ * ballot/popc compaction.  d_flag[0] bit 1: row overflow (counts exact),
+ * bit 4: staging capacity exceeded, d_flag[1] = the largest neighbourhood
+ * (caller retries with max_stage >= d_flag[1], up to the shared-memory limit,
+ * else falls back to pc_nbr_build_sell).  d_flag holds 2 int32. */
 int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_cell_start,
                   const pc_grid* grid, const pc_box* box_local, const pc_box* box_exact,
                   double cutoff2, int32_t width, int32_t max_stage, const int32_t* d_slice0,

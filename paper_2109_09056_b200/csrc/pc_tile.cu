@@ -70,7 +70,10 @@ tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ pos
   __shared__ TileTable t;
   tile_table(blockIdx.x, g, b, cell_start, t);
   if (t.total > p.max_stage) {
-    if (threadIdx.x == 0) atomicOr(flag, kFlagStage);
+    if (threadIdx.x == 0) {
+      atomicOr(flag, kFlagStage);
+      atomicMax(flag + 1, t.total);      // capacity the caller must provide
+    }
     return;
   }
   int cx, cy, z0, z1;

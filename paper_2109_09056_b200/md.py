@@ -253,7 +253,7 @@ class MDDriver:
             self.pl = torch.empty((3, self.cap + 1), dtype=torch.float64, device=dev)
             self.pl[:, self.cap] = float("nan")
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
-        self.build_flag = torch.zeros(1, dtype=torch.int32, device=dev)  # ELL overflow
+        self.build_flag = torch.zeros(2, dtype=torch.int32, device=dev)  # overflow, need
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))   # per-warp rows
         self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
@@ -352,9 +352,14 @@ class MDDriver:
             call("pc_tile_build", ptr(self.pos), None, ptr(cell_start), g, self._pbox,
                  self._pbox, self._search2, self.ell_width, self.max_stage, ptr(self._slice0),
                  ptr(self.cnt), ptr(self._tlist), ptr(self.build_flag), s)
-            fl = int(self.build_flag.item())
+            fl, need = (int(v) for v in self.build_flag.cpu())
             if fl & _lib.FLAG_STAGE:
-                return False
+                # grow the staging capacity (force kernel: 24 B per slot, < 227 KB)
+                cap = int(need * 1.15) + 32
+                if cap * 24 > 220 * 1024 or cap > 65535:
+                    return False
+                self.max_stage = cap
+                continue
             if not (fl & _lib.FLAG_OVERFLOW):
                 break
             self.ell_width = -(-(int(self.cnt[: self.n].max().item()) + 8) // 4) * 4
