@@ -205,11 +205,12 @@ int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_ce
                   double cutoff2, int32_t width, int32_t max_stage, const int32_t* d_slice0,
                   int32_t* d_count, uint16_t* d_list, int32_t* d_flag, void* stream);
 int32_t pc_tile_force_partials(const pc_grid* grid);
-/* LJ force over tile slot lists: the tile's FP64 neighbourhood (planar x|y|z)
- * is staged in shared memory once, rows gather by LDS.64; FP32 band decides
- * the cutoff except within 1e-5 relative of rc^2 (exact FP64 there); FP32 LJ
- * magnitude, FP64 accumulation, fused final kick, per-warp partials. */
-int pc_tile_force(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,
+/* LJ force over tile slot lists: the tile's pos4 neighbourhood is staged into
+ * shared memory once by TMA bulk copies (cp.async.bulk, one per contiguous
+ * z-run, completing on an mbarrier); rows resolve slots with LDS; the
+ * reference's exact FP64 r^2 / cutoff test, FP32 LJ magnitude, FP64
+ * accumulation, fused final kick, per-warp partials. */
+int pc_tile_force(const double* d_pos, const int32_t* d_cell_start,
                   const pc_grid* grid, const pc_box* box_local, const pc_box* box_global,
                   const pc_lj* lj, double mi_guard, int32_t width, int32_t max_stage,
                   const int32_t* d_slice0, const int32_t* d_count, const uint16_t* d_list,

@@ -103,7 +103,7 @@ SIGNATURES = {
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcBox), c_dbl, c_i32,
                                      c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "pc_tile_force_partials": (c_i32, [ctypes.POINTER(PcGrid)]),
-    "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
+    "pc_tile_force": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(PcGrid),
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcBox),
                                      ctypes.POINTER(PcLJ), c_dbl, c_i32, c_i32, c_vp, c_vp,
                                      c_vp, c_vp, c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp,

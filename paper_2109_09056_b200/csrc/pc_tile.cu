@@ -19,7 +19,8 @@
 
 namespace pc {
 
-constexpr int kTileThreads = 256;
+constexpr int kTileThreads = 256;        // build: one warp per home cell
+constexpr int kForceTileThreads = 160;   // force: ~153 home rows per tile
 
 struct TileBuildParams {
   double cutoff2;
@@ -69,10 +70,10 @@ tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ pos
   extern __shared__ float4 stage[];
   __shared__ TileTable t;
   tile_table(blockIdx.x, g, b, cell_start, t);
-  if (t.total > p.max_stage) {
+  if (t.total + 1 > p.max_stage) {       // +1: the dummy padding slot
     if (threadIdx.x == 0) {
       atomicOr(flag, kFlagStage);
-      atomicMax(flag + 1, t.total);      // capacity the caller must provide
+      atomicMax(flag + 1, t.total + 1);  // capacity the caller must provide
     }
     return;
   }
@@ -81,20 +82,24 @@ tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ pos
   const double ox = g.low[0] + (cx + 0.5) * g.width[0];
   const double oy = g.low[1] + (cy + 0.5) * g.width[1];
   const double oz = g.low[2] + 0.5 * (z0 + z1) * g.width[2];
-  for (int s = threadIdx.x; s < t.total; s += blockDim.x) {
-    int c, k;
-    slot_cell(t, s, c, k);
-    const int j = t.src[c][k] + (s - t.off[c][k]);
-    const double4 q = ld_pos4(posb + 4 * (int64_t)j);
-    float4 v;
-    v.x = (float)(q.x + t.shift[c][k][0] - ox);
-    v.y = (float)(q.y + t.shift[c][k][1] - oy);
-    v.z = (float)(q.z + t.shift[c][k][2] - oz);
-    v.w = __int_as_float(j);
-    stage[s] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // stage: warp per cell, lanes over its (contiguous) particles
+  for (int e = warp; e < kTileCols * kTileCells; e += kTileThreads / 32) {
+    const int c = e / kTileCells, k = e - c * kTileCells;
+    const int m = t.off[c][k + 1] - t.off[c][k];
+    const int src = t.src[c][k], dst = t.off[c][k];
+    const double sx = t.shift[c][k][0], sy = t.shift[c][k][1], sz = t.shift[c][k][2];
+    for (int q = lane; q < m; q += 32) {
+      const double4 r = ld_pos4(posb + 4 * (int64_t)(src + q));
+      float4 v;
+      v.x = (float)(r.x + sx - ox);
+      v.y = (float)(r.y + sy - oy);
+      v.z = (float)(r.z + sz - oz);
+      v.w = __int_as_float(src + q);
+      stage[dst + q] = v;
+    }
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int Q = p.Q;
   const int64_t tile_base = (int64_t)slice0[blockIdx.x] * Q * 128;
@@ -137,10 +142,11 @@ tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ pos
           cnt += __popc(m);
         }
       }
-      // pad the open quad with the row's own slot (the force kernel skips it)
+      // pad the open quad with the dummy slot t.total (a NaN row in the force
+      // kernel's staging area: never interacts)
       const int kp = cnt + lane;
       if (lane < 4 && (kp & 3) && (kp >> 2) == (cnt >> 2) && kp < 4 * Q)
-        row[(kp >> 2) * 128 + (kp & 3)] = (uint16_t)(hs + h);
+        row[(kp >> 2) * 128 + (kp & 3)] = (uint16_t)t.total;
       if (lane == 0) {
         count[a] = cnt;
         if (cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
@@ -149,96 +155,147 @@ tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ pos
   }
 }
 
+// ---- TMA / mbarrier helpers ----------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine, UBLKCP); completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// One candidate slot: FP64 displacement from the staged pos4 row (LDS.128 +
+// LDS.64), minimum image on near-face axes, the reference's exact FP64 r^2
+// and cutoff test, FP32 LJ magnitude, FP64 accumulation.
 template <bool MI>
-__device__ __forceinline__ void tile_pair(const double* __restrict__ sx,
-                                          const double* __restrict__ sy,
-                                          const double* __restrict__ sz, int s, int self,
-                                          double xi, double yi, double zi, bool nx, bool ny,
-                                          bool nz, const pc_box& gb, const TileForceParams& p,
+__device__ __forceinline__ void tile_pair(const double4* __restrict__ st, int s, double xi,
+                                          double yi, double zi, bool nx, bool ny, bool nz,
+                                          const pc_box& gb, const TileForceParams& p,
                                           double& fx, double& fy, double& fz, double& pe,
                                           bool& overlap) {
-  double dx = __dsub_rn(sx[s], xi);
-  double dy = __dsub_rn(sy[s], yi);
-  double dz = __dsub_rn(sz[s], zi);
+  const double2 xy = *reinterpret_cast<const double2*>(st + s);
+  const double zz = reinterpret_cast<const double*>(st + s)[2];
+  double dx = __dsub_rn(xy.x, xi);
+  double dy = __dsub_rn(xy.y, yi);
+  double dz = __dsub_rn(zz, zi);
   if (MI) {
     if (nx) { const double a = fabs(dx); if (a >= gb.mi_thresh[0]) dx = copysign(__dsub_rn(a, gb.length[0]), -dx); }
     if (ny) { const double a = fabs(dy); if (a >= gb.mi_thresh[1]) dy = copysign(__dsub_rn(a, gb.length[1]), -dy); }
     if (nz) { const double a = fabs(dz); if (a >= gb.mi_thresh[2]) dz = copysign(__dsub_rn(a, gb.length[2]), -dz); }
   }
-  const float fxd = (float)dx, fyd = (float)dy, fzd = (float)dz;
-  const float r2f = fmaf(fzd, fzd, fmaf(fyd, fyd, fxd * fxd));
-  if (r2f < p.hi2f && s != self) {
-    bool inside = r2f < p.lo2f;
-    if (!inside) inside = r2_exact(dx, dy, dz) < p.cutoff2;     // exact FP64 decision
-    if (inside) {
-      overlap |= (r2f < 1e-10f) && (r2_exact(dx, dy, dz) < p.overlap2);
-      const float inv = rcp_approx(r2f);
-      const float sr2 = p.sig2 * inv;
-      const float sr6 = sr2 * sr2 * sr2;
-      const double fm = (double)(sr6 * (2.f * sr6 - 1.f) * inv);
-      fx = fma(-fm, dx, fx);
-      fy = fma(-fm, dy, fy);
-      fz = fma(-fm, dz, fz);
-      pe += (double)(sr6 * (sr6 - 1.f));
-    }
+  const double r2 = r2_exact(dx, dy, dz);
+  if (r2 < p.cutoff2) {
+    overlap |= r2 < p.overlap2;
+    const float inv = rcp_approx((float)r2);
+    const float sr2 = p.sig2 * inv;
+    const float sr6 = sr2 * sr2 * sr2;
+    const double fm = (double)(sr6 * (2.f * sr6 - 1.f) * inv);
+    fx = fma(-fm, dx, fx);
+    fy = fma(-fm, dy, fy);
+    fz = fma(-fm, dz, fz);
+    pe += (double)(sr6 * (sr6 - 1.f));
   }
 }
 
 template <bool MI>
-__device__ __forceinline__ void tile_row(const double* sx, const double* sy, const double* sz,
-                                         const ushort4* __restrict__ row, int mq, int self,
-                                         double xi, double yi, double zi, bool nx, bool ny,
-                                         bool nz, const pc_box& gb, const TileForceParams& p,
-                                         double& fx, double& fy, double& fz, double& pe,
-                                         bool& overlap) {
+__device__ __forceinline__ void tile_row(const double4* st, const ushort4* __restrict__ row,
+                                         int mq, double xi, double yi, double zi, bool nx,
+                                         bool ny, bool nz, const pc_box& gb,
+                                         const TileForceParams& p, double& fx, double& fy,
+                                         double& fz, double& pe, bool& overlap) {
   ushort4 nxt = make_ushort4(0, 0, 0, 0);
   if (mq > 0) nxt = __ldg(row);
   for (int q = 0; q < mq; ++q) {
     const ushort4 cur = nxt;
     if (q + 1 < mq) nxt = __ldg(row + (int64_t)(q + 1) * 32);
-    tile_pair<MI>(sx, sy, sz, cur.x, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(sx, sy, sz, cur.y, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(sx, sy, sz, cur.z, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(sx, sy, sz, cur.w, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
+    tile_pair<MI>(st, cur.x, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
+    tile_pair<MI>(st, cur.y, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
+    tile_pair<MI>(st, cur.z, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
+    tile_pair<MI>(st, cur.w, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
   }
 }
 
-__global__ void __launch_bounds__(kTileThreads)
-tile_force_kernel(const double* __restrict__ pl, int64_t ps, const int* __restrict__ cell_start,
+// One CTA per tile.  Thread 0 stages the tile's neighbourhood with TMA bulk
+// copies of contiguous pos4 runs (one per z-run of each stencil column) into
+// shared memory, completing on an mbarrier; slot t.total is set to NaN (the
+// build pads rows with it).  Then one thread per home row sweeps its slot list.
+__global__ void __launch_bounds__(kForceTileThreads)
+tile_force_kernel(const double* __restrict__ pos, const int* __restrict__ cell_start,
                   pc_grid g, pc_box b, pc_box gb, TileForceParams p,
                   const int* __restrict__ slice0, const int* __restrict__ count,
                   const uint16_t* __restrict__ list, double* __restrict__ f3, int64_t fs,
                   double* __restrict__ v, int64_t vs, double dtm, double mass,
                   double* __restrict__ partial, int* __restrict__ flag) {
-  extern __shared__ double sxyz[];
+  extern __shared__ __align__(128) double4 st[];
   __shared__ TileTable t;
+  __shared__ __align__(8) uint64_t bar;
   tile_table(blockIdx.x, g, b, cell_start, t);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double ke = 0.0, pet = 0.0, px = 0.0, py = 0.0, pz = 0.0;
-  if (t.total > p.max_stage) {
+  if (t.total + 1 > p.max_stage) {
     if (threadIdx.x == 0) atomicOr(flag, kFlagStage);
   } else {
-    const int S = p.max_stage;
-    double* sx = sxyz;
-    double* sy = sxyz + S;
-    double* sz = sxyz + 2 * S;
-    for (int s = threadIdx.x; s < t.total; s += blockDim.x) {
-      int c, k;
-      slot_cell(t, s, c, k);
-      const int j = t.src[c][k] + (s - t.off[c][k]);
-      sx[s] = __ldg(pl + j);
-      sy[s] = __ldg(pl + ps + j);
-      sz[s] = __ldg(pl + 2 * ps + j);
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, (uint32_t)t.total * 32u);
+      for (int c = 0; c < kTileCols; ++c) {
+        int k = 0;
+        while (k < kTileCells) {
+          const int src = t.src[c][k];
+          int end = src + (t.off[c][k + 1] - t.off[c][k]);
+          const int dst = t.off[c][k];
+          int k2 = k + 1;
+          while (k2 < kTileCells && t.src[c][k2] == end) {   // contiguous in memory
+            end += t.off[c][k2 + 1] - t.off[c][k2];
+            ++k2;
+          }
+          if (end > src)
+            bulk_g2s(st + dst, pos + 4 * (int64_t)src, (uint32_t)(end - src) * 32u, &bar);
+          k = k2;
+        }
+      }
+      st[t.total] = make_double4(__longlong_as_double(0x7ff8000000000000ll),
+                                 __longlong_as_double(0x7ff8000000000000ll),
+                                 __longlong_as_double(0x7ff8000000000000ll), 0.0);
     }
     __syncthreads();
+    mbar_wait(&bar, 0);
     const int Q = p.Q;
     const int64_t tile_base = (int64_t)slice0[blockIdx.x] * Q * 32;       // in ushort4
     const int hs0 = t.off[4][1];
     bool overlap = false;
     for (int u = threadIdx.x; u < t.nhome; u += blockDim.x) {
       const int a = t.home_first + u;
-      const int self = hs0 + u;
-      const double xi = sx[self], yi = sy[self], zi = sz[self];
+      const double4 me = st[hs0 + u];
+      const double xi = me.x, yi = me.y, zi = me.z;
       const int m = count[a];
       const bool nx = gb.periodic[0] && (xi - gb.low[0] < p.guard || gb.high[0] - xi <= p.guard);
       const bool ny = gb.periodic[1] && (yi - gb.low[1] < p.guard || gb.high[1] - yi <= p.guard);
@@ -248,11 +305,9 @@ tile_force_kernel(const double* __restrict__ pl, int64_t ps, const int* __restri
       double fx = 0.0, fy = 0.0, fz = 0.0, pe = 0.0;
       const int mq = (m + 3) >> 2;
       if (__any_sync(__activemask(), nx || ny || nz))
-        tile_row<true>(sx, sy, sz, row, mq, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe,
-                       overlap);
+        tile_row<true>(st, row, mq, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
       else
-        tile_row<false>(sx, sy, sz, row, mq, self, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz,
-                        pe, overlap);
+        tile_row<false>(st, row, mq, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
       fx *= (double)p.eps24;
       fy *= (double)p.eps24;
       fz *= (double)p.eps24;
@@ -282,7 +337,7 @@ tile_force_kernel(const double* __restrict__ pl, int64_t ps, const int* __restri
     py = warp_sum(py);
     pz = warp_sum(pz);
     if (lane == 0) {
-      double* o = partial + ((int64_t)blockIdx.x * (kTileThreads / 32) + warp) * 5;
+      double* o = partial + ((int64_t)blockIdx.x * (kForceTileThreads / 32) + warp) * 5;
       o[0] = ke; o[1] = pet; o[2] = px; o[3] = py; o[4] = pz;
     }
   }
@@ -349,10 +404,10 @@ int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_ce
 }
 
 int32_t pc_tile_force_partials(const pc_grid* grid) {
-  return pc_tile_count(grid) * (kTileThreads / 32);
+  return pc_tile_count(grid) * (kForceTileThreads / 32);
 }
 
-int pc_tile_force(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,
+int pc_tile_force(const double* d_pos, const int32_t* d_cell_start,
                   const pc_grid* grid, const pc_box* box_local, const pc_box* box_global,
                   const pc_lj* lj, double mi_guard, int32_t width, int32_t max_stage,
                   const int32_t* d_slice0, const int32_t* d_count, const uint16_t* d_list,
@@ -370,14 +425,14 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, const int32_t* 
   p.guard = mi_guard;
   p.Q = width / 4;
   p.max_stage = max_stage;
-  const int smem = 3 * max_stage * (int)sizeof(double);
+  const int smem = max_stage * (int)sizeof(double4);
   if (smem > g_force_smem) {
     cudaFuncSetAttribute(tile_force_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     g_force_smem = smem;
   }
   const int nt = pc_tile_count(grid);
-  tile_force_kernel<<<nt, kTileThreads, smem, as_stream(stream)>>>(
-      d_planar, planar_stride, d_cell_start, *grid, *box_local, *box_global, p, d_slice0,
+  tile_force_kernel<<<nt, kForceTileThreads, smem, as_stream(stream)>>>(
+      d_pos, d_cell_start, *grid, *box_local, *box_global, p, d_slice0,
       d_count, d_list, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag);
   return check_launch("pc_tile_force");
 }

@@ -354,9 +354,9 @@ class MDDriver:
                  ptr(self.cnt), ptr(self._tlist), ptr(self.build_flag), s)
             fl, need = (int(v) for v in self.build_flag.cpu())
             if fl & _lib.FLAG_STAGE:
-                # grow the staging capacity (force kernel: 24 B per slot, < 227 KB)
+                # grow the staging capacity (force kernel: 32 B per slot, < 227 KB)
                 cap = int(need * 1.15) + 32
-                if cap * 24 > 220 * 1024 or cap > 65535:
+                if cap * 32 > 220 * 1024 or cap > 65535:
                     return False
                 self.max_stage = cap
                 continue
@@ -375,7 +375,7 @@ class MDDriver:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
         if self.mode == "tile":
-            call("pc_tile_force", ptr(self.pl), self.cap + 1, ptr(self._cell_start), self._grid,
+            call("pc_tile_force", ptr(self.pos), ptr(self._cell_start), self._grid,
                  self._pbox, self._pbox, self._lj, self._mi_guard, self.ell_width,
                  self.max_stage, ptr(self._slice0), ptr(self.cnt), ptr(self._tlist),
                  ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
