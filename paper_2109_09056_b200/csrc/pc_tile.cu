@@ -19,8 +19,8 @@
 
 namespace pc {
 
-constexpr int kTileThreads = 256;        // build: one warp per home cell
-constexpr int kForceTileThreads = 160;   // force: ~153 home rows per tile
+constexpr int kTileThreads = 32 * kTileZ;  // build: one warp per home cell
+constexpr int kForceTileThreads = 96;   // force: ~78 home rows per tile (kTileZ = 4)
 
 struct TileBuildParams {
   double cutoff2;

@@ -14,7 +14,7 @@
 
 namespace pc {
 
-constexpr int kTileZ = 8;
+constexpr int kTileZ = 4;
 constexpr int kTileCells = kTileZ + 2;
 constexpr int kTileCols = 9;
 

@@ -190,7 +190,7 @@ class MDDriver:
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
                  time_phases: bool = True, state=None, planar_gather: bool = True,
-                 tile: bool = True, max_stage: int = 2048):
+                 tile: bool = True, max_stage: int = 1216):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -470,7 +470,7 @@ class MDDriver:
         tile slot lists back to particle rows (test/inspection only)."""
         g = self._grid
         nc = [g.nc[0], g.nc[1], g.nc[2]]
-        tz = 8
+        tz = 4
         nseg = -(-nc[2] // tz)
         cs = self._cell_start.cpu().numpy().astype(np.int64)
         slice0 = self._slice0.cpu().numpy().astype(np.int64)
