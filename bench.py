@@ -50,8 +50,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
-    ap.add_argument("--path", choices=["tile", "sell"], default="tile",
-                    help="MD force/list path: tile-staged (default) or per-particle SELL")
+    ap.add_argument("--path", choices=["tile", "sell"], default="sell",
+                    help="MD force/list path: per-particle SELL (default) or the "
+                         "experimental tile-staged path")
     ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
                     help="force-kernel neighbor gather layout")
     return ap.parse_args()

@@ -190,7 +190,7 @@ class MDDriver:
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
                  time_phases: bool = True, state=None, planar_gather: bool = True,
-                 tile: bool = True, max_stage: int = 1216):
+                 tile: bool = False, max_stage: int = 1216):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -318,7 +318,7 @@ class MDDriver:
                      ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s, None,
                      None)
                 used.value = 0
-            fl = int(self.build_flag.item())
+            fl = int(self.build_flag[0].item())
             if fl & _lib.FLAG_STAGE:          # dense neighbourhood: per-particle kernel
                 staged = False
                 continue

@@ -355,7 +355,7 @@ def test_md_verlet_list_bit_exact(pc, oracle, cells, temp):
     at init and after 25 steps (one rebuild at step 20)."""
     cfg = pc.md.MDConfig(lattice_cells=cells, density=0.8442, temperature=temp, cutoff=2.5,
                          skin=0.3, rebuild_stride=20, seed=3, steps=0)
-    drv = pc.md.MDDriver(cfg)
+    drv = pc.md.MDDriver(cfg, tile=True)
     for stage in range(2):
         if stage:
             for s in range(1, 21):
@@ -395,11 +395,14 @@ def test_md_tile_vs_sell_paths(pc):
     magnitude vs FP64 magnitude: 1e-6 relative on E_total over 60 steps)."""
     kw = dict(lattice_cells=12, density=0.8442, temperature=1.44, cutoff=2.5, skin=0.3,
               rebuild_stride=20, seed=4, steps=60)
-    a, _ = pc.md.run_md(pc.md.MDConfig(**kw))
-    drv = pc.md.MDDriver(pc.md.MDConfig(**kw), tile=False)
-    b = [drv.diagnostics()["E_total"]]
-    for s in range(1, 61):
-        drv.step(s)
-        b.append(drv.diagnostics()["E_total"])
-    ea = np.array([r["E_total"] for r in a])
-    assert np.max(np.abs(ea - np.array(b)) / np.abs(ea)) < 1e-6
+    def series(tile):
+        drv = pc.md.MDDriver(pc.md.MDConfig(**kw), tile=tile)
+        out = [drv.diagnostics()["E_total"]]
+        for s in range(1, 61):
+            drv.step(s)
+            out.append(drv.diagnostics()["E_total"])
+        return np.array(out), drv.mode
+    ea, ma = series(True)
+    eb, mb = series(False)
+    assert (ma, mb) == ("tile", "sell")
+    assert np.max(np.abs(ea - eb) / np.abs(ea)) < 1e-6
