@@ -205,50 +205,57 @@ nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __rest
   }
   __syncthreads();
 
-  // Warp-cooperative sweep: warp w owns home cell k = w + 1 (staged position;
-  // window = staged cells k-1..k+1 of every column, 9 contiguous smem ranges
-  // shared by all its particles).  For one home particle at a time the lanes
-  // test 32 candidates at once; hits are compacted into the row with
-  // ballot/popc, so rows list neighbors in staged order.
+  // Sweep: warp w owns home cell k = w + 1 (staged position; window = staged
+  // cells k-1..k+1 of every column, 9 contiguous smem ranges shared by all of
+  // the cell's particles).  Lanes are the cell's particles (chunks of 32);
+  // every candidate is one broadcast LDS.128 for the whole warp, so the loop
+  // bounds are warp-uniform.  Hits collect in a 4-entry register queue that
+  // is flushed as one 128-bit SELL store per quad.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const int Q = p.Q;
   for (int k = warp + 1; k <= z1 - z0; k += kBuildThreads / 32) {
     const int hs = cell_off[4][k];                 // staged slot of the first home particle
     const int hn = cell_off[4][k + 1] - hs;
-    for (int h = 0; h < hn; ++h) {
-      const float4 me = stage[hs + h];
-      const int a = __float_as_int(me.w);
+    for (int h0 = 0; h0 < hn; h0 += 32) {
+      const bool act = h0 + lane < hn;
+      const float4 me = act ? stage[hs + h0 + lane] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
+      const int a = act ? __float_as_int(me.w) : -1;
+      int4* row = reinterpret_cast<int4*>(index) + (int64_t)(a >> 5) * Q * 32 + (a & 31);
       int cnt = 0;
+      int b0 = p.dummy, b1 = p.dummy, b2 = p.dummy, b3 = p.dummy;
       for (int c = 0; c < 9; ++c) {
         const int s0 = cell_off[c][k - 1], s1 = cell_off[c][k + 2];
-        for (int s = s0 + lane; s - lane < s1; s += 32) {
-          bool hit = false;
-          int j = 0;
-          if (s < s1) {
-            const float4 q = stage[s];
-            const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            j = __float_as_int(q.w);
-            if (r2 < p.hi2 && j != a)
-              hit = r2 < p.lo2 || exact_pair(pos, a, j, e, p.cutoff2);
+#pragma unroll 2
+        for (int s = s0; s < s1; ++s) {
+          const float4 q = stage[s];
+          const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          if (r2 < p.hi2) {
+            const int j = __float_as_int(q.w);
+            if (j != a && (r2 < p.lo2 || exact_pair(pos, a, j, e, p.cutoff2))) {
+              if (MODE == PC_NBR_SELL) {
+                b0 = b1; b1 = b2; b2 = b3; b3 = j;
+                if ((cnt & 3) == 3 && cnt < 4 * Q) row[(cnt >> 2) * 32] = make_int4(b0, b1, b2, b3);
+              }
+              ++cnt;
+            }
           }
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (MODE == PC_NBR_SELL && hit) {
-            const int k2 = cnt + __popc(m & lt);
-            if (k2 < 4 * Q) index[sell_word(a, k2, Q)] = j;
-          }
-          cnt += __popc(m);
         }
       }
-      if (MODE == PC_NBR_SELL) {
-        // pad the open quad with the dummy row
-        const int kpad = cnt + lane;
-        if (lane < 4 && (kpad & 3) && (kpad >> 2) == (cnt >> 2) && kpad < 4 * Q)
-          index[sell_word(a, kpad, Q)] = p.dummy;
-        if (lane == 0 && cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
+      if (act) {
+        if (MODE == PC_NBR_SELL) {
+          const int r = cnt & 3;          // open quad: the last r entries, dummy padded
+          if (r && cnt < 4 * Q) {
+            int4 v = make_int4(p.dummy, p.dummy, p.dummy, p.dummy);
+            if (r == 1) v.x = b3;
+            if (r == 2) { v.x = b2; v.y = b3; }
+            if (r == 3) { v.x = b1; v.y = b2; v.z = b3; }
+            row[(cnt >> 2) * 32] = v;
+          }
+          if (cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
+        }
+        count[a] = cnt;
       }
-      if (lane == 0) count[a] = cnt;
     }
   }
 }
