@@ -202,7 +202,7 @@ def run_ours(args):
         eng = drv.engine
     else:
         drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar",
-                             tile=args.path == "tile")
+                             tile=args.path == "tile", half_list=args.list == "half")
         eng = drv
     n = drv.n                      # global atoms
     W, K = args.warmup, args.steps
@@ -241,7 +241,11 @@ def run_ours(args):
     # once (24 planar / 32 pos4; L2-resident afterwards) + FP64 force write 24
     # + fused final kick v read+write 48
     mode = getattr(eng, "mode", "sell")
-    if mode == "tile":
+    if mode == "half":
+        # half list: 4k_half + count + pos once + f read-modify-write (atomics)
+        bytes_per_atom = 4 * kmean + 4 + 32 + 48
+        kname = "lj_force_sell_half_kernel (Newton-3, FP64 atomics; kick separate)"
+    elif mode == "tile":
         bytes_per_atom = 2 * kmean + 4 + 24 + 24 + 48
         kname = "tile_force_kernel (smem-staged, 16-bit slots, +fused final kick)"
     else:

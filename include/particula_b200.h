@@ -181,7 +181,8 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
                       const pc_grid* grid, const pc_box* box, double cutoff2,
                       int32_t width, int32_t dummy, int32_t* d_count, int32_t* d_index,
                       int32_t* d_flag, int32_t* h_used_staged, void* stream,
-                      const double* d_posb, const pc_box* box_exact);
+                      const double* d_posb, const pc_box* box_exact,
+                      int32_t half /* keep one entry per unordered pair (Newton 3) */);
 
 /* ---- tile-staged MD hot path (pc_tile.cu) -------------------------------- */
 /* A tile = kTileZ (8) consecutive z-cells of one (x, y) column of `grid`; its
@@ -266,7 +267,16 @@ int pc_lj_force_sell(const double* d_pos, const double* d_planar /* x|y|z planar
                      double* d_v, int64_t v_stride, double dtm, double mass,
                      double* d_partial, int32_t* d_flag, void* stream);
 
-/* Half-list Newton-3 variant: rows hold j > i only; f_j -= F via FP32
+/* Half list over the SELL layout of pc_nbr_build_sell(half=1): each pair once,
+ * f_i += F in registers, f_j -= F by FP64 atomics (not bitwise deterministic);
+ * d_f3 zeroed by the caller, final kick by pc_kick.  Partials: per warp, PE
+ * only (full pair energy once). */
+int pc_lj_force_sell_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                          const int32_t* d_index, int32_t width, const pc_box* box,
+                          const pc_lj* lj, double mi_guard, double* d_f3, int64_t f_stride,
+                          double* d_partial, int32_t* d_flag, void* stream);
+
+/* Half-list Newton-3 variant: rows hold j > i only; f_j -= F via FP64
  * atomics (not bitwise deterministic).  d_f3 must be zeroed by the caller. */
 int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,
                      const int32_t* d_index, int64_t ell_stride,

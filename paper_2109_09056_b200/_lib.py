@@ -85,7 +85,10 @@ SIGNATURES = {
     "pc_nbr_build_sell": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
                                          ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_vp,
                                          c_vp, c_vp, ctypes.POINTER(c_i32), c_vp, c_vp,
-                                         ctypes.POINTER(PcBox)]),
+                                         ctypes.POINTER(PcBox), c_i32]),
+    "pc_lj_force_sell_half": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32,
+                                             ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl,
+                                             c_vp, c_i64, c_vp, c_vp, c_vp]),
     "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
     "pc_owner_of": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_vp,
                                    c_vp]),

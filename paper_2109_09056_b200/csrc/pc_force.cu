@@ -353,6 +353,82 @@ lj_force_sell_kernel(const double* __restrict__ pos, const double* __restrict__ 
   }
 }
 
+// Half list over the SELL layout (Newton's third law, ref md.py has no half
+// path: the reference force for a half list is the full-list force).  Each
+// stored pair is evaluated once; the row accumulates +F in registers and the
+// neighbour receives -F through FP64 atomics (RED.E.ADD.F64), so f must be
+// zeroed before and the final kick runs as a separate pc_kick.  PE partials
+// book each pair's full energy once.
+__global__ void __launch_bounds__(kForceThreads, 3)
+lj_force_sell_half_kernel(const double* __restrict__ pos, int n_rows,
+                          const int* __restrict__ count, const int4* __restrict__ nbr, int Q,
+                          pc_box b, LJConst c, double guard, double* __restrict__ f3,
+                          int64_t fs, double* __restrict__ partial, int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = i < n_rows;
+  double4 pi = make_double4(0.0, 0.0, 0.0, 0.0);
+  int m = 0;
+  if (live) {
+    pi = ld_pos4(pos + 4 * (int64_t)i);
+    m = count[i];
+  }
+  const bool nx = b.periodic[0] && (pi.x - b.low[0] < guard || b.high[0] - pi.x <= guard);
+  const bool ny = b.periodic[1] && (pi.y - b.low[1] < guard || b.high[1] - pi.y <= guard);
+  const bool nz = b.periodic[2] && (pi.z - b.low[2] < guard || b.high[2] - pi.z <= guard);
+  const int4* row = nbr + (int64_t)(i >> 5) * Q * 32 + lane;
+  double fx = 0.0, fy = 0.0, fz = 0.0, pe = 0.0;
+  bool overlap = false;
+  const int mq = (m + 3) >> 2;
+  int4 nxt = make_int4(0, 0, 0, 0);
+  if (mq > 0) nxt = __ldg(row);
+  for (int q = 0; q < mq; ++q) {
+    const int4 cur = nxt;
+    if (q + 1 < mq) nxt = __ldg(row + (int64_t)(q + 1) * 32);
+    const int js[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = js[u];
+      const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
+      double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
+      if (nx) dx = min_image_wrapped(dx, b.length[0], b.mi_thresh[0]);
+      if (ny) dy = min_image_wrapped(dy, b.length[1], b.mi_thresh[1]);
+      if (nz) dz = min_image_wrapped(dz, b.length[2], b.mi_thresh[2]);
+      const double r2 = r2_exact(dx, dy, dz);
+      if (r2 < c.cutoff2) {
+        overlap |= (r2 < c.overlap2);
+        double inv;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(r2));
+        inv = fma(inv, fma(-r2, inv, 1.0), inv);
+        const double sr2 = c.sig2d * inv;
+        const double sr6 = sr2 * sr2 * sr2;
+        const double fm = c.eps24d * fma(2.0 * sr6, sr6, -sr6) * inv;
+        const double gx = fm * dx, gy = fm * dy, gz = fm * dz;
+        fx -= gx;
+        fy -= gy;
+        fz -= gz;
+        atomicAdd(f3 + j, gx);
+        atomicAdd(f3 + fs + j, gy);
+        atomicAdd(f3 + 2 * fs + j, gz);
+        pe = fma(sr6, sr6, pe - sr6);
+      }
+    }
+  }
+  if (overlap) atomicOr(flag, kFlagOverlap);
+  if (live) {
+    atomicAdd(f3 + i, fx);
+    atomicAdd(f3 + fs + i, fy);
+    atomicAdd(f3 + 2 * fs + i, fz);
+  }
+  if (partial) {
+    pe = warp_sum(pe * 2.0 * c.eps2d);                       // 4 eps (sr12 - sr6)
+    if (lane == 0) {
+      double* o = partial + (int64_t)(i >> 5) * 5;
+      o[0] = 0.0; o[1] = pe; o[2] = 0.0; o[3] = 0.0; o[4] = 0.0;
+    }
+  }
+}
+
 static LJConst make_const(const pc_lj* lj) {
   LJConst c;
   c.cutoff2 = lj->cutoff2;
@@ -431,6 +507,22 @@ int pc_lj_force_sell(const double* d_pos, const double* d_planar, int64_t planar
         width / 4, *box, c, mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial,
         d_flag);
   return check_launch("pc_lj_force_sell");
+}
+
+int pc_lj_force_sell_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,
+                          const int32_t* d_index, int32_t width, const pc_box* box,
+                          const pc_lj* lj, double mi_guard, double* d_f3, int64_t f_stride,
+                          double* d_partial, int32_t* d_flag, void* stream) {
+  if (n_rows < 0 || width % 4) {
+    set_error("pc_lj_force_sell_half: bad rows/width");
+    return PC_ERR_VALUE;
+  }
+  LJConst c = make_const(lj);
+  unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
+  lj_force_sell_half_kernel<<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+      d_pos, n_rows, d_count, reinterpret_cast<const int4*>(d_index), width / 4, *box, c,
+      mi_guard, d_f3, f_stride, d_partial, d_flag);
+  return check_launch("pc_lj_force_sell_half");
 }
 
 int pc_lj_force_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,

@@ -110,6 +110,7 @@ struct StagedParams {
   int dummy;           // padding row index
   int max_stage;       // staged-candidate capacity (float4 entries)
   int nseg;            // z segments per column
+  int half;            // keep only j > i (sorted row index): Newton-3 half list
 };
 
 __device__ __forceinline__ bool exact_pair(const double* pos, int a, int j, const pc_box& b,
@@ -232,7 +233,8 @@ nbr_build_staged_kernel(const double* __restrict__ pos, int n, const int* __rest
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           if (r2 < p.hi2) {
             const int j = __float_as_int(q.w);
-            if (j != a && (r2 < p.lo2 || exact_pair(pos, a, j, e, p.cutoff2))) {
+            if ((p.half ? j > a : j != a) &&
+                (r2 < p.lo2 || exact_pair(pos, a, j, e, p.cutoff2))) {
               if (MODE == PC_NBR_SELL) {
                 b0 = b1; b1 = b2; b2 = b3; b3 = j;
                 if ((cnt & 3) == 3 && cnt < 4 * Q) row[(cnt >> 2) * 32] = make_int4(b0, b1, b2, b3);
@@ -372,7 +374,8 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
                                  const pc_box* box, double cutoff2, int32_t width,
                                  int32_t dummy, int32_t* d_count, int32_t* d_index,
                                  int32_t* d_flag, int32_t* h_used_staged, void* stream,
-                                 const double* d_posb, const pc_box* box_exact) {
+                                 const double* d_posb, const pc_box* box_exact,
+                                 int32_t half) {
   using namespace pc;
   if (n <= 0) return PC_OK;
   if (width % 4 || width <= 0) {
@@ -384,8 +387,10 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
   for (int a = 0; a < 3; ++a) staged &= !(box->periodic[a] && grid->nc[a] < 3);
   if (h_used_staged) *h_used_staged = staged ? 1 : 0;
   if (!staged) {
-    return pc_nbr_build(d_pos_sorted, n, d_cell_start, grid, box, cutoff2, 0, PC_NBR_SELL, 0,
-                        d_count, nullptr, d_index, dummy, width, d_flag, stream, d_posb,
+    // half: the per-particle kernel compares tags (global ids) -- also one
+    // entry per unordered pair
+    return pc_nbr_build(d_pos_sorted, n, d_cell_start, grid, box, cutoff2, half, PC_NBR_SELL,
+                        0, d_count, nullptr, d_index, dummy, width, d_flag, stream, d_posb,
                         box_exact);
   }
   // FP32 prefilter band (see header comment of nbr_build_staged_kernel)
@@ -405,6 +410,7 @@ extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
   const int stage_bytes = 32 * 1024;
   p.max_stage = stage_bytes / (int)sizeof(float4);
   p.nseg = (grid->nc[2] + kSegCells - 1) / kSegCells;
+  p.half = half;
   if (g_stage_bytes < stage_bytes) {
     cudaFuncSetAttribute(nbr_build_staged_kernel<PC_NBR_SELL>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);

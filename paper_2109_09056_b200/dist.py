@@ -417,7 +417,7 @@ class DomainEngine:
                 call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
                      self._lbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
                      ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s,
-                     ptr(self.binpos), self._gbox)
+                     ptr(self.binpos), self._gbox, 0)
             else:
                 call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
                      self._lbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,

@@ -190,7 +190,7 @@ class MDDriver:
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
                  time_phases: bool = True, state=None, planar_gather: bool = True,
-                 tile: bool = False, max_stage: int = 1216):
+                 tile: bool = False, max_stage: int = 1216, half_list: bool = False):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -241,7 +241,14 @@ class MDDriver:
         self.used_staged = None
         # tile-staged path (pc_tile.cu): shared-memory neighbourhoods + 16-bit
         # slot lists; falls back to the SELL path for small or dense grids
-        self.tile = bool(tile)
+        self.tile = bool(tile) and not half_list
+        # Newton-3 half list (pc_lj_force_sell_half): each pair once, FP64
+        # atomics for the neighbour side, kick as a separate pass
+        self.half_list = bool(half_list)
+        self._ke_in_k = False
+        self.partial_k = torch.zeros((int(_lib.load().pc_lj_force_blocks(n)), 5),
+                                     dtype=torch.float64, device=dev)
+        self.diag_k = torch.zeros(5, dtype=torch.float64, device=dev)
         self.max_stage = int(max_stage)
         self.mode = "sell"
         self._tlist = None
@@ -302,19 +309,21 @@ class MDDriver:
             self._t1("neighbor", e0)
             self.rebuilds += 1
             return
-        self.mode = "sell"
+        self.mode = "half" if self.half_list else "sell"
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))
         used = ctypes.c_int32(0)
         staged = True
+        half = int(self.half_list)
         while True:
             self.build_flag.zero_()
             if staged:
                 call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
                      self._pbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
-                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s, None, None)
+                     ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s, None, None,
+                     half)
             else:
                 call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
-                     self._pbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
+                     self._pbox, self._search2, half, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
                      ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s, None,
                      None)
                 used.value = 0
@@ -380,6 +389,11 @@ class MDDriver:
                  self.max_stage, ptr(self._slice0), ptr(self.cnt), ptr(self._tlist),
                  ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
                  float(self.cfg.mass), ptr(self.partial), ptr(self.flag), stream())
+        elif self.mode == "half":
+            self.frc.zero_()
+            call("pc_lj_force_sell_half", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
+                 self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
+                 ptr(self.partial), ptr(self.flag), stream())
         else:
             call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n,
                  ptr(self.cnt), ptr(self.nbr),
@@ -390,6 +404,14 @@ class MDDriver:
             b.record()
             self.force_events.append((a, b))
         self._t1("force", e0)
+        if self.mode == "half":      # atomics finish f: final kick + KE partials separately
+            e0 = self._t0()
+            call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial_k), stream())
+            self._t1("integrate", e0)
+            self._ke_in_k = True
+        else:
+            self._ke_in_k = False
         self._ke_fresh = True
 
     def _integrate(self):
@@ -414,15 +436,17 @@ class MDDriver:
     # -- diagnostics --------------------------------------------------------
     def device_diagnostics(self) -> torch.Tensor:
         """(KE, PE, px, py, pz) on the device, no host sync."""
-        if not self._ke_fresh:
-            kp = torch.zeros_like(self.partial)
+        if not self._ke_fresh:       # velocities changed outside a force pass
             call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n, 0.0,
-                 float(self.cfg.mass), ptr(kp), stream())
-            pe_col = self.partial[:, 1].clone()
-            self.partial = kp
-            self.partial[:, 1] = pe_col
+                 float(self.cfg.mass), ptr(self.partial_k), stream())
+            self._ke_in_k = True
             self._ke_fresh = True
         call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(self.diag), stream())
+        if self._ke_in_k:            # KE / momentum from the kick partials, PE from force
+            nk = int(_lib.load().pc_lj_force_blocks(self.n))
+            call("pc_reduce_partials", ptr(self.partial_k), nk, ptr(self.diag_k), stream())
+            self.diag_k[1] = self.diag[1]
+            return self.diag_k
         return self.diag
 
     def diagnostics(self):
