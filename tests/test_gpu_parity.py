@@ -427,6 +427,16 @@ def test_md_half_list_path(pc, oracle):
     assert drv.mode == "half"
     assert np.max(np.abs(ef - eh) / np.abs(ef)) < 1e-9
     assert np.max(np.abs(d["momentum"])) < 1e-9
-    # half list content: each unordered pair exactly once
-    full_total = sum(len(r) for r in oracle.rows_from_csr(*drv.verlet_sets()[::2]))
-    assert 2 * int(drv.cnt[: drv.n].sum().item()) == 2 * full_total
+    # half list content: each unordered pair of the (last rebuild's) full
+    # list exactly once
+    drv2 = pc.md.MDDriver(pc.md.MDConfig(**kw), half_list=True)
+    counts, offsets, idx = drv2.verlet_sets()
+    rows = np.repeat(np.arange(drv2.n), counts)
+    pairs = set(zip(np.minimum(rows, idx).tolist(), np.maximum(rows, idx).tolist()))
+    assert len(pairs) == idx.size
+    p = drv2.pos[: drv2.n].cpu().numpy()
+    x = np.empty((drv2.n, 3))
+    x[p[:, 3].copy().view(np.int64)] = p[:, :3]
+    ref = oracle.build_verlet(x, drv2.box.low, drv2.box.high, [True] * 3, drv2.search,
+                              half_or_full="half")
+    assert idx.size == ref["indices"].size
