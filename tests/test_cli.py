@@ -1,0 +1,87 @@
+"""CLI contract (ref tests/test_cli.py, acceptance criteria 2 and 11).
+Config errors are checked on CPU; runs need the GPU (marked)."""
+
+import json
+
+import pytest
+
+from paper_2109_09056_b200 import cli
+
+
+def test_unknown_config_key_exit_2(tmp_path, capsys):
+    f = tmp_path / "c.json"
+    f.write_text(json.dumps({"subcommannd": "md"}))
+    assert cli.main(["md", "--config", str(f)]) == 2
+    assert "unknown key: subcommannd" in capsys.readouterr().err
+
+
+def test_bad_values_and_constraints_exit_2(tmp_path, capsys):
+    f = tmp_path / "c.json"
+    f.write_text(json.dumps({"steps": "many"}))
+    assert cli.main(["md", "--config", str(f)]) == 2
+    assert cli.main(["md", "--dt", "-0.1", "--output", "-"]) == 2
+    assert cli.main(["md", "--cutoff", "99", "--output", "-"]) == 2
+    assert cli.main(["md", "--ranks", "2,2", "--output", "-"]) == 2
+    bad = tmp_path / "bad.json"
+    bad.write_text(json.dumps({"steps": 5, "lattice_sells": 4}))
+    assert cli.main(["md", "--config", str(bad)]) == 2
+    assert "lattice_sells" in capsys.readouterr().err
+
+
+def test_subcommand_mismatch_exit_2(tmp_path, capsys):
+    f = tmp_path / "c.json"
+    f.write_text(json.dumps({"subcommand": "pic"}))
+    assert cli.main(["md", "--config", str(f)]) == 2
+    capsys.readouterr()
+
+
+def test_parse_precedence():
+    cfg = cli.parse_config("md", None, {"steps": "7", "lattice_cells": None})
+    assert cfg["steps"] == 7 and cfg["lattice_cells"] == 4
+
+
+@pytest.mark.gpu
+def test_seeded_runs_byte_identical_and_format(tmp_path):
+    a, b = tmp_path / "a.csv", tmp_path / "b.csv"
+    args = ["md", "--steps", "5", "--lattice-cells", "3", "--density", "1.1", "--cutoff",
+            "2.0", "--seed", "9"]
+    assert cli.main(args + ["--output", str(a)]) == 0
+    assert cli.main(args + ["--output", str(b)]) == 0
+    assert a.read_bytes() == b.read_bytes()
+    raw = a.read_bytes()
+    assert b"\r" not in raw
+    lines = raw.decode().splitlines()
+    assert lines[0].startswith("# ") and "steps=5" in lines[0]
+    assert lines[1] == "step,KE,PE,E_total,temperature"
+    assert len(lines) == 2 + 6
+    assert (tmp_path / "a.csv.phases.csv").read_bytes().splitlines()[1] == b"phase,seconds"
+
+
+@pytest.mark.gpu
+def test_layout_transparency(tmp_path):
+    """Criterion 2 (md part): physics rows bitwise identical for V in {1,4,8,16,SoA}."""
+    n_md = 4 * 4 ** 3
+    outs = []
+    for v in (1, 4, 8, 16, n_md):
+        p = tmp_path / f"md_{v}.csv"
+        assert cli.main(["md", "--steps", "10", "--lattice-cells", "4", "--density", "1.1",
+                         "--cutoff", "2.3", "--vector-length", str(v), "--output",
+                         str(p)]) == 0
+        outs.append(p.read_bytes().split(b"\n", 1)[1])
+    assert all(o == outs[0] for o in outs)
+
+
+@pytest.mark.gpu
+def test_layout_bench_and_fabric(tmp_path):
+    p = tmp_path / "lb.csv"
+    assert cli.main(["layout-bench", "--steps", "3", "--lattice-cells", "4", "--density",
+                     "1.1", "--cutoff", "2.3", "--vector-lengths", "1,16", "--output",
+                     str(p)]) == 0
+    lines = p.read_text().splitlines()
+    assert lines[1] == "vector_length,phase,seconds,checksum"
+    sums = {ln.split(",")[3] for ln in lines[2:]}
+    assert len(sums) == 1
+    q = tmp_path / "fab.csv"
+    assert cli.main(["md", "--steps", "5", "--lattice-cells", "4", "--density", "1.1",
+                     "--cutoff", "2.3", "--ranks", "2,2,2", "--output", str(q)]) == 0
+    assert len(q.read_text().splitlines()) == 8
