@@ -50,9 +50,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
-    ap.add_argument("--path", choices=["tile", "sell"], default="sell",
-                    help="MD force/list path: per-particle SELL (default) or the "
-                         "experimental tile-staged path")
+    ap.add_argument("--path", choices=["tile", "sell"], default="tile",
+                    help="MD force/list path: TMA-staged tile rounds (default) or the "
+                         "per-particle SELL list")
     ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
                     help="force-kernel neighbor gather layout")
     return ap.parse_args()
@@ -235,21 +235,24 @@ def run_ours(args):
     eng.force_events = None
     n_rows = eng.n_total if world > 1 else n          # rows this rank's force kernel sweeps
     n_local = eng.n_owned if world > 1 else n
-    kmean = float(eng.cnt[:n_rows].float().sum().item()) / max(1, n_local)
-    # algorithmic bytes per force launch per atom: list entries
-    # (2 B tile slots / 4 B SELL indices) x k + row count 4 + position read
-    # once (24 planar / 32 pos4; L2-resident afterwards) + FP64 force write 24
-    # + fused final kick v read+write 48
+    if world > 1:
+        kmean = float(eng.cnt[:n_rows].float().sum().item()) / max(1, n_local)
+    else:
+        kmean = eng.mean_neighbors()
+    # algorithmic bytes per force launch per atom (SURVEY §8d
+    # K6 + the fused final kick): a 4-B neighbour index per list entry (k)
+    # + row length 4 + position read once 24 + FP64 force write 24 + final
+    # kick v read+write 48 -- the same figure for every list layout
     mode = getattr(eng, "mode", "sell")
     if mode == "half":
         # half list: 4k_half + count + pos once + f read-modify-write (atomics)
-        bytes_per_atom = 4 * kmean + 4 + 32 + 48
+        bytes_per_atom = 4 * kmean + 4 + 24 + 48
         kname = "lj_force_sell_half_kernel (Newton-3, FP64 atomics; kick separate)"
     elif mode == "tile":
-        bytes_per_atom = 2 * kmean + 4 + 24 + 24 + 48
-        kname = "tile_force_kernel (smem-staged, 16-bit slots, +fused final kick)"
+        bytes_per_atom = 4 * kmean + 4 + 24 + 24 + 48
+        kname = "tile_force_kernel (TMA-staged smem neighbourhood, 16-bit slot rounds, +fused final kick)"
     else:
-        bytes_per_atom = 4 * kmean + 4 + 32 + 24 + 48
+        bytes_per_atom = 4 * kmean + 4 + 24 + 24 + 48
         kname = "lj_force_sell_kernel (+fused final kick)"
     force_avg_s = float(np.mean(force_ms)) * 1e-3
     achieved = n_local * bytes_per_atom / force_avg_s / 1e9

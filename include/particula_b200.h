@@ -185,38 +185,53 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
                       int32_t half /* keep one entry per unordered pair (Newton 3) */);
 
 /* ---- tile-staged MD hot path (pc_tile.cu) -------------------------------- */
-/* A tile = kTileZ (8) consecutive z-cells of one (x, y) column of `grid`; its
- * home rows are one contiguous index range.  Its 27-cell neighbourhood is
- * enumerated column by column, cell by cell ("slots", < 65536), identically in
- * the build and the force kernel.  Lists: per tile, 32-row slices; entry k of
- * tile row u at uint16 ((slice0[tile] + u/32)*(width/4) + k/4)*128 + (u%32)*4
- * + k%4, the open quad padded with the row's own slot. */
+/* MD-engine replacement of ref neighbors.py:49-97 (Verlet build) +
+ * md.py:99-126 (forces) + md.py:251-257 (final half kick) for a 3-D box with
+ * >= 3 cells of `grid` per axis.  A tile = 2x2 columns x 4 z-cells of `grid`;
+ * its neighbourhood (4x4 columns x 6 cells = cell-sorted index runs) is
+ * staged in shared memory by TMA bulk copies; lists hold 16-bit slots into
+ * that staging area, grouped per row-warp of 32 home rows in bank-conflict-
+ * free "rounds" (layout: pc_tile.cu header).  Positions are the planar FP64
+ * arrays x|y|z at d_planar with stride planar_stride (a multiple of 16
+ * elements, >= n + 1).
+ *
+ * pc_tile_count: number of tiles.  pc_tile_rows: d_rw[tile] = row-warps of
+ * the tile (ceil(home rows / 32)); the caller scans them into d_rw0
+ * (ntiles + 1 entries; total row-warps RW = d_rw0[ntiles]) and provides
+ * d_plan (ntiles * pc_tile_plan_ints() int32), d_rowidx (RW * 32 int32),
+ * d_rounds (RW int32), d_partial (RW * 5 doubles) and d_list (RW * q8 * 512
+ * bytes). */
 int32_t pc_tile_count(const pc_grid* grid);
-/* slices[tile] = ceil(home rows / 32); the caller scans them into slice0. */
-int pc_tile_slices(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_slices,
-                   void* stream);
-/* Verlet build into tile slot lists: the reference's FP64 predicate decided
- * through the FP32 band prefilter of pc_nbr_build_sell, warp-cooperative
- * ballot/popc compaction.  d_flag[0] bit 1: row overflow (counts exact),
- * bit 4: staging capacity exceeded, d_flag[1] = the largest neighbourhood
- * (caller retries with max_stage >= d_flag[1], up to the shared-memory limit,
- * else falls back to pc_nbr_build_sell).  d_flag holds 2 int32. */
-int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_cell_start,
-                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_exact,
-                  double cutoff2, int32_t width, int32_t max_stage, const int32_t* d_slice0,
-                  int32_t* d_count, uint16_t* d_list, int32_t* d_flag, void* stream);
-int32_t pc_tile_force_partials(const pc_grid* grid);
-/* LJ force over tile slot lists: the tile's pos4 neighbourhood is staged into
- * shared memory once by TMA bulk copies (cp.async.bulk, one per contiguous
- * z-run, completing on an mbarrier); rows resolve slots with LDS; the
- * reference's exact FP64 r^2 / cutoff test, FP32 LJ magnitude, FP64
- * accumulation, fused final kick, per-warp partials. */
-int pc_tile_force(const double* d_pos, const int32_t* d_cell_start,
-                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_global,
-                  const pc_lj* lj, double mi_guard, int32_t width, int32_t max_stage,
-                  const int32_t* d_slice0, const int32_t* d_count, const uint16_t* d_list,
-                  double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride, double dtm,
-                  double mass, double* d_partial, int32_t* d_flag, void* stream);
+int32_t pc_tile_plan_ints(void);
+int32_t pc_tile_stage_cap(void);
+int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw,
+                 void* stream);
+/* Verlet build at cutoff2 (the reference's FP64 predicate behind an FP32
+ * band prefilter) + round scheduling.  d_flag (3 int32, zeroed by the
+ * caller): [0] bit 1 = a row-warp needs more than 8*q8 rounds ([2] = the
+ * largest; >= 2^20: a row exceeds 128 entries), bit 4 = a neighbourhood
+ * exceeds pc_tile_stage_cap() slots ([1] = the largest).  The caller grows
+ * q8 and rebuilds, or falls back to pc_nbr_build_sell. */
+int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,
+                  const pc_grid* grid, const pc_box* box, double cutoff2, int32_t q8,
+                  const int32_t* d_rw0, int32_t* d_plan, int32_t* d_rowidx, int32_t* d_rounds,
+                  void* d_list, int32_t* d_flag, void* stream);
+/* LJ force over the tile lists: exact FP64 r^2 < rc^2 re-test in the
+ * reference's rounding order (minimum image on rows within mi_guard of a
+ * periodic face), FP32 LJ magnitude, FP64 accumulation; writes f (planar,
+ * f_stride), applies the final half kick v += dtm*f when d_v != NULL and
+ * writes per-row-warp (KE, PE, px, py, pz) partials.  Overlap
+ * (r^2 < overlap2) sets d_flag bit 2. */
+int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
+                  const int32_t* d_plan, const int32_t* d_rowidx, const int32_t* d_rounds,
+                  const void* d_list, int32_t q8, const pc_box* box, const pc_lj* lj,
+                  double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
+                  double dtm, double mass, double* d_partial, int32_t* d_flag, void* stream);
+/* Tile lists -> per-row particle indices: d_count[row], d_table[row*width+k]
+ * (rows = cell-sorted particle indices; inspection / parity tests). */
+int pc_tile_decode(int32_t ntiles, const int32_t* d_plan, const int32_t* d_rowidx,
+                   const int32_t* d_rounds, const void* d_list, int32_t q8, int32_t width,
+                   int32_t* d_count, int32_t* d_table, void* stream);
 
 /* CSR -> dense (n, width) int64 table, -1 padded (ref neighbors.py:130-134). */
 int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,

@@ -101,16 +101,17 @@ SIGNATURES = {
     "pc_scatter_add": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_halo_pack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pc_tile_count": (c_i32, [ctypes.POINTER(PcGrid)]),
-    "pc_tile_slices": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp]),
-    "pc_tile_build": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(PcGrid),
-                                     ctypes.POINTER(PcBox), ctypes.POINTER(PcBox), c_dbl, c_i32,
-                                     c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "pc_tile_force_partials": (c_i32, [ctypes.POINTER(PcGrid)]),
-    "pc_tile_force": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(PcGrid),
-                                     ctypes.POINTER(PcBox), ctypes.POINTER(PcBox),
-                                     ctypes.POINTER(PcLJ), c_dbl, c_i32, c_i32, c_vp, c_vp,
-                                     c_vp, c_vp, c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp,
-                                     c_vp]),
+    "pc_tile_plan_ints": (c_i32, []),
+    "pc_tile_stage_cap": (c_i32, []),
+    "pc_tile_rows": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp]),
+    "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
+                                     ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp, c_vp,
+                                     c_vp, c_vp, c_vp, c_vp]),
+    "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
+                                     ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl, c_vp,
+                                     c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
+    "pc_tile_decode": (ctypes.c_int, [c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                      c_vp]),
     "pc_halo_unpack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "pc_lj_force_sell": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
                                         ctypes.POINTER(PcBox),

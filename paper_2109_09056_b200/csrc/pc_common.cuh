@@ -52,6 +52,14 @@ __device__ __forceinline__ double min_image(double d, double L, double T) {
   return d;
 }
 
+// Branch-free minimum image for wrapped coordinates (|d| < L): the fast form
+// of pc::min_image without its |d| >= L division fallback.
+__device__ __forceinline__ double min_image_wrapped(double d, double L, double T) {
+  const double a = fabs(d);
+  const double t = copysign(__dsub_rn(a, L), -d);
+  return a >= T ? t : d;
+}
+
 // numpy einsum order on this build: (x*x + z*z) + y*y, no FMA.
 __device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));

@@ -166,13 +166,6 @@ lj_force_half_kernel(const double* __restrict__ pos, int n_rows, const int* __re
 // near a periodic face, see pc_lj_force_sell), exact FP64 cutoff test, FP64
 // LJ magnitude and accumulation; energy booked half on each side of the pair.
 //
-// Branch-free minimum image for wrapped coordinates (|d| < L): the fast form
-// of pc::min_image without its |d| >= L division fallback.
-__device__ __forceinline__ double min_image_wrapped(double d, double L, double T) {
-  const double a = fabs(d);
-  const double t = copysign(__dsub_rn(a, L), -d);
-  return a >= T ? t : d;
-}
 
 // The pair magnitude is evaluated in FP64 from an approximate reciprocal
 // (MUFU.RCP64H, ~2^-22) refined by one Newton step (~2^-44): no FP32<->FP64

@@ -1,158 +1,227 @@
-// Tile-staged MD hot path: Verlet build into 16-bit slot lists and the LJ
-// force kernel that resolves those slots in shared memory.
+// Tile-staged MD hot path (sm_100a): Verlet build into per-warp "round"
+// lists of 16-bit shared-memory slots, and the LJ force kernel that resolves
+// those slots against an FP64 neighbourhood staged by the TMA engine.
 //
-// Why: with one thread per particle the 75 neighbour gathers of a warp hit
-// ~24 distinct 32-B sectors per load instruction and saturate the L1 data
-// pipe (profiles/r01: 80 % of peak, 270 us per 1M-atom force pass).  A tile
-// (one column segment of kTileZ cells, pc_tile.cuh) stages the FP64
-// positions of its 27-cell neighbourhood once per step into shared memory
-// (planar x/y/z, 8-B words), and its rows store 2-byte slots into that
-// staging area instead of 4-byte particle indices: the index stream from HBM
-// halves and the gathers become LDS.64.
+// Why (profiles/r01, profiles/r01b): with one thread per particle gathering
+// its neighbours from global memory, a warp's 32 scattered 32-B requests
+// touch ~21 distinct 128-B L1 lines per load instruction; the L1 tag/data
+// pipe serves about one line per cycle, which alone costs ~180 us of the
+// 282 us force pass at 1M atoms.  Here a CTA owns a tile of 2x2 columns x
+// kTZ cells of the linked-cell grid; the FP64 x|y|z of its 4x4 x (kTZ+2)
+// cell neighbourhood (~1900 particles, ~45 KB) is copied into shared memory
+// by cp.async.bulk (one bulk copy per contiguous index run and coordinate,
+// completing on an mbarrier), and every candidate becomes three LDS.64.
 //
-// Exactness is unchanged: the build's pair test is the reference's FP64
-// predicate (FP32 prefilter with the rigorous band of pc_nbr_build_sell),
-// and the force kernel's cutoff test is exact FP64 inside a band around rc^2
-// decided in FP32 elsewhere.  The LJ magnitude is FP32 (F2F conversions run
-// at full rate on B200, measured), accumulation FP64 (exact antisymmetry).
-#include "pc_tile.cuh"
+// Tile geometry (tile_setup, shared by the build, the force kernel and the
+// host decoder): staged column sc = sxo*4 + syo (sxo, syo in 0..3 map to grid
+// columns x0-1+sxo, y0-1+syo, periodic wrap); each staged column contributes
+// three "segments" -- the z-cell below the grid (periodic wrap, z0 == 0), the
+// in-range cells, the z-cell above the grid (wrap) -- each a contiguous run of
+// the cell-sorted particle arrays.  A segment is copied from its even-aligned
+// start (16-B TMA alignment), so slot = seg_dst + (index - seg_src).  Slots
+// [max_stage, max_stage + 16) hold NaN positions ("dummies", one per
+// LDS.64 bank pair) used as padding: a NaN r^2 fails the cutoff test.
+//
+// List layout: home rows of a tile are numbered column by column and grouped
+// in row-warps of 32.  Row-warp rw (global numbering rw0[tile] + w) holds
+// rounds[rw] rounds; in round r lane l reads slot
+//   list16[((rw*Q8 + r/8)*32 + l)*8 + r%8]
+// i.e. one 128-bit load gives a lane its next 8 slots and a warp's load is 512
+// contiguous bytes.  Every round is a row's neighbour or a dummy.
+//
+// Exactness: the build decides each candidate with FP32 coordinates relative
+// to the tile centre outside a rigorously bounded band around cutoff^2 and
+// with the reference's FP64 predicate inside it (same bound as
+// pc_nbr_build_sell); the force kernel re-tests r^2 < rc^2 in FP64 with the
+// reference's rounding order (pc_common.cuh r2_exact) on raw positions, with
+// the exact threshold minimum image on rows near a periodic face.  The LJ
+// magnitude is FP32 (r^2 narrowed by integer bit operations: FP64->FP32 F2F
+// issues at ~8 lanes/clk/SM on B200, measured, scripts/micro/pipes2.cu),
+// the force is accumulated in FP64 as f += fm*dx so pair terms are exactly
+// antisymmetric (momentum conserved to FP64 rounding).
+#include <stdlib.h>
+
+#include "pc_common.cuh"
 
 namespace pc {
 
-constexpr int kTileThreads = 32 * kTileZ;  // build: one warp per home cell
-constexpr int kForceTileThreads = 96;   // force: ~78 home rows per tile (kTileZ = 4)
+constexpr int kBX = 2, kBY = 2, kTZ = 4;
+constexpr int kSX = kBX + 2, kSY = kBY + 2, kSZ = kTZ + 2;
+constexpr int kSCols = kSX * kSY;
+constexpr int kSegs = kSCols * 3;
+constexpr int kNDummy = 16;
+constexpr int kForceWarps = 24;
+constexpr int kBuildWarps = 8;
+constexpr int kHitCap = 128;
+// force-kernel staging capacity (slots) and per-coordinate stride in shared
+// memory: compile-time so every LDS is [slot*8 + immediate]
+constexpr int kStageCap = 2304;
+constexpr int kStageStride = kStageCap + 16;
 
-struct TileBuildParams {
-  double cutoff2;
-  float lo2, hi2;
-  int Q;            // quads (4 slots) per row
-  int max_stage;    // staged particles capacity
+struct TileSetup {
+  int seg_src[kSegs];          // even-aligned first index of the copied run
+  int seg_len[kSegs];          // copied elements (even, 0 = empty)
+  int seg_dst[kSegs];          // first slot
+  float seg_shift[kSegs][3];   // periodic image (build prefilter only; exact multiples of L in FP64 below)
+  int cell_lo[kSCols][kSZ];    // slot range of each staged cell (build only)
+  int cell_hi[kSCols][kSZ];
+  int home_start[kBX * kBY];   // first particle of each home column's z-range
+  int home_pre[kBX * kBY + 1]; // tile-row offset of each home column
+  int home_cell0[kBX * kBY];   // cell_start index of the first home cell of the column
+  int S, H, bx, by, bz, z0;
+  double ox, oy, oz;           // tile centre (build prefilter origin)
 };
 
-struct TileForceParams {
-  double cutoff2, overlap2;
-  float lo2f, hi2f;    // FP32 band around cutoff^2 for the exact decision
-  float sig2, eps24, eps2;
-  double guard;        // min image only within this distance of a global face
-  int Q;
-  int max_stage;
+struct TileDims {
+  int ntx, nty, ntz, ntiles;
 };
 
-// home rows per tile -> 32-row slices -> slice offsets (scan done on host side)
-__global__ void tile_slices_kernel(const int* __restrict__ cell_start, pc_grid g, int ntiles,
-                                   int* __restrict__ slices) {
-  int tile = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tile >= ntiles) return;
-  int cx, cy, z0, z1;
-  tile_coords(tile, g, cx, cy, z0, z1);
-  const int base = (cx * g.nc[1] + cy) * g.nc[2];
-  const int nh = cell_start[base + z1] - cell_start[base + z0];
-  slices[tile] = (nh + 31) >> 5;
+__host__ __device__ inline TileDims tile_dims(const pc_grid& g) {
+  TileDims d;
+  d.ntx = (g.nc[0] + kBX - 1) / kBX;
+  d.nty = (g.nc[1] + kBY - 1) / kBY;
+  d.ntz = (g.nc[2] + kTZ - 1) / kTZ;
+  d.ntiles = d.ntx * d.nty * d.ntz;
+  return d;
 }
 
-// staged slot -> (column, cell) by binary search over the cumulative offsets
-__device__ __forceinline__ void slot_cell(const TileTable& t, int s, int& c, int& k) {
-  int lo = 0, hi = kTileCols * kTileCells - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    const int cm = mid / kTileCells, km = mid - cm * kTileCells;
-    if (t.off[cm][km] <= s) lo = mid; else hi = mid - 1;
-  }
-  c = lo / kTileCells;
-  k = lo - c * kTileCells;
-}
-
-__global__ void __launch_bounds__(kTileThreads)
-tile_build_kernel(const double* __restrict__ pos, const double* __restrict__ posb,
-                  const int* __restrict__ cell_start, pc_grid g, pc_box b, pc_box e,
-                  TileBuildParams p, const int* __restrict__ slice0, int* __restrict__ count,
-                  uint16_t* __restrict__ list, int* __restrict__ flag) {
-  extern __shared__ float4 stage[];
-  __shared__ TileTable t;
-  tile_table(blockIdx.x, g, b, cell_start, t);
-  if (t.total + 1 > p.max_stage) {       // +1: the dummy padding slot
-    if (threadIdx.x == 0) {
-      atomicOr(flag, kFlagStage);
-      atomicMax(flag + 1, t.total + 1);  // capacity the caller must provide
+// Fill T for `tile`.  All threads call it (contains barriers).  CELLS: also
+// the per-cell slot table used by the build.
+template <bool CELLS>
+__device__ void tile_setup(int tile, const pc_grid& g, const pc_box& b,
+                           const int* __restrict__ cs, TileSetup& T) {
+  const TileDims d = tile_dims(g);
+  const int tz = tile % d.ntz;
+  const int t2 = tile / d.ntz;
+  const int ty = t2 % d.nty, tx = t2 / d.nty;
+  const int x0 = tx * kBX, y0 = ty * kBY, z0 = tz * kTZ;
+  const int bx = min(kBX, g.nc[0] - x0), by = min(kBY, g.nc[1] - y0), bz = min(kTZ, g.nc[2] - z0);
+  const int nx = g.nc[0], ny = g.nc[1], nz = g.nc[2];
+  for (int e = threadIdx.x; e < kSegs; e += blockDim.x) {
+    const int col = e / 3, part = e - col * 3;
+    const int sxo = col / kSY, syo = col - sxo * kSY;
+    int gx = x0 - 1 + sxo, gy = y0 - 1 + syo;
+    bool ok = sxo <= bx + 1 && syo <= by + 1;
+    float shx = 0.f, shy = 0.f, shz = 0.f;
+    if (gx < 0) { if (b.periodic[0]) { gx += nx; shx = -1.f; } else ok = false; }
+    if (gx >= nx) { if (b.periodic[0]) { gx -= nx; shx = 1.f; } else ok = false; }
+    if (gy < 0) { if (b.periodic[1]) { gy += ny; shy = -1.f; } else ok = false; }
+    if (gy >= ny) { if (b.periodic[1]) { gy -= ny; shy = 1.f; } else ok = false; }
+    const int zlo = z0 - 1, zhi = z0 + bz;      // staged z-cells, inclusive
+    int za = 0, zb = -1;
+    if (part == 0) {
+      if (zlo < 0 && b.periodic[2]) { za = zb = nz - 1; shz = -1.f; }
+    } else if (part == 1) {
+      za = max(zlo, 0);
+      zb = min(zhi, nz - 1);
+    } else {
+      if (zhi >= nz && b.periodic[2]) { za = zb = 0; shz = 1.f; }
     }
-    return;
+    int src = 0, len = 0;
+    if (ok && zb >= za) {
+      const int base = (gx * ny + gy) * nz;
+      const int first = cs[base + za], end = cs[base + zb + 1];
+      if (end > first) {
+        src = first & ~1;
+        len = ((end + 1) & ~1) - src;
+      }
+    }
+    T.seg_src[e] = src;
+    T.seg_len[e] = len;
+    T.seg_shift[e][0] = shx;
+    T.seg_shift[e][1] = shy;
+    T.seg_shift[e][2] = shz;
   }
-  int cx, cy, z0, z1;
-  tile_coords(blockIdx.x, g, cx, cy, z0, z1);
-  const double ox = g.low[0] + (cx + 0.5) * g.width[0];
-  const double oy = g.low[1] + (cy + 0.5) * g.width[1];
-  const double oz = g.low[2] + 0.5 * (z0 + z1) * g.width[2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // stage: warp per cell, lanes over its (contiguous) particles
-  for (int e = warp; e < kTileCols * kTileCells; e += kTileThreads / 32) {
-    const int c = e / kTileCells, k = e - c * kTileCells;
-    const int m = t.off[c][k + 1] - t.off[c][k];
-    const int src = t.src[c][k], dst = t.off[c][k];
-    const double sx = t.shift[c][k][0], sy = t.shift[c][k][1], sz = t.shift[c][k][2];
-    for (int q = lane; q < m; q += 32) {
-      const double4 r = ld_pos4(posb + 4 * (int64_t)(src + q));
-      float4 v;
-      v.x = (float)(r.x + sx - ox);
-      v.y = (float)(r.y + sy - oy);
-      v.z = (float)(r.z + sz - oz);
-      v.w = __int_as_float(src + q);
-      stage[dst + q] = v;
+  if (threadIdx.x < kBX * kBY) {
+    const int c = threadIdx.x, hx = c / kBY, hy = c - hx * kBY;
+    int st = 0, cnt = 0, c0 = 0;
+    if (hx < bx && hy < by) {
+      c0 = ((x0 + hx) * ny + (y0 + hy)) * nz + z0;
+      st = cs[c0];
+      cnt = cs[c0 + bz] - st;
+    }
+    T.home_start[c] = st;
+    T.home_cell0[c] = c0;
+    T.home_pre[c + 1] = cnt;     // scanned below
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int base = 0; base < kSegs; base += 32) {
+      const int e = base + lane;
+      const int v = e < kSegs ? T.seg_len[e] : 0;
+      int inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      if (e < kSegs) T.seg_dst[e] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      T.S = carry;
+      T.home_pre[0] = 0;
+      for (int c = 0; c < kBX * kBY; ++c) T.home_pre[c + 1] += T.home_pre[c];
+      T.H = T.home_pre[kBX * kBY];
+      T.bx = bx;
+      T.by = by;
+      T.bz = bz;
+      T.z0 = z0;
+      T.ox = g.low[0] + (x0 + 0.5 * bx) * g.width[0];
+      T.oy = g.low[1] + (y0 + 0.5 * by) * g.width[1];
+      T.oz = g.low[2] + (z0 + 0.5 * bz) * g.width[2];
+    }
+  }
+  if (CELLS) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSCols * kSZ; e += blockDim.x) {
+      const int col = e / kSZ, k = e - col * kSZ;
+      int lo = 0, hi = 0;
+      if (k <= bz + 1) {
+        const int part = (k == 0 && z0 == 0) ? 0 : ((k == bz + 1 && z0 + bz == nz) ? 2 : 1);
+        const int seg = col * 3 + part;
+        if (T.seg_len[seg] > 0) {
+          const int sxo = col / kSY, syo = col - sxo * kSY;
+          const int gx = (x0 - 1 + sxo + nx) % nx, gy = (y0 - 1 + syo + ny) % ny;
+          const int gz = (z0 - 1 + k + nz) % nz;
+          const int cell = (gx * ny + gy) * nz + gz;
+          lo = T.seg_dst[seg] + (cs[cell] - T.seg_src[seg]);
+          hi = lo + (cs[cell + 1] - cs[cell]);
+        }
+      }
+      T.cell_lo[col][k] = lo;
+      T.cell_hi[col][k] = hi;
     }
   }
   __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  const int Q = p.Q;
-  const int64_t tile_base = (int64_t)slice0[blockIdx.x] * Q * 128;
-  for (int k = warp + 1; k <= t.nzh; k += kTileThreads / 32) {
-    const int hs = t.off[4][k];
-    const int hn = t.off[4][k + 1] - hs;
-    for (int h = 0; h < hn; ++h) {
-      const float4 me = stage[hs + h];
-      const int a = __float_as_int(me.w);
-      const int u = a - t.home_first;                      // row within the tile
-      uint16_t* row = list + tile_base + (int64_t)(u >> 5) * Q * 128 + (u & 31) * 4;
-      int cnt = 0;
-      for (int c = 0; c < kTileCols; ++c) {
-        const int s0 = t.off[c][k - 1], s1 = t.off[c][k + 2];
-        for (int s = s0 + lane; s - lane < s1; s += 32) {
-          bool hit = false;
-          if (s < s1) {
-            const float4 q = stage[s];
-            const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const int j = __float_as_int(q.w);
-            if (r2 < p.hi2 && j != a) {
-              if (r2 < p.lo2) {
-                hit = true;
-              } else {
-                const double4 pa = ld_pos4(pos + 4 * (int64_t)a);
-                const double4 pj = ld_pos4(pos + 4 * (int64_t)j);
-                const double ex = min_image(__dsub_rn(pj.x, pa.x), e.length[0], e.mi_thresh[0]);
-                const double ey = min_image(__dsub_rn(pj.y, pa.y), e.length[1], e.mi_thresh[1]);
-                const double ez = min_image(__dsub_rn(pj.z, pa.z), e.length[2], e.mi_thresh[2]);
-                hit = r2_exact(ex, ey, ez) < p.cutoff2;
-              }
-            }
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (hit) {
-            const int kk = cnt + __popc(m & lt);
-            if (kk < 4 * Q) row[(kk >> 2) * 128 + (kk & 3)] = (uint16_t)s;
-          }
-          cnt += __popc(m);
-        }
-      }
-      // pad the open quad with the dummy slot t.total (a NaN row in the force
-      // kernel's staging area: never interacts)
-      const int kp = cnt + lane;
-      if (lane < 4 && (kp & 3) && (kp >> 2) == (cnt >> 2) && kp < 4 * Q)
-        row[(kp >> 2) * 128 + (kp & 3)] = (uint16_t)t.total;
-      if (lane == 0) {
-        count[a] = cnt;
-        if (cnt > 4 * Q) atomicOr(flag, kFlagOverflow);
-      }
+}
+
+// tile row u -> particle index (and home column)
+__device__ __forceinline__ int home_row(const TileSetup& T, int u, int& c) {
+  c = 0;
+#pragma unroll
+  for (int k = 1; k < kBX * kBY; ++k) c += (u >= T.home_pre[k]) ? 1 : 0;
+  return T.home_start[c] + (u - T.home_pre[c]);
+}
+
+// per tile: row-warps = ceil(home rows / 32)
+__global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __restrict__ rw) {
+  const TileDims d = tile_dims(g);
+  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tile >= d.ntiles) return;
+  const int tz = tile % d.ntz, t2 = tile / d.ntz;
+  const int ty = t2 % d.nty, tx = t2 / d.nty;
+  const int x0 = tx * kBX, y0 = ty * kBY, z0 = tz * kTZ;
+  const int bx = min(kBX, g.nc[0] - x0), by = min(kBY, g.nc[1] - y0), bz = min(kTZ, g.nc[2] - z0);
+  int h = 0;
+  for (int hx = 0; hx < bx; ++hx)
+    for (int hy = 0; hy < by; ++hy) {
+      const int c0 = ((x0 + hx) * g.nc[1] + (y0 + hy)) * g.nc[2] + z0;
+      h += cs[c0 + bz] - cs[c0];
     }
-  }
+  rw[tile] = (h + 31) >> 5;
 }
 
 // ---- TMA / mbarrier helpers ----------------------------------------------
@@ -192,249 +261,739 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-// One candidate slot: FP64 displacement from the staged pos4 row (LDS.128 +
-// LDS.64), minimum image on near-face axes, the reference's exact FP64 r^2
-// and cutoff test, FP32 LJ magnitude, FP64 accumulation.
-template <bool MI>
-__device__ __forceinline__ void tile_pair(const double4* __restrict__ st, int s, double xi,
-                                          double yi, double zi, bool nx, bool ny, bool nz,
-                                          const pc_box& gb, const TileForceParams& p,
-                                          double& fx, double& fy, double& fz, double& pe,
-                                          bool& overlap) {
-  const double2 xy = *reinterpret_cast<const double2*>(st + s);
-  const double zz = reinterpret_cast<const double*>(st + s)[2];
-  double dx = __dsub_rn(xy.x, xi);
-  double dy = __dsub_rn(xy.y, yi);
-  double dz = __dsub_rn(zz, zi);
-  if (MI) {
-    if (nx) { const double a = fabs(dx); if (a >= gb.mi_thresh[0]) dx = copysign(__dsub_rn(a, gb.length[0]), -dx); }
-    if (ny) { const double a = fabs(dy); if (a >= gb.mi_thresh[1]) dy = copysign(__dsub_rn(a, gb.length[1]), -dy); }
-    if (nz) { const double a = fabs(dz); if (a >= gb.mi_thresh[2]) dz = copysign(__dsub_rn(a, gb.length[2]), -dz); }
-  }
-  const double r2 = r2_exact(dx, dy, dz);
-  if (r2 < p.cutoff2) {
-    overlap |= r2 < p.overlap2;
-    const float inv = rcp_approx((float)r2);
-    const float sr2 = p.sig2 * inv;
-    const float sr6 = sr2 * sr2 * sr2;
-    const double fm = (double)(sr6 * (2.f * sr6 - 1.f) * inv);
-    fx = fma(-fm, dx, fx);
-    fy = fma(-fm, dy, fy);
-    fz = fma(-fm, dz, fz);
-    pe += (double)(sr6 * (sr6 - 1.f));
-  }
+// streaming 128-bit load of list words (read once per step: no L1 allocation)
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
 }
 
-template <bool MI>
-__device__ __forceinline__ void tile_row(const double4* st, const ushort4* __restrict__ row,
-                                         int mq, double xi, double yi, double zi, bool nx,
-                                         bool ny, bool nz, const pc_box& gb,
-                                         const TileForceParams& p, double& fx, double& fy,
-                                         double& fz, double& pe, bool& overlap) {
-  ushort4 nxt = make_ushort4(0, 0, 0, 0);
-  if (mq > 0) nxt = __ldg(row);
-  for (int q = 0; q < mq; ++q) {
-    const ushort4 cur = nxt;
-    if (q + 1 < mq) nxt = __ldg(row + (int64_t)(q + 1) * 32);
-    tile_pair<MI>(st, cur.x, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(st, cur.y, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(st, cur.z, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-    tile_pair<MI>(st, cur.w, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-  }
+// ---- per-tile plan (written by the build, read by the force kernel) --------
+// ints: [0] non-empty segments m, [1] staged slots S, [2] row-warps, [3] rw0,
+// then m x (src, len, dst).
+constexpr int kPlanInts = 4 + 3 * kSegs;
+
+// ---- build ------------------------------------------------------------------
+struct TileBuildParams {
+  double cutoff2;
+  float lo2, hi2;      // FP32 band: r2f < lo2 -> hit, r2f >= hi2 -> miss, else exact FP64
+  int Q8;              // list capacity per row-warp, in 8-round groups
+  int max_stage;       // staged slots capacity (multiple of 16); dummies follow
+  int sched;           // 1: bank-conflict-free round schedule, 0: ascending order
+  int64_t ps;          // planar stride
+};
+
+constexpr int kWin = 8;     // scheduling window (entries a lane may pick from per round)
+constexpr int kIters = 2;   // proposal/resolution passes per round
+
+__device__ __forceinline__ bool exact_pair_pl(const double* __restrict__ pl, int64_t ps, int a,
+                                              int j, const pc_box& b, double cutoff2) {
+  const double dx = min_image(__dsub_rn(pl[j], pl[a]), b.length[0], b.mi_thresh[0]);
+  const double dy = min_image(__dsub_rn(pl[ps + j], pl[ps + a]), b.length[1], b.mi_thresh[1]);
+  const double dz =
+      min_image(__dsub_rn(pl[2 * ps + j], pl[2 * ps + a]), b.length[2], b.mi_thresh[2]);
+  return r2_exact(dx, dy, dz) < cutoff2;
 }
 
-// One CTA per tile.  Thread 0 stages the tile's neighbourhood with TMA bulk
-// copies of contiguous pos4 runs (one per z-run of each stencil column) into
-// shared memory, completing on an mbarrier; slot t.total is set to NaN (the
-// build pads rows with it).  Then one thread per home row sweeps its slot list.
-__global__ void __launch_bounds__(kForceTileThreads)
-tile_force_kernel(const double* __restrict__ pos, const int* __restrict__ cell_start,
-                  pc_grid g, pc_box b, pc_box gb, TileForceParams p,
-                  const int* __restrict__ slice0, const int* __restrict__ count,
-                  const uint16_t* __restrict__ list, double* __restrict__ f3, int64_t fs,
-                  double* __restrict__ v, int64_t vs, double dtm, double mass,
-                  double* __restrict__ partial, int* __restrict__ flag) {
-  extern __shared__ __align__(128) double4 st[];
-  __shared__ TileTable t;
-  __shared__ __align__(8) uint64_t bar;
-  tile_table(blockIdx.x, g, b, cell_start, t);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double ke = 0.0, pet = 0.0, px = 0.0, py = 0.0, pz = 0.0;
-  if (t.total + 1 > p.max_stage) {
-    if (threadIdx.x == 0) atomicOr(flag, kFlagStage);
-  } else {
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      mbar_expect_tx(&bar, (uint32_t)t.total * 32u);
-      for (int c = 0; c < kTileCols; ++c) {
-        int k = 0;
-        while (k < kTileCells) {
-          const int src = t.src[c][k];
-          int end = src + (t.off[c][k + 1] - t.off[c][k]);
-          const int dst = t.off[c][k];
-          int k2 = k + 1;
-          while (k2 < kTileCells && t.src[c][k2] == end) {   // contiguous in memory
-            end += t.off[c][k2 + 1] - t.off[c][k2];
-            ++k2;
+// Bank-conflict-free round schedule of one row-warp.  Every lane holds its
+// row's slots in ascending order (hits[k*32]); in each round each lane takes
+// one entry so that within a half-warp (one LDS.64 wavefront phase of 16
+// lanes) all lanes read distinct bank pairs (slot % 16) or the very same slot
+// (broadcast).  Greedy, kIters passes per round: every unassigned lane
+// proposes the first entry of its kWin-entry window whose residue is still
+// free in its half; per residue the winner is the lowest "critical" lane
+// (remaining entries >= the warp's maximum - 1: it bounds the round count),
+// else the lowest lane, and every lane proposing the winner's slot wins with
+// it.  Residue groups come from four ballots on the residue bits (no
+// MATCH, no per-group loops).  Lanes left unassigned read a dummy of a free
+// residue.  Simulated on LJ liquid tiles: 1.05x the rounds of the longest
+// row (unscheduled ascending order: 4.8 wavefronts per LDS.64 instead of 2).
+// Emits slot*8 (the byte offset of the slot in one coordinate array).
+__device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, int cnt,
+                                             int lane, int dummy0, uint4* __restrict__ out,
+                                             int cap_rounds) {
+  const unsigned FULL = 0xffffffffu;
+  const int half = lane >> 4;
+  const unsigned halfmask = half ? 0xFFFF0000u : 0x0000FFFFu;
+  int win[kWin];
+#pragma unroll
+  for (int i = 0; i < kWin; ++i) win[i] = i < cnt ? (int)hits[i * 32] : -1;
+  int ptr = min(cnt, kWin);
+  int rem = cnt;
+  int R = 0;
+  uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;     // 8 x u16 shift register
+  for (;;) {
+    const int maxrem = __reduce_max_sync(FULL, rem);
+    if (maxrem == 0) break;
+    const unsigned crit = __ballot_sync(FULL, rem > 0 && rem >= maxrem - 1);
+    unsigned taken = 0u;
+    int outs = -1;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      int pi = -1, ps = 0;
+      if (outs < 0 && rem > 0) {
+        if (it == 0) {
+          pi = 0;
+          ps = win[0];
+        } else {
+#pragma unroll
+          for (int i = kWin - 1; i >= 0; --i) {
+            const int sl = win[i];
+            if (sl >= 0 && !((taken >> (sl & 15)) & 1u)) { pi = i; ps = sl; }
           }
-          if (end > src)
-            bulk_g2s(st + dst, pos + 4 * (int64_t)src, (uint32_t)(end - src) * 32u, &bar);
-          k = k2;
         }
       }
-      st[t.total] = make_double4(__longlong_as_double(0x7ff8000000000000ll),
-                                 __longlong_as_double(0x7ff8000000000000ll),
-                                 __longlong_as_double(0x7ff8000000000000ll), 0.0);
+      const bool has = pi >= 0;
+      const int r = ps & 15;
+      unsigned g = __ballot_sync(FULL, has) & halfmask;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned bk = __ballot_sync(FULL, has && ((r >> k) & 1));
+        g &= ((r >> k) & 1) ? bk : ~bk;
+      }
+      const unsigned gc = g & crit;
+      const unsigned cands = gc ? gc : g;
+      const int wl = cands ? __ffs(cands) - 1 : lane;
+      const int wslot = __shfl_sync(FULL, ps, wl);
+      const unsigned all = __reduce_or_sync(FULL, has ? (1u << ((half << 4) + r)) : 0u);
+      taken |= (all >> (half << 4)) & 0xFFFFu;
+      if (has && ps == wslot) {
+        outs = ps;
+#pragma unroll
+        for (int i = 0; i < kWin - 1; ++i)
+          if (i >= pi) win[i] = win[i + 1];
+        win[kWin - 1] = ptr < cnt ? (int)hits[ptr * 32] : -1;
+        ptr += ptr < cnt ? 1 : 0;
+        --rem;
+      }
     }
-    __syncthreads();
-    mbar_wait(&bar, 0);
-    const int Q = p.Q;
-    const int64_t tile_base = (int64_t)slice0[blockIdx.x] * Q * 32;       // in ushort4
-    const int hs0 = t.off[4][1];
+    if (outs < 0) outs = dummy0 + (__ffs(~taken & 0xFFFFu) - 1);
+    b0 = __funnelshift_r(b0, b1, 16);
+    b1 = __funnelshift_r(b1, b2, 16);
+    b2 = __funnelshift_r(b2, b3, 16);
+    b3 = (b3 >> 16) | ((uint32_t)(outs * 8) << 16);
+    ++R;
+    if ((R & 7) == 0 && R <= cap_rounds) out[((R >> 3) - 1) * 32] = make_uint4(b0, b1, b2, b3);
+  }
+  if (R & 7) {     // pad the open group with conflict-free dummies
+    const uint32_t d = (uint32_t)((dummy0 + (lane & 15)) * 8);
+    for (int r = R; r & 7; ++r) {
+      b0 = __funnelshift_r(b0, b1, 16);
+      b1 = __funnelshift_r(b1, b2, 16);
+      b2 = __funnelshift_r(b2, b3, 16);
+      b3 = (b3 >> 16) | (d << 16);
+    }
+    if (((R + 7) & ~7) <= cap_rounds) out[(R >> 3) * 32] = make_uint4(b0, b1, b2, b3);
+  }
+  return R;
+}
+
+// Unscheduled rounds: entry k of every row in round k (ascending slots),
+// padded with dummies -- the cheap alternative to schedule_rows.
+__device__ __forceinline__ int plain_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
+                                          int dummy0, uint4* __restrict__ out, int cap_rounds) {
+  const int R = __reduce_max_sync(0xffffffffu, cnt);
+  const uint32_t d = (uint32_t)((dummy0 + (lane & 15)) * 8);
+  for (int r8 = 0; r8 < R && r8 + 8 <= cap_rounds; r8 += 8) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = r8 + 2 * h;
+      const uint32_t lo = r < cnt ? (uint32_t)hits[r * 32] * 8u : d;
+      const uint32_t hi = r + 1 < cnt ? (uint32_t)hits[(r + 1) * 32] * 8u : d;
+      w[h] = lo | (hi << 16);
+    }
+    out[(r8 >> 3) * 32] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  return R;
+}
+
+__global__ void __launch_bounds__(kBuildWarps * 32, 2)
+tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
+                  TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
+                  int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
+                  int* __restrict__ flag) {
+  // dynamic: staged FP32 (rel x, y, z, index) | per-warp hit lists [warp][k][lane]
+  extern __shared__ float4 st[];
+  __shared__ TileSetup T;
+  uint16_t* hits_all = reinterpret_cast<uint16_t*>(st + p.max_stage);
+  tile_setup<true>(blockIdx.x, g, b, cs, T);
+  if (T.S > p.max_stage) {
+    if (threadIdx.x == 0) {
+      atomicOr(flag, kFlagStage);
+      atomicMax(flag + 1, T.S);
+    }
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nrw = (T.H + 31) >> 5;
+  if (warp == 0) {                       // compacted plan of this tile
+    int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
+    int base = 0;
+    for (int e0 = 0; e0 < kSegs; e0 += 32) {
+      const int e = e0 + lane;
+      const bool ne = e < kSegs && T.seg_len[e] > 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, ne);
+      if (ne) {
+        const int k = base + __popc(bal & ((1u << lane) - 1u));
+        pg[4 + 3 * k] = T.seg_src[e];
+        pg[5 + 3 * k] = T.seg_len[e];
+        pg[6 + 3 * k] = T.seg_dst[e];
+      }
+      base += __popc(bal);
+    }
+    if (lane == 0) {
+      pg[0] = base;
+      pg[1] = T.S;
+      pg[2] = nrw;
+      pg[3] = rw0[blockIdx.x];
+    }
+  }
+  const int64_t ps = p.ps;
+  // stage: FP32 coordinates relative to the tile centre, periodic image applied
+  for (int e = 0; e < kSegs; ++e) {
+    const int len = T.seg_len[e];
+    if (len == 0) continue;
+    const int src = T.seg_src[e], dst = T.seg_dst[e];
+    const double sx = (double)T.seg_shift[e][0] * b.length[0] - T.ox;
+    const double sy = (double)T.seg_shift[e][1] * b.length[1] - T.oy;
+    const double sz = (double)T.seg_shift[e][2] * b.length[2] - T.oz;
+    for (int t = threadIdx.x; t < len; t += blockDim.x) {
+      const int j = src + t;
+      float4 q;
+      q.x = (float)(pl[j] + sx);
+      q.y = (float)(pl[ps + j] + sy);
+      q.z = (float)(pl[2 * ps + j] + sz);
+      q.w = __int_as_float(j);
+      st[dst + t] = q;
+    }
+  }
+  __syncthreads();
+  uint16_t* hits = hits_all + warp * kHitCap * 32 + lane;
+  for (int w = warp; w < nrw; w += kBuildWarps) {
+    const int u = w * 32 + lane;
+    const bool act = u < T.H;
+    int cnt = 0, a = -1;
+    if (act) {
+      int c;
+      a = home_row(T, u, c);
+      const int hx = c / kBY, hy = c - hx * kBY;
+      // z-cell of a within its column (staged k = cell - z0 + 1)
+      int k = 1;
+      for (int zz = 1; zz < T.bz; ++zz) k += (a >= cs[T.home_cell0[c] + zz]) ? 1 : 0;
+      const int seg = ((hx + 1) * kSY + (hy + 1)) * 3 + 1;
+      const float4 me = st[T.seg_dst[seg] + (a - T.seg_src[seg])];
+      for (int dxo = 0; dxo < 3; ++dxo) {
+        for (int dyo = 0; dyo < 3; ++dyo) {
+          const int col = (hx + dxo) * kSY + (hy + dyo);
+          for (int dk = -1; dk <= 1; ++dk) {
+            const int s0 = T.cell_lo[col][k + dk], s1 = T.cell_hi[col][k + dk];
+#pragma unroll 4
+            for (int s = s0; s < s1; ++s) {
+              const float4 q = st[s];
+              const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+              if (r2 < p.hi2) {
+                const int j = __float_as_int(q.w);
+                if (j != a && (r2 < p.lo2 || exact_pair_pl(pl, ps, a, j, b, p.cutoff2))) {
+                  if (cnt < kHitCap) hits[cnt * 32] = (uint16_t)s;
+                  ++cnt;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    const int rw = rw0[blockIdx.x] + w;
+    rowidx[(int64_t)rw * 32 + lane] = a;
+    const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+    if (cmax > kHitCap) {
+      if (lane == 0) {
+        atomicOr(flag, kFlagOverflow);
+        atomicMax(flag + 2, 1 << 20);
+      }
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    const int cap = 8 * p.Q8;
+    const int R = p.sched ? schedule_rows(hits, cnt, lane, p.max_stage,
+                                          list + (int64_t)rw * p.Q8 * 32 + lane, cap)
+                          : plain_rows(hits, cnt, lane, p.max_stage,
+                                       list + (int64_t)rw * p.Q8 * 32 + lane, cap);
+    if (lane == 0) {
+      rounds[rw] = R;
+      if (((R + 7) & ~7) > cap) {
+        atomicOr(flag, kFlagOverflow);
+        atomicMax(flag + 2, R);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- force ------------------------------------------------------------------
+// Persistent kernel: one CTA of kForceWarps warps per SM walks its tiles
+// (blockIdx.x + k*gridDim.x) through a ring of kNBuf shared-memory staging
+// buffers.  Row-warps of all its tiles form one queue (item i -> tile k by
+// the prefix of row-warp counts); a warp takes the next item, prefetches the
+// row's list / position / index words, waits on the buffer's mbarrier and
+// sweeps the rounds.  The warp finishing a tile's last row-warp frees its
+// buffer and immediately issues the TMA bulk copies of the next unloaded
+// tile into it, so staging overlaps the compute of the tiles in flight and
+// no warp idles at a tile boundary.
+constexpr int kNBuf = 4;       // max staging buffers (runtime: as many as fit)
+
+struct TileForceParams {
+  double cutoff2, overlap2;
+  float sig2;
+  double eps24d, eps2d;
+  double guard;        // minimum image only within this distance of a periodic face
+  int Q8;
+  int64_t ps;
+};
+
+struct ForceShared {
+  uint64_t bar[kNBuf];
+  volatile int seq[kNBuf];   // tile sequence index held by each buffer (-1: none)
+  int par[kNBuf];            // mbarrier parity of the current use
+  int uses[kNBuf];
+  int done[kNBuf];           // finished row-warps of the current tile
+  int next_item;
+  int loaded;                // tickets: next tile sequence index to load
+  int K;                     // tiles of this CTA
+  int items;                 // row-warps of this CTA
+};
+
+// FP64 -> FP32 by truncation in two integer instructions (SHF.L.W + IADD):
+// the funnel shift moves exponent bits 8..0 and 23 mantissa bits into place,
+// +0x40000000 rebiases the 9-bit exponent field modulo 512 (1023 - 127 = 896
+// = 384 mod 512, -384 = 128 mod 512).  Exact for positive v with FP32-normal
+// magnitude (an interacting pair's r^2); anything else is garbage, which the
+// caller replaces by a select.
+__device__ __forceinline__ float d2f_fast(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v);
+  const unsigned lo = (unsigned)__double2loint(v);
+  return __uint_as_float(__funnelshift_l(lo, hi, 3) + 0x40000000u);
+}
+
+// One round: `off` is the byte offset of the slot in a coordinate array.
+template <bool MI, bool UNIT_SIGMA>
+__device__ __forceinline__ void tile_pair(const char* __restrict__ st, uint32_t off, double xi,
+                                          double yi, double zi, bool nx, bool ny, bool nz,
+                                          const pc_box& b, const TileForceParams& p, double& fx,
+                                          double& fy, double& fz, float& pe, bool& overlap) {
+  const double* q = reinterpret_cast<const double*>(st + off);
+  double dx = __dsub_rn(q[0], xi);
+  double dy = __dsub_rn(q[kStageStride], yi);
+  double dz = __dsub_rn(q[2 * kStageStride], zi);
+  if (MI) {
+    // staged coordinates are wrapped into the box: |d| < L, so the exact
+    // threshold form needs no division fallback (dummies: 1e30 stays huge)
+    if (nx) dx = min_image_wrapped(dx, b.length[0], b.mi_thresh[0]);
+    if (ny) dy = min_image_wrapped(dy, b.length[1], b.mi_thresh[1]);
+    if (nz) dz = min_image_wrapped(dz, b.length[2], b.mi_thresh[2]);
+  }
+  const double r2 = r2_exact(dx, dy, dz);
+  const bool inter = r2 < p.cutoff2;
+  overlap |= r2 < p.overlap2;
+  // branch-free: a non-interacting lane evaluates the pair at r^2 = 1e30
+  // (all terms underflow to exactly 0; 0 * dx = 0 for the finite dummies)
+  const float r2f = inter ? d2f_fast(r2) : 1e30f;
+  const float inv = rcp_approx(r2f);
+  const float sr2 = UNIT_SIGMA ? inv : p.sig2 * inv;
+  const float sr6 = sr2 * sr2 * sr2;
+  const float fm = (sr6 * inv) * fmaf(2.0f, sr6, -1.0f);     // (2 sr12 - sr6) / r2
+  pe += fmaf(sr6, sr6, -sr6);                                  // sr12 - sr6
+  const double fmd = (double)fm;
+  fx = fma(-fmd, dx, fx);
+  fy = fma(-fmd, dy, fy);
+  fz = fma(-fmd, dz, fz);
+}
+
+template <bool MI, bool UNIT_SIGMA>
+__device__ __forceinline__ void tile_row(const char* __restrict__ st,
+                                         const uint4* __restrict__ lp, uint4 first, int R,
+                                         double xi, double yi, double zi, bool nx, bool ny,
+                                         bool nz, const pc_box& b, const TileForceParams& p,
+                                         double& fx, double& fy, double& fz, float& pe,
+                                         bool& overlap) {
+  const int G = (R + 7) >> 3;     // 8-round groups; the open group is padded with dummies
+  uint4 nxt = first;
+  for (int gi = 0; gi < G; ++gi) {
+    const uint4 q = nxt;
+    if (gi + 1 < G) nxt = ld_stream(lp + (gi + 1) * 32);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      tile_pair<MI, UNIT_SIGMA>(st, w[h] & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz,
+                                pe, overlap);
+      tile_pair<MI, UNIT_SIGMA>(st, w[h] >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+                                overlap);
+    }
+  }
+}
+
+// whole warp: stage tile sequence k of this CTA into buffer b
+__device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ stage, int b,
+                                           int k, const int* __restrict__ plan,
+                                           const double* __restrict__ pl, int64_t ps, int lane) {
+  const int tile = blockIdx.x + k * gridDim.x;
+  const int* gp = plan + (int64_t)tile * kPlanInts;
+  const int m = gp[0], S = gp[1];
+  double* st = stage + (int64_t)b * 3 * kStageStride;
+  if (lane == 0) {
+    F.done[b] = 0;
+    F.par[b] = F.uses[b] & 1;
+    F.uses[b] += 1;
+    mbar_expect_tx(&F.bar[b], (uint32_t)S * 24u);
+  }
+  __syncwarp();
+  for (int e = lane; e < m; e += 32) {
+    const int src = gp[4 + 3 * e], len = gp[5 + 3 * e], dst = gp[6 + 3 * e];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      bulk_g2s(st + a * kStageStride + dst, pl + a * ps + src, (uint32_t)len * 8u, &F.bar[b]);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    F.seq[b] = k;
+  }
+}
+
+template <bool UNIT_SIGMA>
+__global__ void __launch_bounds__(kForceWarps * 32, 1)
+tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
+                  const int* __restrict__ plan, const int* __restrict__ rowidx,
+                  const int* __restrict__ rounds, const uint4* __restrict__ list, pc_box b,
+                  double* __restrict__ f3, int64_t fs, double* __restrict__ v, int64_t vs,
+                  double dtm, double mass, double* __restrict__ partial, int* __restrict__ flag,
+                  int nbuf) {
+  extern __shared__ double dyn[];
+  double* stage = dyn;                                             // nbuf x (x|y|z)
+  int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
+  __shared__ ForceShared F;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (warp == 0) {
+    // row-warp prefix over this CTA's tiles
+    int carry = 0;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      const int k = k0 + lane;
+      const int c = k < K ? plan[(int64_t)(blockIdx.x + k * gridDim.x) * kPlanInts + 2] : 0;
+      int inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      if (k < K) pre[k] = carry + inc - c;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      pre[K] = carry;
+      F.items = carry;
+      F.K = K;
+      F.next_item = 0;
+      for (int q = 0; q < kNBuf; ++q) {
+        F.seq[q] = -1;
+        F.uses[q] = 0;
+        mbar_init(&F.bar[q], 1);
+      }
+      F.loaded = min(K, nbuf);
+    }
+    __syncwarp();
+    for (int q = 0; q < min(K, nbuf); ++q) force_load(F, stage, q, q, plan, pl, p.ps, lane);
+  } else if (warp == 1) {
+    for (int q = 0; q < nbuf; ++q)
+      if (lane < kNDummy)
+        for (int a = 0; a < 3; ++a) stage[(q * 3 + a) * kStageStride + kStageCap + lane] = 1e30;
+  }
+  __syncthreads();
+  const int items = F.items;
+
+  for (;;) {
+    int i = 0;
+    if (lane == 0) i = atomicAdd(&F.next_item, 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= items) break;
+    // tile sequence index of item i (pre is ascending; K is small)
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pre[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    const int k = lo;
+    const int tile = blockIdx.x + k * gridDim.x;
+    const int rw = plan[(int64_t)tile * kPlanInts + 3] + (i - pre[k]);
+    // prefetch everything that does not depend on the staged tile
+    const int a = rowidx[(int64_t)rw * 32 + lane];
+    const int R = rounds[rw];
+    const uint4* lp = list + (int64_t)rw * p.Q8 * 32 + lane;
+    const uint4 first = R > 0 ? ld_stream(lp) : make_uint4(0u, 0u, 0u, 0u);
+    const bool act = a >= 0;
+    double xi = 0.0, yi = 0.0, zi = 0.0;
+    if (act) {
+      xi = pl[a];
+      yi = pl[p.ps + a];
+      zi = pl[2 * p.ps + a];
+    }
+    // buffer holding tile k (loaded in ticket order; spin until published)
+    int bsel = -1;
+    for (;;) {
+#pragma unroll
+      for (int q = 0; q < kNBuf; ++q)
+        if (F.seq[q] == k) bsel = q;
+      if (bsel >= 0) break;
+      __nanosleep(64);
+    }
+    __threadfence_block();
+    mbar_wait(&F.bar[bsel], (uint32_t)F.par[bsel]);
+    const char* st = reinterpret_cast<const char*>(stage + (int64_t)bsel * 3 * kStageStride);
+
+    const bool nx = act && b.periodic[0] && (xi - b.low[0] < p.guard || b.high[0] - xi <= p.guard);
+    const bool ny = act && b.periodic[1] && (yi - b.low[1] < p.guard || b.high[1] - yi <= p.guard);
+    const bool nz = act && b.periodic[2] && (zi - b.low[2] < p.guard || b.high[2] - zi <= p.guard);
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    float pe = 0.f;
     bool overlap = false;
-    for (int u = threadIdx.x; u < t.nhome; u += blockDim.x) {
-      const int a = t.home_first + u;
-      const double4 me = st[hs0 + u];
-      const double xi = me.x, yi = me.y, zi = me.z;
-      const int m = count[a];
-      const bool nx = gb.periodic[0] && (xi - gb.low[0] < p.guard || gb.high[0] - xi <= p.guard);
-      const bool ny = gb.periodic[1] && (yi - gb.low[1] < p.guard || gb.high[1] - yi <= p.guard);
-      const bool nz = gb.periodic[2] && (zi - gb.low[2] < p.guard || gb.high[2] - zi <= p.guard);
-      const ushort4* row = reinterpret_cast<const ushort4*>(list) + tile_base +
-                           (int64_t)(u >> 5) * Q * 32 + (u & 31);
-      double fx = 0.0, fy = 0.0, fz = 0.0, pe = 0.0;
-      const int mq = (m + 3) >> 2;
-      if (__any_sync(__activemask(), nx || ny || nz))
-        tile_row<true>(st, row, mq, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-      else
-        tile_row<false>(st, row, mq, xi, yi, zi, nx, ny, nz, gb, p, fx, fy, fz, pe, overlap);
-      fx *= (double)p.eps24;
-      fy *= (double)p.eps24;
-      fz *= (double)p.eps24;
+    if (__any_sync(0xffffffffu, nx || ny || nz))
+      tile_row<true, UNIT_SIGMA>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+                                 overlap);
+    else
+      tile_row<false, UNIT_SIGMA>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+                                  overlap);
+    // release the buffer when this was the tile's last row-warp; refill it
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&F.done[bsel], 1) + 1 == pre[k + 1] - pre[k];
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      int kn = 0;
+      if (lane == 0) {
+        F.seq[bsel] = -1;
+        kn = atomicAdd(&F.loaded, 1);
+      }
+      kn = __shfl_sync(0xffffffffu, kn, 0);
+      if (kn < K) force_load(F, stage, bsel, kn, plan, pl, p.ps, lane);
+    }
+    if (overlap) atomicOr(flag, kFlagOverlap);
+    double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0, ped = 0.0;
+    if (act) {
+      fx *= p.eps24d;
+      fy *= p.eps24d;
+      fz *= p.eps24d;
+      ped = (double)pe * p.eps2d;
       f3[a] = fx;
       f3[fs + a] = fy;
       f3[2 * fs + a] = fz;
-      pet += pe * (double)p.eps2;
       if (v) {
+        // numpy: v[:o] += dtm * f[:o]  (ref md.py:251-257), no contraction
         const double vx = __dadd_rn(v[a], __dmul_rn(dtm, fx));
         const double vy = __dadd_rn(v[vs + a], __dmul_rn(dtm, fy));
         const double vz = __dadd_rn(v[2 * vs + a], __dmul_rn(dtm, fz));
         v[a] = vx;
         v[vs + a] = vy;
         v[2 * vs + a] = vz;
-        ke += __dmul_rn(0.5 * mass, r2_exact(vx, vy, vz));
-        px += mass * vx;
-        py += mass * vy;
-        pz += mass * vz;
+        ke = __dmul_rn(0.5 * mass, r2_exact(vx, vy, vz));
+        px = mass * vx;
+        py = mass * vy;
+        pz = mass * vz;
       }
     }
-    if (overlap) atomicOr(flag, kFlagOverlap);
-  }
-  if (partial) {
-    ke = warp_sum(ke);
-    pet = warp_sum(pet);
-    px = warp_sum(px);
-    py = warp_sum(py);
-    pz = warp_sum(pz);
-    if (lane == 0) {
-      double* o = partial + ((int64_t)blockIdx.x * (kForceTileThreads / 32) + warp) * 5;
-      o[0] = ke; o[1] = pet; o[2] = px; o[3] = py; o[4] = pz;
+    if (partial) {
+      ke = warp_sum(ke);
+      ped = warp_sum(ped);
+      px = warp_sum(px);
+      py = warp_sum(py);
+      pz = warp_sum(pz);
+      if (lane == 0) {
+        double* o = partial + (int64_t)rw * 5;
+        o[0] = ke; o[1] = ped; o[2] = px; o[3] = py; o[4] = pz;
+      }
     }
   }
 }
 
-static double band_margin(const pc_grid& g, double cutoff2) {
-  const double U = fmax(fmax(1.5 * g.width[0], 1.5 * g.width[1]), (kTileZ / 2.0 + 1.0) * g.width[2]);
-  const double rc = sqrt(cutoff2);
-  const double e23 = ldexp(1.0, -23), e24 = ldexp(1.0, -24);
-  const double err = 2.0 * sqrt(3.0) * rc * (e23 * U + e24 * rc) + 3.0 * e24 * cutoff2;
-  return 8.0 * err + 1e-12 * cutoff2;
+// ---- decode: tile lists -> per-row dense table of particle indices ---------
+__global__ void __launch_bounds__(256)
+tile_decode_kernel(const int* __restrict__ plan, int Q8, int max_stage,
+                   const int* __restrict__ rowidx, const int* __restrict__ rounds,
+                   const uint4* __restrict__ list, int width, int* __restrict__ count,
+                   int* __restrict__ table) {
+  __shared__ int pg[kPlanInts];
+  const int* gp = plan + (int64_t)blockIdx.x * kPlanInts;
+  for (int i = threadIdx.x; i < kPlanInts; i += blockDim.x) pg[i] = gp[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = pg[0], nrw = pg[2];
+  for (int w = warp; w < nrw; w += blockDim.x / 32) {
+    const int rw = pg[3] + w;
+    const int a = rowidx[(int64_t)rw * 32 + lane];
+    if (a < 0) continue;
+    const int R = rounds[rw];
+    const uint16_t* lp = reinterpret_cast<const uint16_t*>(list + (int64_t)rw * Q8 * 32 + lane);
+    int cnt = 0;
+    for (int r = 0; r < R; ++r) {
+      const int s = lp[(r >> 3) * 32 * 8 + (r & 7)] >> 3;
+      if (s >= max_stage) continue;
+      int e = 0;
+      while (e < m - 1 && !(s >= pg[6 + 3 * e] && s < pg[6 + 3 * e] + pg[5 + 3 * e])) ++e;
+      const int j = pg[4 + 3 * e] + (s - pg[6 + 3 * e]);
+      if (cnt < width) table[(int64_t)a * width + cnt] = j;
+      ++cnt;
+    }
+    count[a] = cnt;
+  }
 }
-
-static int g_build_smem = 0, g_force_smem = 0;
 
 }  // namespace pc
 
 using namespace pc;
 
+namespace {
+int g_build_smem = 0, g_force_smem = 0;
+}
+
 extern "C" {
 
-int32_t pc_tile_count(const pc_grid* grid) {
-  return grid->nc[0] * grid->nc[1] * ((grid->nc[2] + kTileZ - 1) / kTileZ);
+int32_t pc_tile_count(const pc_grid* grid) { return tile_dims(*grid).ntiles; }
+int32_t pc_tile_plan_ints(void) { return kPlanInts; }
+int32_t pc_tile_stage_cap(void) { return kStageCap; }
+
+int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw, void* stream) {
+  const int nt = tile_dims(*grid).ntiles;
+  if (nt <= 0) return PC_OK;
+  tile_rows_kernel<<<(nt + 127) / 128, 128, 0, as_stream(stream)>>>(d_cell_start, *grid, d_rw);
+  return check_launch("pc_tile_rows");
 }
 
-int pc_tile_slices(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_slices,
-                   void* stream) {
-  const int nt = pc_tile_count(grid);
-  tile_slices_kernel<<<(nt + 255) / 256, 256, 0, as_stream(stream)>>>(d_cell_start, *grid, nt,
-                                                                      d_slices);
-  return check_launch("pc_tile_slices");
-}
-
-int pc_tile_build(const double* d_pos, const double* d_posb, const int32_t* d_cell_start,
-                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_exact,
-                  double cutoff2, int32_t width, int32_t max_stage, const int32_t* d_slice0,
-                  int32_t* d_count, uint16_t* d_list, int32_t* d_flag, void* stream) {
-  if (width % 4 || width <= 0 || max_stage > 65535) {
-    set_error("pc_tile_build: width must be a positive multiple of 4, max_stage <= 65535");
+int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,
+                  const pc_grid* grid, const pc_box* box, double cutoff2, int32_t q8,
+                  const int32_t* d_rw0, int32_t* d_plan, int32_t* d_rowidx, int32_t* d_rounds,
+                  void* d_list, int32_t* d_flag, void* stream) {
+  if (q8 <= 0 || planar_stride % 16) {
+    set_error("pc_tile_build: bad list capacity or planar stride");
     return PC_ERR_VALUE;
   }
   for (int a = 0; a < 3; ++a)
-    if (box_local->periodic[a] && grid->nc[a] < 3) {
-      set_error("pc_tile_build: periodic axis with fewer than 3 cells");
+    if (grid->nc[a] < 3 || grid->ndim != 3) {
+      set_error("pc_tile_build: needs >= 3 cells per axis in 3-D");
       return PC_ERR_VALUE;
     }
+  // FP32 prefilter band (same bound as pc_nbr_build_sell): |coordinate
+  // relative to the tile centre| <= U
+  const double U = fmax(fmax((kBX / 2.0 + 1.0) * grid->width[0], (kBY / 2.0 + 1.0) * grid->width[1]),
+                        (kTZ / 2.0 + 1.0) * grid->width[2]);
+  const double rc = sqrt(cutoff2);
+  const double e23 = ldexp(1.0, -23), e24 = ldexp(1.0, -24);
+  const double err = 2.0 * sqrt(3.0) * rc * (e23 * U + e24 * rc) + 3.0 * e24 * cutoff2;
+  const double margin = 8.0 * err + 1e-12 * cutoff2;
   TileBuildParams p;
-  const double margin = band_margin(*grid, cutoff2);
   p.cutoff2 = cutoff2;
   p.lo2 = nextafterf((float)(cutoff2 - margin), -INFINITY);
   p.hi2 = nextafterf((float)(cutoff2 + margin), INFINITY);
-  p.Q = width / 4;
-  p.max_stage = max_stage;
-  const int smem = max_stage * (int)sizeof(float4);
+  p.Q8 = q8;
+  p.max_stage = kStageCap;
+  p.sched = getenv("PC_TILE_NOSCHED") ? 0 : 1;
+  p.ps = planar_stride;
+  const int smem = (kStageCap + kNDummy) * (int)sizeof(float4) +
+                   kBuildWarps * kHitCap * 32 * (int)sizeof(uint16_t);
   if (smem > g_build_smem) {
-    cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess) {
+      set_error("pc_tile_build: %d B of shared memory not available", smem);
+      return PC_ERR_CAPACITY;
+    }
     g_build_smem = smem;
   }
-  const int nt = pc_tile_count(grid);
-  tile_build_kernel<<<nt, kTileThreads, smem, as_stream(stream)>>>(
-      d_pos, d_posb ? d_posb : d_pos, d_cell_start, *grid, *box_local,
-      box_exact ? *box_exact : *box_local, p, d_slice0, d_count, d_list, d_flag);
+  const int nt = tile_dims(*grid).ntiles;
+  tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
+      d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
+      reinterpret_cast<uint4*>(d_list), d_flag);
   return check_launch("pc_tile_build");
 }
 
-int32_t pc_tile_force_partials(const pc_grid* grid) {
-  return pc_tile_count(grid) * (kForceTileThreads / 32);
-}
-
-int pc_tile_force(const double* d_pos, const int32_t* d_cell_start,
-                  const pc_grid* grid, const pc_box* box_local, const pc_box* box_global,
-                  const pc_lj* lj, double mi_guard, int32_t width, int32_t max_stage,
-                  const int32_t* d_slice0, const int32_t* d_count, const uint16_t* d_list,
-                  double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride, double dtm,
-                  double mass, double* d_partial, int32_t* d_flag, void* stream) {
+int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
+                  const int32_t* d_plan, const int32_t* d_rowidx, const int32_t* d_rounds,
+                  const void* d_list, int32_t q8, const pc_box* box, const pc_lj* lj,
+                  double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
+                  double dtm, double mass, double* d_partial, int32_t* d_flag, void* stream) {
+  if (q8 <= 0 || planar_stride % 16) {
+    set_error("pc_tile_force: bad list capacity or planar stride");
+    return PC_ERR_VALUE;
+  }
+  if (ntiles <= 0) return PC_OK;
   TileForceParams p;
   p.cutoff2 = lj->cutoff2;
   p.overlap2 = lj->overlap2;
-  // FP32 r^2 from FP32-rounded FP64 displacements: relative error < 4 ulp
-  p.lo2f = nextafterf((float)(lj->cutoff2 * (1.0 - 1e-5)), -INFINITY);
-  p.hi2f = nextafterf((float)(lj->cutoff2 * (1.0 + 1e-5)), INFINITY);
   p.sig2 = (float)(lj->sigma * lj->sigma);
-  p.eps24 = (float)(24.0 * lj->epsilon);
-  p.eps2 = (float)(2.0 * lj->epsilon);
+  p.eps24d = 24.0 * lj->epsilon;
+  p.eps2d = 2.0 * lj->epsilon;
   p.guard = mi_guard;
-  p.Q = width / 4;
-  p.max_stage = max_stage;
-  const int smem = max_stage * (int)sizeof(double4);
+  p.Q8 = q8;
+  p.ps = planar_stride;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int grid = ntiles < sms ? ntiles : sms;
+  const int K = (ntiles + grid - 1) / grid;
+  // as many staging buffers as fit next to the item prefix (2..kNBuf)
+  static int smem_max = 0;
+  if (smem_max == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem_max <= 0) smem_max = 227 * 1024;
+  }
+  const int buf_bytes = 3 * kStageStride * (int)sizeof(double);
+  const int pre_bytes = (K + 1) * (int)sizeof(int);
+  const int static_bytes = 512;
+  int nbuf = kNBuf;
+  while (nbuf > 2 && nbuf * buf_bytes + pre_bytes + static_bytes > smem_max) --nbuf;
+  const int smem = nbuf * buf_bytes + pre_bytes;
+  if (smem + static_bytes > smem_max) {
+    set_error("pc_tile_force: %d tiles per CTA do not fit in shared memory", K);
+    return PC_ERR_CAPACITY;
+  }
+  const bool unit = lj->sigma == 1.0;
   if (smem > g_force_smem) {
-    cudaFuncSetAttribute(tile_force_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e1 = cudaFuncSetAttribute(tile_force_kernel<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e2 = cudaFuncSetAttribute(tile_force_kernel<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      set_error("pc_tile_force: %d B of shared memory not available", smem);
+      return PC_ERR_CAPACITY;
+    }
     g_force_smem = smem;
   }
-  const int nt = pc_tile_count(grid);
-  tile_force_kernel<<<nt, kForceTileThreads, smem, as_stream(stream)>>>(
-      d_pos, d_cell_start, *grid, *box_local, *box_global, p, d_slice0,
-      d_count, d_list, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag);
+  if (unit)
+    tile_force_kernel<true><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
+        d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf);
+  else
+    tile_force_kernel<false><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
+        d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf);
   return check_launch("pc_tile_force");
+}
+
+int pc_tile_decode(int32_t ntiles, const int32_t* d_plan, const int32_t* d_rowidx,
+                   const int32_t* d_rounds, const void* d_list, int32_t q8, int32_t width,
+                   int32_t* d_count, int32_t* d_table, void* stream) {
+  if (ntiles <= 0) return PC_OK;
+  tile_decode_kernel<<<ntiles, 256, 0, as_stream(stream)>>>(
+      d_plan, q8, kStageCap, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list), width,
+      d_count, d_table);
+  return check_launch("pc_tile_decode");
 }
 
 }  // extern "C"

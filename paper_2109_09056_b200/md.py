@@ -190,7 +190,7 @@ class MDDriver:
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
                  time_phases: bool = True, state=None, planar_gather: bool = True,
-                 tile: bool = False, max_stage: int = 1216, half_list: bool = False):
+                 tile: bool = True, half_list: bool = False):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -239,8 +239,9 @@ class MDDriver:
         # see pc_lj_force_sell in include/particula_b200.h)
         self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
         self.used_staged = None
-        # tile-staged path (pc_tile.cu): shared-memory neighbourhoods + 16-bit
-        # slot lists; falls back to the SELL path for small or dense grids
+        # tile-staged path (pc_tile.cu, the default): TMA-staged shared-memory
+        # neighbourhoods + 16-bit slot lists in per-warp rounds; falls back to
+        # the SELL path for grids with < 3 cells on an axis or extreme density
         self.tile = bool(tile) and not half_list
         # Newton-3 half list (pc_lj_force_sell_half): each pair once, FP64
         # atomics for the neighbour side, kick as a separate pass
@@ -249,18 +250,22 @@ class MDDriver:
         self.partial_k = torch.zeros((int(_lib.load().pc_lj_force_blocks(n)), 5),
                                      dtype=torch.float64, device=dev)
         self.diag_k = torch.zeros(5, dtype=torch.float64, device=dev)
-        self.max_stage = int(max_stage)
         self.mode = "sell"
         self._tlist = None
-        # planar x|y|z copy (stride cap+1, NaN dummy row) read by the force
-        # gathers: 24 B in 8-B items per candidate instead of one 32-B pos4
+        self._tplan = None
+        # tile list capacity: rounds per row-warp (in groups of 8), grown on
+        # demand by the build
+        k_est = 4.0 / 3.0 * np.pi * self.search ** 3 * n / np.prod(self.box.lengths)
+        self._q8 = max(2, -(-int(k_est * 1.45 + 8) // 8))
+        # planar x|y|z copy (stride _ps: a multiple of 16 elements, NaN rows
+        # from cap on) -- the TMA staging source of the tile path and the
+        # gather source of the SELL force kernel (24 B in 8-B items)
         self.planar_gather = planar_gather
-        self.pl = None
-        if planar_gather:
-            self.pl = torch.empty((3, self.cap + 1), dtype=torch.float64, device=dev)
-            self.pl[:, self.cap] = float("nan")
+        self._ps = -(-(self.cap + 1) // 16) * 16
+        self.pl = torch.empty((3, self._ps), dtype=torch.float64, device=dev)
+        self.pl[:, self.cap:] = float("nan")
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
-        self.build_flag = torch.zeros(2, dtype=torch.int32, device=dev)  # overflow, need
+        self.build_flag = torch.zeros(3, dtype=torch.int32, device=dev)  # flags, need, rounds
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))   # per-warp rows
         self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
@@ -300,8 +305,7 @@ class MDDriver:
             _kernels.gather_rows(self.vel[a], srt.order, n, out=self._vel_alt[a])
         self.pos, self._pos_alt = self._pos_alt, self.pos
         self.vel, self._vel_alt = self._vel_alt, self.vel
-        if self.pl is not None:
-            call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self.cap + 1, s)
+        call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
         e0 = self._t0()
         self._cell_start = srt.cell_start
@@ -341,41 +345,46 @@ class MDDriver:
         self.rebuilds += 1
 
     def _tile_build(self, cell_start) -> bool:
-        """Tile slot-list build (pc_tile.cu); False when this grid or density
+        """Tile round-list build (pc_tile.cu); False when this grid or density
         does not fit the tile path (the SELL path then runs)."""
         g = self._grid
-        if min(g.nc[0], g.nc[1], g.nc[2]) < 3 or self.pl is None:
+        if min(g.nc[0], g.nc[1], g.nc[2]) < 3 or g.ndim != 3:
             return False
-        lib, s = _lib.load(), stream()
+        lib, s, dev = _lib.load(), stream(), self.device
         nt = int(lib.pc_tile_count(g))
-        slices = torch.empty(nt, dtype=torch.int32, device=self.device)
-        call("pc_tile_slices", ptr(cell_start), g, ptr(slices), s)
-        self._slice0 = _kernels.scan_i32(slices)
-        total = int(self._slice0[nt].item())
+        rw = torch.empty(nt, dtype=torch.int32, device=dev)
+        call("pc_tile_rows", ptr(cell_start), g, ptr(rw), s)
+        self._rw0 = _kernels.scan_i32(rw)
+        total = int(self._rw0[nt].item())
+        self._ntiles = nt
+        if self._tlist is None or self._rounds.numel() < total:
+            grow = int(total * 1.05) + 16
+            self._rounds = torch.empty(grow, dtype=torch.int32, device=dev)
+            self._rowidx = torch.empty(grow * 32, dtype=torch.int32, device=dev)
+        if self._tplan is None or self._tplan.numel() < nt * int(lib.pc_tile_plan_ints()):
+            self._tplan = torch.empty(nt * int(lib.pc_tile_plan_ints()), dtype=torch.int32,
+                                      device=dev)
         while True:
-            need = total * self.ell_width * 32
+            need = total * self._q8 * 512
             if self._tlist is None or self._tlist.numel() < need:
-                self._tlist = torch.empty(int(need * 1.1) + 64, dtype=torch.int16,
-                                          device=self.device)
+                self._tlist = torch.empty(int(need * 1.05) + 512, dtype=torch.uint8, device=dev)
             self.build_flag.zero_()
-            call("pc_tile_build", ptr(self.pos), None, ptr(cell_start), g, self._pbox,
-                 self._pbox, self._search2, self.ell_width, self.max_stage, ptr(self._slice0),
-                 ptr(self.cnt), ptr(self._tlist), ptr(self.build_flag), s)
-            fl, need = (int(v) for v in self.build_flag.cpu())
-            if fl & _lib.FLAG_STAGE:
-                # grow the staging capacity (force kernel: 32 B per slot, < 227 KB)
-                cap = int(need * 1.15) + 32
-                if cap * 32 > 220 * 1024 or cap > 65535:
+            call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
+                 self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
+                 ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
+            fl, need_stage, need_rounds = (int(v) for v in self.build_flag.cpu())
+            if fl & _lib.FLAG_STAGE:           # neighbourhood beyond the smem staging area
+                return False
+            if fl & _lib.FLAG_OVERFLOW:
+                if need_rounds >= 1 << 20:      # a row beyond the build's hit capacity
                     return False
-                self.max_stage = cap
+                self._q8 = -(-(need_rounds + 8) // 8)
                 continue
-            if not (fl & _lib.FLAG_OVERFLOW):
-                break
-            self.ell_width = -(-(int(self.cnt[: self.n].max().item()) + 8) // 4) * 4
+            break
         self.mode = "tile"
-        self._nblk = int(lib.pc_tile_force_partials(g))
+        self._nblk = total
         if self._nblk > self.partial.shape[0]:
-            self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=self.device)
+            self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         return True
 
     def _force(self, kick_dtm):
@@ -384,18 +393,19 @@ class MDDriver:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
         if self.mode == "tile":
-            call("pc_tile_force", ptr(self.pos), ptr(self._cell_start), self._grid,
-                 self._pbox, self._pbox, self._lj, self._mi_guard, self.ell_width,
-                 self.max_stage, ptr(self._slice0), ptr(self.cnt), ptr(self._tlist),
-                 ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
-                 float(self.cfg.mass), ptr(self.partial), ptr(self.flag), stream())
+            call("pc_tile_force", ptr(self.pl), self._ps, self._ntiles, ptr(self._tplan),
+                 ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._pbox,
+                 self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
+                 stream())
         elif self.mode == "half":
             self.frc.zero_()
             call("pc_lj_force_sell_half", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
                  self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
                  ptr(self.partial), ptr(self.flag), stream())
         else:
-            call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n,
+            call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl) if self.planar_gather else None,
+                 self._ps, self.n,
                  ptr(self.cnt), ptr(self.nbr),
                  self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
                  ptr(self.vel), self.cap, float(kick_dtm), float(self.cfg.mass),
@@ -418,7 +428,7 @@ class MDDriver:
         e0 = self._t0()
         call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
              self.cap, self.n, self._dtm, float(self.cfg.dt), self._pbox, ptr(self.pl),
-             self.cap + 1, stream())
+             self._ps, stream())
         self._t1("integrate", e0)
 
     def step(self, step_index: int):
@@ -473,13 +483,17 @@ class MDDriver:
         (counts, offsets, indices), rows in id order, row entries sorted --
         the layout of ref neighbors.build_verlet for parity checks."""
         n, Q = self.n, self.ell_width // 4
-        cnt = self.cnt[:n].to(torch.int64).cpu().numpy()
         gid = self.pos[:n, 3].contiguous().view(torch.int64).cpu().numpy()
-        a = np.repeat(np.arange(n), cnt)
-        k = np.arange(a.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
         if self.mode == "tile":
-            j = self._tile_decode(a, k, Q)
+            cnt_t, table = self._tile_rows()
+            cnt = cnt_t.to(torch.int64).cpu().numpy()
+            a = np.repeat(np.arange(n), cnt)
+            k = np.arange(a.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+            j = table.cpu().numpy()[a, k]
         else:
+            cnt = self.cnt[:n].to(torch.int64).cpu().numpy()
+            a = np.repeat(np.arange(n), cnt)
+            k = np.arange(a.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
             words = self.nbr.cpu().numpy()
             w = ((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)
             j = words[w]
@@ -489,47 +503,23 @@ class MDDriver:
         offsets = np.concatenate(([0], np.cumsum(counts)))
         return counts, offsets, nb_gid[o]
 
-    def _tile_decode(self, rows, ks, Q):
-        """Host replica of the tile slot enumeration (pc_tile.cuh) to map
-        tile slot lists back to particle rows (test/inspection only)."""
-        g = self._grid
-        nc = [g.nc[0], g.nc[1], g.nc[2]]
-        tz = 4
-        nseg = -(-nc[2] // tz)
-        cs = self._cell_start.cpu().numpy().astype(np.int64)
-        slice0 = self._slice0.cpu().numpy().astype(np.int64)
-        lst = self._tlist.cpu().numpy().view(np.uint16)
-        per = [bool(self._pbox.periodic[i]) for i in range(3)]
-        out = np.empty(rows.size, np.int64)
-        for t in range(nc[0] * nc[1] * nseg):
-            col, seg = divmod(t, nseg)
-            cx, cy = divmod(col, nc[1])
-            z0, z1 = seg * tz, min(seg * tz + tz, nc[2])
-            slots = []
-            for c in range(9):
-                xs, ys = cx + c // 3 - 1, cy + c % 3 - 1
-                for kk in range(z1 - z0 + 2):
-                    zs = z0 - 1 + kk
-                    v = [xs, ys, zs]
-                    ok = True
-                    for ax in range(3):
-                        if not 0 <= v[ax] < nc[ax]:
-                            if per[ax]:
-                                v[ax] %= nc[ax]
-                            else:
-                                ok = False
-                    if ok:
-                        cell = (v[0] * nc[1] + v[1]) * nc[2] + v[2]
-                        slots.extend(range(cs[cell], cs[cell + 1]))
-            slots = np.asarray(slots, np.int64)
-            h0 = cs[(cx * nc[1] + cy) * nc[2] + z0]
-            h1 = cs[(cx * nc[1] + cy) * nc[2] + z1]
-            sel = (rows >= h0) & (rows < h1)
-            u = rows[sel] - h0
-            kk = ks[sel]
-            w = ((slice0[t] + (u >> 5)) * Q + (kk >> 2)) * 128 + (u & 31) * 4 + (kk & 3)
-            out[sel] = slots[lst[w].astype(np.int64)]
-        return out
+    def _tile_rows(self, width: int = 128):
+        """Tile lists as (count, table): row = cell-sorted particle index,
+        table[row, :count[row]] its neighbours (pc_tile_decode)."""
+        n = self.n
+        cnt = torch.zeros(n, dtype=torch.int32, device=self.device)
+        table = torch.full((n, width), -1, dtype=torch.int32, device=self.device)
+        call("pc_tile_decode", self._ntiles, ptr(self._tplan), ptr(self._rowidx),
+             ptr(self._rounds), ptr(self._tlist), self._q8, width, ptr(cnt), ptr(table),
+             stream())
+        return cnt, table
+
+    def mean_neighbors(self) -> float:
+        """Mean Verlet-list length of the current build."""
+        if self.mode == "tile":
+            cnt, _ = self._tile_rows()
+            return float(cnt.double().mean().item())
+        return float(self.cnt[: self.n].double().mean().item())
 
     def negate_velocities(self):
         self.vel.neg_()
