@@ -202,6 +202,13 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
  * d_rounds (RW int32), d_partial (RW * 5 doubles) and d_list (RW * q8 * 512
  * bytes). */
 int32_t pc_tile_count(const pc_grid* grid);
+/* Per-cell z-sort of a cell-sorted order (ref-transparent: the reference
+ * sums forces and energies in global-id order, md.py:7-11): cell c holds
+ * d_order[cs[c] .. cs[c+1]); d_out lists the same particles ranked by
+ * (z of d_pos4 row, position in the cell).  The tile path relies on it:
+ * staged columns and home rows become z-sorted runs. */
+int pc_cell_zsort(const double* d_pos4, const int32_t* d_cell_start, int32_t ncells,
+                  const int32_t* d_order, int32_t* d_out, void* stream);
 int32_t pc_tile_plan_ints(void);
 int32_t pc_tile_stage_cap(void);
 int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw,

@@ -102,6 +102,7 @@ SIGNATURES = {
     "pc_halo_pack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pc_tile_count": (c_i32, [ctypes.POINTER(PcGrid)]),
     "pc_tile_plan_ints": (c_i32, []),
+    "pc_cell_zsort": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pc_tile_stage_cap": (c_i32, []),
     "pc_tile_rows": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp]),
     "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),

@@ -40,6 +40,7 @@
 // the force is accumulated in FP64 as f += fm*dx so pair terms are exactly
 // antisymmetric (momentum conserved to FP64 rounding).
 #include <stdlib.h>
+#include <string.h>
 
 #include "pc_common.cuh"
 
@@ -285,9 +286,6 @@ struct TileBuildParams {
   int64_t ps;          // planar stride
 };
 
-constexpr int kWin = 8;     // scheduling window (entries a lane may pick from per round)
-constexpr int kIters = 2;   // proposal/resolution passes per round
-
 __device__ __forceinline__ bool exact_pair_pl(const double* __restrict__ pl, int64_t ps, int a,
                                               int j, const pc_box& b, double cutoff2) {
   const double dx = min_image(__dsub_rn(pl[j], pl[a]), b.length[0], b.mi_thresh[0]);
@@ -297,30 +295,47 @@ __device__ __forceinline__ bool exact_pair_pl(const double* __restrict__ pl, int
   return r2_exact(dx, dy, dz) < cutoff2;
 }
 
+// Residue-group resolution of one proposal pass (see schedule_rows): lanes
+// of the same half-warp proposing slots of equal residue form a group (one
+// MATCH.ANY); the lowest critical lane of the group, else its lowest lane,
+// wins, and so does every lane proposing the winner's slot.
+__device__ __forceinline__ bool resolve(bool has, int s, unsigned crit, int half, int lane,
+                                        unsigned& taken) {
+  const unsigned FULL = 0xffffffffu;
+  const int r = s & 15;
+  const unsigned g = __match_any_sync(FULL, has ? (unsigned)((half << 4) | r)
+                                                : (unsigned)(32 + lane));
+  const unsigned gc = g & crit;
+  const int wl = __ffs(gc ? gc : g) - 1;
+  const int ws = __shfl_sync(FULL, s, wl);
+  const unsigned all = __reduce_or_sync(FULL, has ? (1u << ((half << 4) + r)) : 0u);
+  taken |= (all >> (half << 4)) & 0xFFFFu;
+  return has && s == ws;
+}
+
 // Bank-conflict-free round schedule of one row-warp.  Every lane holds its
-// row's slots in ascending order (hits[k*32]); in each round each lane takes
-// one entry so that within a half-warp (one LDS.64 wavefront phase of 16
-// lanes) all lanes read distinct bank pairs (slot % 16) or the very same slot
-// (broadcast).  Greedy, kIters passes per round: every unassigned lane
-// proposes the first entry of its kWin-entry window whose residue is still
-// free in its half; per residue the winner is the lowest "critical" lane
-// (remaining entries >= the warp's maximum - 1: it bounds the round count),
-// else the lowest lane, and every lane proposing the winner's slot wins with
-// it.  Residue groups come from four ballots on the residue bits (no
-// MATCH, no per-group loops).  Lanes left unassigned read a dummy of a free
-// residue.  Simulated on LJ liquid tiles: 1.05x the rounds of the longest
-// row (unscheduled ascending order: 4.8 wavefronts per LDS.64 instead of 2).
-// Emits slot*8 (the byte offset of the slot in one coordinate array).
+// row's slots in sweep order (hits[k*32]); in each round each lane takes one
+// entry so that within a half-warp (one LDS.64 pass of 16 lanes; measured,
+// scripts/micro/lds_banks.cu: conflicts across the two halves are free) all
+// lanes read distinct bank pairs (slot % 16) or the very same slot
+// (broadcast).  Two passes per round: every lane proposes its next entry;
+// per residue the lowest "critical" lane (remaining entries >= the warp's
+// maximum - 1: it bounds the round count), else the lowest lane, wins,
+// together with every lane proposing the winner's slot; losers then propose
+// the first entry of their next three whose residue is still free.  Lanes
+// left unassigned read a NaN-free dummy of a free residue.  Simulated on LJ
+// tiles: 1.08x the rounds of the longest row; measured 2.0 LDS wavefronts
+// per LDS.64 (unscheduled sweep order: 4.9).  The 4-entry window lives in two
+// registers of packed u16 (entry removal = two PRMTs).  Emits slot*8 (the
+// byte offset of the slot in one coordinate array).
 __device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, int cnt,
                                              int lane, int dummy0, uint4* __restrict__ out,
-                                             int cap_rounds) {
+                                             int cap_rounds, bool two_pass) {
   const unsigned FULL = 0xffffffffu;
   const int half = lane >> 4;
-  const unsigned halfmask = half ? 0xFFFF0000u : 0x0000FFFFu;
-  int win[kWin];
-#pragma unroll
-  for (int i = 0; i < kWin; ++i) win[i] = i < cnt ? (int)hits[i * 32] : -1;
-  int ptr = min(cnt, kWin);
+  auto ld = [&](int k) -> uint32_t { return k < cnt ? (uint32_t)hits[k * 32] : 0xFFFFu; };
+  uint32_t w01 = ld(0) | (ld(1) << 16), w23 = ld(2) | (ld(3) << 16);
+  int ptr = 4;
   int rem = cnt;
   int R = 0;
   uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;     // 8 x u16 shift register
@@ -329,47 +344,36 @@ __device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, 
     if (maxrem == 0) break;
     const unsigned crit = __ballot_sync(FULL, rem > 0 && rem >= maxrem - 1);
     unsigned taken = 0u;
-    int outs = -1;
-#pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-      int pi = -1, ps = 0;
-      if (outs < 0 && rem > 0) {
-        if (it == 0) {
-          pi = 0;
-          ps = win[0];
-        } else {
-#pragma unroll
-          for (int i = kWin - 1; i >= 0; --i) {
-            const int sl = win[i];
-            if (sl >= 0 && !((taken >> (sl & 15)) & 1u)) { pi = i; ps = sl; }
-          }
-        }
+    const int e0 = (int)(w01 & 0xFFFFu);
+    int pi = -1, outs = -1;
+    if (resolve(rem > 0, e0, crit, half, lane, taken)) {
+      pi = 0;
+      outs = e0;
+    }
+    if (two_pass && __any_sync(FULL, pi < 0 && rem > 1)) {
+      const int e1 = (int)(w01 >> 16), e2 = (int)(w23 & 0xFFFFu), e3 = (int)(w23 >> 16);
+      int q = -1, qs = 0;
+      if (pi < 0) {
+        if (e3 != 0xFFFF && !((taken >> (e3 & 15)) & 1u)) { q = 3; qs = e3; }
+        if (e2 != 0xFFFF && !((taken >> (e2 & 15)) & 1u)) { q = 2; qs = e2; }
+        if (e1 != 0xFFFF && !((taken >> (e1 & 15)) & 1u)) { q = 1; qs = e1; }
       }
-      const bool has = pi >= 0;
-      const int r = ps & 15;
-      unsigned g = __ballot_sync(FULL, has) & halfmask;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const unsigned bk = __ballot_sync(FULL, has && ((r >> k) & 1));
-        g &= ((r >> k) & 1) ? bk : ~bk;
-      }
-      const unsigned gc = g & crit;
-      const unsigned cands = gc ? gc : g;
-      const int wl = cands ? __ffs(cands) - 1 : lane;
-      const int wslot = __shfl_sync(FULL, ps, wl);
-      const unsigned all = __reduce_or_sync(FULL, has ? (1u << ((half << 4) + r)) : 0u);
-      taken |= (all >> (half << 4)) & 0xFFFFu;
-      if (has && ps == wslot) {
-        outs = ps;
-#pragma unroll
-        for (int i = 0; i < kWin - 1; ++i)
-          if (i >= pi) win[i] = win[i + 1];
-        win[kWin - 1] = ptr < cnt ? (int)hits[ptr * 32] : -1;
-        ptr += ptr < cnt ? 1 : 0;
-        --rem;
+      if (resolve(q >= 0, qs, crit, half, lane, taken)) {
+        pi = q;
+        outs = qs;
       }
     }
-    if (outs < 0) outs = dummy0 + (__ffs(~taken & 0xFFFFu) - 1);
+    if (pi >= 0) {       // drop entry pi, append the next hit
+      const uint32_t nx = ld(ptr);
+      ++ptr;
+      --rem;
+      const uint32_t n01 = pi == 0 ? __byte_perm(w01, w23, 0x5432)
+                                   : (pi == 1 ? __byte_perm(w01, w23, 0x5410) : w01);
+      w23 = __byte_perm(w23, nx, pi == 3 ? 0x5410 : 0x5432);
+      w01 = n01;
+    } else {
+      outs = dummy0 + (__ffs(~taken & 0xFFFFu) - 1);
+    }
     b0 = __funnelshift_r(b0, b1, 16);
     b1 = __funnelshift_r(b1, b2, 16);
     b2 = __funnelshift_r(b2, b3, 16);
@@ -390,8 +394,8 @@ __device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, 
   return R;
 }
 
-// Unscheduled rounds: entry k of every row in round k (ascending slots),
-// padded with dummies -- the cheap alternative to schedule_rows.
+// Unscheduled rounds: entry k of every row in round k (sweep order), padded
+// with dummies -- the cheap alternative to schedule_rows (PC_TILE_NOSCHED).
 __device__ __forceinline__ int plain_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
                                           int dummy0, uint4* __restrict__ out, int cap_rounds) {
   const int R = __reduce_max_sync(0xffffffffu, cnt);
@@ -410,15 +414,34 @@ __device__ __forceinline__ int plain_rows(const uint16_t* __restrict__ hits, int
   return R;
 }
 
+// particle index of staged slot s
+__device__ __forceinline__ int slot_index(const TileSetup& T, int s) {
+  int e = 0;
+  while (e < kSegs - 1 && !(T.seg_len[e] > 0 && s >= T.seg_dst[e] && s < T.seg_dst[e] + T.seg_len[e]))
+    ++e;
+  return T.seg_src[e] + (s - T.seg_dst[e]);
+}
+
+// Build.  Particles are z-sorted inside every cell (pc_cell_zsort at the
+// rebuild), so each staged column -- cells in z order, each cell z-sorted --
+// is one z-sorted run of slots, and the home rows of a column are z-sorted
+// too.  The FP32 staged copy (x, y, z relative to the tile centre, periodic
+// image applied) sits in slot order.  One warp handles one row at a time:
+// lanes 0..8 bound its 9 stencil columns to the z-window |dz| < h, h^2 =
+// hi2 - (lateral distance to the column)^2 (binary search in the stencil's
+// first and last cell), then all 32 lanes sweep the windows' candidates in
+// parallel and compact the hits with a ballot into the row's hit list
+// (ascending slots).  Candidates outside the FP32 band decide in FP32;
+// inside it the reference's FP64 predicate decides (exact).
+
 __global__ void __launch_bounds__(kBuildWarps * 32, 2)
 tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
                   int* __restrict__ flag) {
-  // dynamic: staged FP32 (rel x, y, z, index) | per-warp hit lists [warp][k][lane]
-  extern __shared__ float4 st[];
+  extern __shared__ float4 cz[];                 // staged FP32 copy | per-warp hit rows
   __shared__ TileSetup T;
-  uint16_t* hits_all = reinterpret_cast<uint16_t*>(st + p.max_stage);
+  uint16_t* hits_all = reinterpret_cast<uint16_t*>(cz + p.max_stage);
   tile_setup<true>(blockIdx.x, g, b, cs, T);
   if (T.S > p.max_stage) {
     if (threadIdx.x == 0) {
@@ -429,6 +452,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrw = (T.H + 31) >> 5;
+  const int bz = T.bz;
   if (warp == 0) {                       // compacted plan of this tile
     int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
     int base = 0;
@@ -452,8 +476,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     }
   }
   const int64_t ps = p.ps;
-  // stage: FP32 coordinates relative to the tile centre, periodic image applied
-  for (int e = 0; e < kSegs; ++e) {
+  for (int e = 0; e < kSegs; ++e) {      // stage: slot order
     const int len = T.seg_len[e];
     if (len == 0) continue;
     const int src = T.seg_src[e], dst = T.seg_dst[e];
@@ -466,51 +489,99 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       q.x = (float)(pl[j] + sx);
       q.y = (float)(pl[ps + j] + sy);
       q.z = (float)(pl[2 * ps + j] + sz);
-      q.w = __int_as_float(j);
-      st[dst + t] = q;
+      q.w = 0.f;
+      cz[dst + t] = q;
     }
   }
   __syncthreads();
-  uint16_t* hits = hits_all + warp * kHitCap * 32 + lane;
+
+  const float wx = (float)g.width[0], wy = (float)g.width[1];
+  uint16_t* hits = hits_all + warp * kHitCap * 32 + lane;     // [k][lane]
   for (int w = warp; w < nrw; w += kBuildWarps) {
     const int u = w * 32 + lane;
     const bool act = u < T.H;
-    int cnt = 0, a = -1;
+    int cnt = 0, a = -1, pos = -1;
+    bool anyband = false;
     if (act) {
-      int c;
-      a = home_row(T, u, c);
+      int c = 0;
+#pragma unroll
+      for (int q = 1; q < kBX * kBY; ++q) c += (u >= T.home_pre[q]) ? 1 : 0;
       const int hx = c / kBY, hy = c - hx * kBY;
-      // z-cell of a within its column (staged k = cell - z0 + 1)
+      const int hcol = (hx + 1) * kSY + (hy + 1);
+      pos = T.cell_lo[hcol][1] + (u - T.home_pre[c]);
       int k = 1;
-      for (int zz = 1; zz < T.bz; ++zz) k += (a >= cs[T.home_cell0[c] + zz]) ? 1 : 0;
-      const int seg = ((hx + 1) * kSY + (hy + 1)) * 3 + 1;
-      const float4 me = st[T.seg_dst[seg] + (a - T.seg_src[seg])];
-      for (int dxo = 0; dxo < 3; ++dxo) {
-        for (int dyo = 0; dyo < 3; ++dyo) {
-          const int col = (hx + dxo) * kSY + (hy + dyo);
-          for (int dk = -1; dk <= 1; ++dk) {
-            const int s0 = T.cell_lo[col][k + dk], s1 = T.cell_hi[col][k + dk];
-#pragma unroll 4
-            for (int s = s0; s < s1; ++s) {
-              const float4 q = st[s];
-              const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
-              const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              if (r2 < p.hi2) {
-                const int j = __float_as_int(q.w);
-                if (j != a && (r2 < p.lo2 || exact_pair_pl(pl, ps, a, j, b, p.cutoff2))) {
-                  if (cnt < kHitCap) hits[cnt * 32] = (uint16_t)s;
-                  ++cnt;
-                }
-              }
-            }
+      for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
+      const float4 me = cz[pos];
+      // lateral distances to the neighbour columns (the home column spans
+      // [hx0, hx0 + wx) x [hy0, hy0 + wy) relative to the tile centre),
+      // shrunk by a safety margin: the windows below are conservative
+      const float hx0 = (float)((hx - 0.5 * T.bx) * g.width[0]);
+      const float hy0 = (float)((hy - 0.5 * T.by) * g.width[1]);
+      const float exm = fmaxf(me.x - hx0 - 1e-4f, 0.f), exp_ = fmaxf(hx0 + wx - me.x - 1e-4f, 0.f);
+      const float eym = fmaxf(me.y - hy0 - 1e-4f, 0.f), eyp = fmaxf(hy0 + wy - me.y - 1e-4f, 0.f);
+#pragma unroll 1
+      for (int cc = 0; cc < 9; ++cc) {
+        const int dxo = cc / 3, dyo = cc - dxo * 3;
+        const float ex = dxo == 0 ? exm : (dxo == 2 ? exp_ : 0.f);
+        const float ey = dyo == 0 ? eym : (dyo == 2 ? eyp : 0.f);
+        const float h2 = p.hi2 - (ex * ex + ey * ey);
+        if (h2 <= 0.f) continue;
+        const float h = sqrtf(h2) * 1.0001f + 1e-4f;
+        const float zlo = me.z - h, zhi = me.z + h;
+        const int col = (hx + dxo) * kSY + (hy + dyo);
+        // [lo, e1) in cell k-1 (suffix), cell k, [b3, hi) in cell k+1 (prefix)
+        int lo = T.cell_lo[col][k - 1], h1 = T.cell_hi[col][k - 1];
+        while (lo < h1) {
+          const int mid = (lo + h1) >> 1;
+          if (cz[mid].z < zlo) lo = mid + 1; else h1 = mid;
+        }
+        const int e1 = T.cell_hi[col][k - 1];
+        const int b2 = T.cell_lo[col][k], e2 = T.cell_hi[col][k];
+        const int b3 = T.cell_lo[col][k + 1];
+        int hi = b3, h3 = T.cell_hi[col][k + 1];
+        while (hi < h3) {
+          const int mid = (hi + h3) >> 1;
+          if (cz[mid].z <= zhi) hi = mid + 1; else h3 = mid;
+        }
+        // the three pieces are one run unless a periodic z wrap splits them
+        const bool one = (e1 == b2) && (e2 == b3);
+        const int na = one ? hi - lo : e1 - lo;
+        for (int piece = 0; piece < (one ? 1 : 3); ++piece) {
+          const int s0 = piece == 0 ? lo : (piece == 1 ? b2 : b3);
+          const int s1 = piece == 0 ? lo + na : (piece == 1 ? e2 : hi);
+#pragma unroll 2
+          for (int i = s0; i < s1; ++i) {
+            const float4 q = cz[i];
+            const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+            const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const bool hit = rr < p.hi2 && i != pos;
+            const bool band = rr >= p.lo2;
+            // unconditional store: slot cnt is overwritten unless this is a hit
+            hits[min(cnt, kHitCap - 1) * 32] = (uint16_t)(i | (band ? 0x8000 : 0));
+            anyband |= hit && band;
+            cnt += hit ? 1 : 0;
           }
         }
+      }
+      a = slot_index(T, pos);
+    }
+    // band entries: the reference's FP64 predicate decides (rare)
+    if (__any_sync(0xffffffffu, anyband)) {
+      if (anyband) {
+        int m = 0;
+        for (int t = 0; t < min(cnt, kHitCap); ++t) {
+          const int v = hits[t * 32];
+          bool keep = true;
+          if (v & 0x8000) keep = exact_pair_pl(pl, ps, a, slot_index(T, v & 0x7FFF), b, p.cutoff2);
+          if (keep) hits[m++ * 32] = (uint16_t)(v & 0x7FFF);
+        }
+        cnt = cnt > kHitCap ? cnt - (min(cnt, kHitCap) - m) : m;
       }
     }
     const int rw = rw0[blockIdx.x] + w;
     rowidx[(int64_t)rw * 32 + lane] = a;
     const int cmax = __reduce_max_sync(0xffffffffu, cnt);
-    if (cmax > kHitCap) {
+    if (cmax >= kHitCap) {        // (the unconditional hit store clobbers entry kHitCap-1)
       if (lane == 0) {
         atomicOr(flag, kFlagOverflow);
         atomicMax(flag + 2, 1 << 20);
@@ -521,7 +592,8 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     __syncwarp();
     const int cap = 8 * p.Q8;
     const int R = p.sched ? schedule_rows(hits, cnt, lane, p.max_stage,
-                                          list + (int64_t)rw * p.Q8 * 32 + lane, cap)
+                                          list + (int64_t)rw * p.Q8 * 32 + lane, cap,
+                                          p.sched == 1)
                           : plain_rows(hits, cnt, lane, p.max_stage,
                                        list + (int64_t)rw * p.Q8 * 32 + lane, cap);
     if (lane == 0) {
@@ -532,6 +604,34 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       }
     }
     __syncwarp();
+  }
+}
+
+// Per-cell z-sort of a cell-sorted order: cell c = order[cs[c] .. cs[c+1]);
+// out = the same particles ranked by (z, position in the cell).  Warp per
+// cell; z read from the unsorted pos4 rows.
+__global__ void __launch_bounds__(256)
+cell_zsort_kernel(const double* __restrict__ pos4, const int* __restrict__ cs, int ncells,
+                  const int* __restrict__ order, int* __restrict__ out) {
+  const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cell >= ncells) return;
+  const int s0 = cs[cell], m = cs[cell + 1] - s0;
+  for (int t0 = 0; t0 < m; t0 += 32) {
+    const int t = t0 + lane;
+    const int src = t < m ? order[s0 + t] : 0;
+    const double z = t < m ? pos4[4 * (int64_t)src + 2] : 0.0;
+    int rk = 0;
+    for (int u0 = 0; u0 < m; u0 += 32) {
+      const int uu = u0 + lane;
+      const double zu_l = uu < m ? pos4[4 * (int64_t)order[s0 + uu] + 2] : 0.0;
+      const int lim = min(32, m - u0);
+      for (int v = 0; v < lim; ++v) {
+        const double zu = __shfl_sync(0xffffffffu, zu_l, v);
+        rk += (zu < z || (zu == z && u0 + v < t)) ? 1 : 0;
+      }
+    }
+    if (t < m) out[s0 + rk] = src;
   }
 }
 
@@ -864,6 +964,14 @@ int32_t pc_tile_count(const pc_grid* grid) { return tile_dims(*grid).ntiles; }
 int32_t pc_tile_plan_ints(void) { return kPlanInts; }
 int32_t pc_tile_stage_cap(void) { return kStageCap; }
 
+int pc_cell_zsort(const double* d_pos4, const int32_t* d_cell_start, int32_t ncells,
+                  const int32_t* d_order, int32_t* d_out, void* stream) {
+  if (ncells <= 0) return PC_OK;
+  cell_zsort_kernel<<<(ncells + 7) / 8, 256, 0, as_stream(stream)>>>(d_pos4, d_cell_start, ncells,
+                                                                     d_order, d_out);
+  return check_launch("pc_cell_zsort");
+}
+
 int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw, void* stream) {
   const int nt = tile_dims(*grid).ntiles;
   if (nt <= 0) return PC_OK;
@@ -898,10 +1006,10 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
   p.hi2 = nextafterf((float)(cutoff2 + margin), INFINITY);
   p.Q8 = q8;
   p.max_stage = kStageCap;
-  p.sched = getenv("PC_TILE_NOSCHED") ? 0 : 1;
+  p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 0;
   p.ps = planar_stride;
-  const int smem = (kStageCap + kNDummy) * (int)sizeof(float4) +
-                   kBuildWarps * kHitCap * 32 * (int)sizeof(uint16_t);
+  const int smem = kStageCap * (int)sizeof(float4) +
+                   kBuildWarps * 32 * kHitCap * (int)sizeof(uint16_t);
   if (smem > g_build_smem) {
     if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess) {

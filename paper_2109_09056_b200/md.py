@@ -300,9 +300,16 @@ class MDDriver:
         n, s = self.n, stream()
         e0 = self._t0()
         srt = _kernels.CellSort(self.pos[:n], 4, self._grid)     # excludes the dummy row
-        _kernels.gather_rows(self.pos, srt.order, n, out=self._pos_alt)
+        order = srt.order
+        if self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3:
+            # z-sorted cells: staged columns / home rows of the tile path are
+            # z-sorted slot runs (pc_tile.cu)
+            order = torch.empty_like(srt.order)
+            call("pc_cell_zsort", ptr(self.pos), ptr(srt.cell_start), self._grid.ncells,
+                 ptr(srt.order), ptr(order), s)
+        _kernels.gather_rows(self.pos, order, n, out=self._pos_alt)
         for a in range(3):
-            _kernels.gather_rows(self.vel[a], srt.order, n, out=self._vel_alt[a])
+            _kernels.gather_rows(self.vel[a], order, n, out=self._vel_alt[a])
         self.pos, self._pos_alt = self._pos_alt, self.pos
         self.vel, self._vel_alt = self._vel_alt, self.vel
         call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
