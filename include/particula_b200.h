@@ -228,12 +228,20 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
  * periodic face), FP32 LJ magnitude, FP64 accumulation; writes f (planar,
  * f_stride), applies the final half kick v += dtm*f when d_v != NULL and
  * writes per-row-warp (KE, PE, px, py, pz) partials.  Overlap
- * (r^2 < overlap2) sets d_flag bit 2. */
+ * (r^2 < overlap2) sets d_flag bit 2.  With d_planar_next != NULL the next
+ * step's integrate block (v' = v + dtm_next f, x' = wrap(x + dt v'), ref
+ * md.py:219-231) is fused into the epilogue and written to d_planar_next /
+ * d_v_next (same strides); d_planar and d_v keep this step's state. */
 int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
                   const int32_t* d_plan, const int32_t* d_rowidx, const int32_t* d_rounds,
                   const void* d_list, int32_t q8, const pc_box* box, const pc_lj* lj,
                   double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
-                  double dtm, double mass, double* d_partial, int32_t* d_flag, void* stream);
+                  double dtm, double mass, double* d_partial, int32_t* d_flag,
+                  double* d_planar_next, double* d_v_next, double dtm_next, double dt,
+                  void* stream);
+/* pos4 x, y, z <- planar rows [0, n) (tags untouched). */
+int pc_pos_from_planar(const double* d_planar, int64_t planar_stride, int32_t n, double* d_pos4,
+                       void* stream);
 /* Tile lists -> per-row particle indices: d_count[row], d_table[row*width+k]
  * (rows = cell-sorted particle indices; inspection / parity tests). */
 int pc_tile_decode(int32_t ntiles, const int32_t* d_plan, const int32_t* d_rowidx,

@@ -110,7 +110,9 @@ SIGNATURES = {
                                      c_vp, c_vp, c_vp, c_vp]),
     "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl, c_vp,
-                                     c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
+                                     c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp,
+                                     c_dbl, c_dbl, c_vp]),
+    "pc_pos_from_planar": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_tile_decode": (ctypes.c_int, [c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                       c_vp]),
     "pc_halo_unpack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),

@@ -60,6 +60,24 @@ __device__ __forceinline__ double min_image_wrapped(double d, double L, double T
   return a >= T ? t : d;
 }
 
+// ---- periodic wrap of ref geometry.py:40-49 (numpy rounding) --------------
+// numpy float mod (npy_divmod): fmod, then shift a nonzero remainder whose
+// sign differs from the divisor's; zero takes the divisor's sign.
+__device__ __forceinline__ double np_mod(double a, double L) {
+  double m = fmod(a, L);
+  if (m != 0.0) {
+    if ((L < 0.0) != (m < 0.0)) m = __dadd_rn(m, L);
+  } else {
+    m = copysign(0.0, L);
+  }
+  return m;
+}
+
+__device__ __forceinline__ double wrap_axis(double x, double low, double high, double L) {
+  double w = __dadd_rn(low, np_mod(__dsub_rn(x, low), L));
+  return w >= high ? low : w;
+}
+
 // numpy einsum order on this build: (x*x + z*z) + y*y, no FMA.
 __device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));

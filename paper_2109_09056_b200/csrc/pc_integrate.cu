@@ -6,23 +6,6 @@ namespace pc {
 
 constexpr int kIntThreads = 256;
 
-// numpy float mod (npy_divmod): fmod, then shift a nonzero remainder whose
-// sign differs from the divisor's; zero takes the divisor's sign.
-__device__ __forceinline__ double np_mod(double a, double L) {
-  double m = fmod(a, L);
-  if (m != 0.0) {
-    if ((L < 0.0) != (m < 0.0)) m = __dadd_rn(m, L);
-  } else {
-    m = copysign(0.0, L);
-  }
-  return m;
-}
-
-__device__ __forceinline__ double wrap_axis(double x, double low, double high, double L) {
-  double w = __dadd_rn(low, np_mod(__dsub_rn(x, low), L));
-  return w >= high ? low : w;
-}
-
 __global__ void __launch_bounds__(kIntThreads)
 kick_drift_wrap_kernel(double* __restrict__ pos, double* __restrict__ v, int64_t vs,
                        const double* __restrict__ f, int64_t fs, int n, double dtm, double dt,

@@ -607,6 +607,15 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
 }
 
+__global__ void pos_from_planar_kernel(const double* __restrict__ pl, int64_t ps, int n,
+                                       double* __restrict__ pos4) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  pos4[4 * (int64_t)i] = pl[i];
+  pos4[4 * (int64_t)i + 1] = pl[ps + i];
+  pos4[4 * (int64_t)i + 2] = pl[2 * ps + i];
+}
+
 // Per-cell z-sort of a cell-sorted order: cell c = order[cs[c] .. cs[c+1]);
 // out = the same particles ranked by (z, position in the cell).  Warp per
 // cell; z read from the unsorted pos4 rows.
@@ -772,7 +781,8 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
                   const int* __restrict__ rounds, const uint4* __restrict__ list, pc_box b,
                   double* __restrict__ f3, int64_t fs, double* __restrict__ v, int64_t vs,
                   double dtm, double mass, double* __restrict__ partial, int* __restrict__ flag,
-                  int nbuf) {
+                  int nbuf, double* __restrict__ x_next, double* __restrict__ v_next,
+                  double dtm_next, double dt) {
   extern __shared__ double dyn[];
   double* stage = dyn;                                             // nbuf x (x|y|z)
   int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
@@ -902,6 +912,27 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
         px = mass * vx;
         py = mass * vy;
         pz = mass * vz;
+        if (x_next) {
+          // next step's integrate block (ref md.py:219-231) fused: it uses
+          // this force, so v' = v + dtm f, x' = wrap(x + dt v') are final
+          // now; written to the alternate buffers (neighbour tiles still
+          // stage x of this step)
+          const double ux = __dadd_rn(vx, __dmul_rn(dtm_next, fx));
+          const double uy = __dadd_rn(vy, __dmul_rn(dtm_next, fy));
+          const double uz = __dadd_rn(vz, __dmul_rn(dtm_next, fz));
+          double nx_ = __dadd_rn(xi, __dmul_rn(dt, ux));
+          double ny_ = __dadd_rn(yi, __dmul_rn(dt, uy));
+          double nz_ = __dadd_rn(zi, __dmul_rn(dt, uz));
+          if (b.periodic[0]) nx_ = wrap_axis(nx_, b.low[0], b.high[0], b.length[0]);
+          if (b.periodic[1]) ny_ = wrap_axis(ny_, b.low[1], b.high[1], b.length[1]);
+          if (b.periodic[2]) nz_ = wrap_axis(nz_, b.low[2], b.high[2], b.length[2]);
+          v_next[a] = ux;
+          v_next[vs + a] = uy;
+          v_next[2 * vs + a] = uz;
+          x_next[a] = nx_;
+          x_next[p.ps + a] = ny_;
+          x_next[2 * p.ps + a] = nz_;
+        }
       }
     }
     if (partial) {
@@ -963,6 +994,14 @@ extern "C" {
 int32_t pc_tile_count(const pc_grid* grid) { return tile_dims(*grid).ntiles; }
 int32_t pc_tile_plan_ints(void) { return kPlanInts; }
 int32_t pc_tile_stage_cap(void) { return kStageCap; }
+
+int pc_pos_from_planar(const double* d_planar, int64_t planar_stride, int32_t n, double* d_pos4,
+                       void* stream) {
+  if (n <= 0) return PC_OK;
+  pos_from_planar_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(d_planar, planar_stride,
+                                                                         n, d_pos4);
+  return check_launch("pc_pos_from_planar");
+}
 
 int pc_cell_zsort(const double* d_pos4, const int32_t* d_cell_start, int32_t ncells,
                   const int32_t* d_order, int32_t* d_out, void* stream) {
@@ -1029,7 +1068,13 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
                   const int32_t* d_plan, const int32_t* d_rowidx, const int32_t* d_rounds,
                   const void* d_list, int32_t q8, const pc_box* box, const pc_lj* lj,
                   double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
-                  double dtm, double mass, double* d_partial, int32_t* d_flag, void* stream) {
+                  double dtm, double mass, double* d_partial, int32_t* d_flag,
+                  double* d_planar_next, double* d_v_next, double dtm_next, double dt,
+                  void* stream) {
+  if (d_planar_next && !d_v) {
+    set_error("pc_tile_force: the fused integrate needs the velocities");
+    return PC_ERR_VALUE;
+  }
   if (q8 <= 0 || planar_stride % 16) {
     set_error("pc_tile_force: bad list capacity or planar stride");
     return PC_ERR_VALUE;
@@ -1086,11 +1131,13 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
   if (unit)
     tile_force_kernel<true><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
-        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf);
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
+        d_v_next, dtm_next, dt);
   else
     tile_force_kernel<false><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
-        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf);
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
+        d_v_next, dtm_next, dt);
   return check_launch("pc_tile_force");
 }
 

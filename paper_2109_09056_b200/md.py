@@ -264,6 +264,13 @@ class MDDriver:
         self._ps = -(-(self.cap + 1) // 16) * 16
         self.pl = torch.empty((3, self._ps), dtype=torch.float64, device=dev)
         self.pl[:, self.cap:] = float("nan")
+        # tile path: the force epilogue also performs the next step's
+        # integrate block into these (pc_tile_force, fused); `_advanced`
+        # marks them valid, `_pos_stale` that pos4 xyz lags behind pl
+        self._pl_n = self.pl.clone()
+        self._vel_n = None
+        self._advanced = False
+        self._pos_stale = False
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)        # force errors
         self.build_flag = torch.zeros(3, dtype=torch.int32, device=dev)  # flags, need, rounds
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))   # per-warp rows
@@ -295,10 +302,17 @@ class MDDriver:
         slices = -(-self.cap // 32)
         return torch.empty(slices * self.ell_width * 32, dtype=torch.int32, device=self.device)
 
+    def _sync_pos4(self):
+        """pos4 x, y, z <- pl (the fused tile integrate only writes pl)."""
+        if self._pos_stale:
+            call("pc_pos_from_planar", ptr(self.pl), self._ps, self.n, ptr(self.pos), stream())
+            self._pos_stale = False
+
     def _rebuild(self):
         """Cell sort of all particle fields + SELL Verlet build (md.py:169-188)."""
         n, s = self.n, stream()
         e0 = self._t0()
+        self._sync_pos4()
         srt = _kernels.CellSort(self.pos[:n], 4, self._grid)     # excludes the dummy row
         order = srt.order
         if self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3:
@@ -400,11 +414,14 @@ class MDDriver:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
         if self.mode == "tile":
+            if self._vel_n is None:
+                self._vel_n = torch.empty_like(self.vel)
             call("pc_tile_force", ptr(self.pl), self._ps, self._ntiles, ptr(self._tplan),
                  ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._pbox,
                  self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
                  float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
-                 stream())
+                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), stream())
+            self._advanced = True
         elif self.mode == "half":
             self.frc.zero_()
             call("pc_lj_force_sell_half", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
@@ -432,7 +449,14 @@ class MDDriver:
         self._ke_fresh = True
 
     def _integrate(self):
+        if self._advanced:          # done by the previous force epilogue
+            self.pl, self._pl_n = self._pl_n, self.pl
+            self.vel, self._vel_n = self._vel_n, self.vel
+            self._advanced = False
+            self._pos_stale = True
+            return
         e0 = self._t0()
+        self._sync_pos4()
         call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
              self.cap, self.n, self._dtm, float(self.cfg.dt), self._pbox, ptr(self.pl),
              self._ps, stream())
@@ -477,6 +501,7 @@ class MDDriver:
 
     def gather_state(self):
         """Positions and velocities in global-id order (ref md.py:279-287)."""
+        self._sync_pos4()
         p = self.pos[: self.n].cpu().numpy()
         ids = p[:, 3].view(np.int64)
         x = np.zeros((self.n, 3))
@@ -530,6 +555,7 @@ class MDDriver:
 
     def negate_velocities(self):
         self.vel.neg_()
+        self._advanced = False      # the pre-integrated next state is stale
         self._ke_fresh = False
 
     @property

@@ -360,10 +360,7 @@ def test_md_verlet_list_bit_exact(pc, oracle, cells, temp):
         if stage:
             for s in range(1, 21):
                 drv.step(s)
-        p = drv.pos[: drv.n].cpu().numpy()
-        ids = p[:, 3].copy().view(np.int64)
-        x = np.empty((drv.n, 3))
-        x[ids] = p[:, :3]
+        x, _ = drv.gather_state()
         counts, offsets, idx = drv.verlet_sets()
         ref = oracle.build_verlet(x, drv.box.low, drv.box.high, [True] * 3, drv.search)
         assert np.array_equal(counts, ref["counts"])
@@ -383,10 +380,7 @@ def test_md_sell_path_verlet_bit_exact(pc, oracle, cells, temp):
     drv = pc.md.MDDriver(cfg, tile=False)
     for s in range(1, 21):
         drv.step(s)
-    p = drv.pos[: drv.n].cpu().numpy()
-    ids = p[:, 3].copy().view(np.int64)
-    x = np.empty((drv.n, 3))
-    x[ids] = p[:, :3]
+    x, _ = drv.gather_state()
     counts, offsets, idx = drv.verlet_sets()
     ref = oracle.build_verlet(x, drv.box.low, drv.box.high, [True] * 3, drv.search)
     assert np.array_equal(counts, ref["counts"]) and np.array_equal(idx, ref["indices"])
@@ -458,10 +452,8 @@ def test_md_engine_forces_vs_oracle(pc, oracle, cells, temp, steps):
     assert drv.mode == "tile"
     for s in range(1, steps + 1):
         drv.step(s)
-    p = drv.pos[: drv.n].cpu().numpy()
-    ids = p[:, 3].copy().view(np.int64)
-    x = np.empty((drv.n, 3))
-    x[ids] = p[:, :3]
+    x, _ = drv.gather_state()
+    ids = drv.pos[: drv.n, 3].contiguous().view(__import__("torch").int64).cpu().numpy()
     f = np.empty((drv.n, 3))
     f[ids] = drv.frc[:, : drv.n].cpu().numpy().T
     pi, pj = oracle.neighbor_pairs(x, drv.box.low, drv.box.high, [True] * 3, 2.5 * 1.0000001)
