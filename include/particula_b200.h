@@ -216,7 +216,7 @@ int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw
 /* Verlet build at cutoff2 (the reference's FP64 predicate behind an FP32
  * band prefilter) + round scheduling.  d_flag (3 int32, zeroed by the
  * caller): [0] bit 1 = a row-warp needs more than 8*q8 rounds ([2] = the
- * largest; >= 2^20: a row exceeds 128 entries), bit 4 = a neighbourhood
+ * largest; >= 2^20: a row exceeds 112 entries), bit 4 = a neighbourhood
  * exceeds pc_tile_stage_cap() slots ([1] = the largest).  The caller grows
  * q8 and rebuilds, or falls back to pc_nbr_build_sell. */
 int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,

@@ -52,8 +52,8 @@ constexpr int kSCols = kSX * kSY;
 constexpr int kSegs = kSCols * 3;
 constexpr int kNDummy = 16;
 constexpr int kForceWarps = 24;
-constexpr int kBuildWarps = 8;
-constexpr int kHitCap = 128;
+constexpr int kBuildWarps = 10;
+constexpr int kHitCap = 112;
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
 // memory: compile-time so every LDS is [slot*8 + immediate]
 constexpr int kStageCap = 2304;
@@ -495,13 +495,11 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
   __syncthreads();
 
-  const float wx = (float)g.width[0], wy = (float)g.width[1];
   uint16_t* hits = hits_all + warp * kHitCap * 32 + lane;     // [k][lane]
   for (int w = warp; w < nrw; w += kBuildWarps) {
     const int u = w * 32 + lane;
     const bool act = u < T.H;
-    int cnt = 0, a = -1, pos = -1;
-    bool anyband = false;
+    int cnt = 0, a = -1, pos = -1, nband = 0;
     if (act) {
       int c = 0;
 #pragma unroll
@@ -512,23 +510,14 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       int k = 1;
       for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
       const float4 me = cz[pos];
-      // lateral distances to the neighbour columns (the home column spans
-      // [hx0, hx0 + wx) x [hy0, hy0 + wy) relative to the tile centre),
-      // shrunk by a safety margin: the windows below are conservative
-      const float hx0 = (float)((hx - 0.5 * T.bx) * g.width[0]);
-      const float hy0 = (float)((hy - 0.5 * T.by) * g.width[1]);
-      const float exm = fmaxf(me.x - hx0 - 1e-4f, 0.f), exp_ = fmaxf(hx0 + wx - me.x - 1e-4f, 0.f);
-      const float eym = fmaxf(me.y - hy0 - 1e-4f, 0.f), eyp = fmaxf(hy0 + wy - me.y - 1e-4f, 0.f);
+      // every stencil column is swept over the same z-window |dz| < h,
+      // h = sqrt(hi2) (lateral pruning would only shorten some lanes'
+      // windows; the warp runs the longest anyway)
+      const float h = sqrtf(p.hi2) * 1.0001f + 1e-4f;
+      const float zlo = me.z - h, zhi = me.z + h;
 #pragma unroll 1
       for (int cc = 0; cc < 9; ++cc) {
-        const int dxo = cc / 3, dyo = cc - dxo * 3;
-        const float ex = dxo == 0 ? exm : (dxo == 2 ? exp_ : 0.f);
-        const float ey = dyo == 0 ? eym : (dyo == 2 ? eyp : 0.f);
-        const float h2 = p.hi2 - (ex * ex + ey * ey);
-        if (h2 <= 0.f) continue;
-        const float h = sqrtf(h2) * 1.0001f + 1e-4f;
-        const float zlo = me.z - h, zhi = me.z + h;
-        const int col = (hx + dxo) * kSY + (hy + dyo);
+        const int col = (hx + cc / 3) * kSY + (hy + cc % 3);
         // [lo, e1) in cell k-1 (suffix), cell k, [b3, hi) in cell k+1 (prefix)
         int lo = T.cell_lo[col][k - 1], h1 = T.cell_hi[col][k - 1];
         while (lo < h1) {
@@ -545,37 +534,39 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
         }
         // the three pieces are one run unless a periodic z wrap splits them
         const bool one = (e1 == b2) && (e2 == b3);
-        const int na = one ? hi - lo : e1 - lo;
         for (int piece = 0; piece < (one ? 1 : 3); ++piece) {
           const int s0 = piece == 0 ? lo : (piece == 1 ? b2 : b3);
-          const int s1 = piece == 0 ? lo + na : (piece == 1 ? e2 : hi);
-#pragma unroll 2
+          const int s1 = one ? hi : (piece == 0 ? e1 : (piece == 1 ? e2 : hi));
+#pragma unroll 4
           for (int i = s0; i < s1; ++i) {
             const float4 q = cz[i];
             const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
             const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const bool hit = rr < p.hi2 && i != pos;
-            const bool band = rr >= p.lo2;
             // unconditional store: slot cnt is overwritten unless this is a hit
-            hits[min(cnt, kHitCap - 1) * 32] = (uint16_t)(i | (band ? 0x8000 : 0));
-            anyband |= hit && band;
+            hits[min(cnt, kHitCap - 1) * 32] = (uint16_t)i;
+            const bool hit = rr < p.hi2 && i != pos;
+            nband += (hit && rr >= p.lo2) ? 1 : 0;
             cnt += hit ? 1 : 0;
           }
         }
       }
       a = slot_index(T, pos);
     }
-    // band entries: the reference's FP64 predicate decides (rare)
-    if (__any_sync(0xffffffffu, anyband)) {
-      if (anyband) {
+    // hits inside the FP32 band: the reference's FP64 predicate decides (rare)
+    if (__any_sync(0xffffffffu, nband > 0)) {
+      if (nband > 0 && cnt < kHitCap) {
+        const float4 me = cz[pos];
         int m = 0;
-        for (int t = 0; t < min(cnt, kHitCap); ++t) {
+        for (int t = 0; t < cnt; ++t) {
           const int v = hits[t * 32];
-          bool keep = true;
-          if (v & 0x8000) keep = exact_pair_pl(pl, ps, a, slot_index(T, v & 0x7FFF), b, p.cutoff2);
-          if (keep) hits[m++ * 32] = (uint16_t)(v & 0x7FFF);
+          const float4 q = cz[v];
+          const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+          const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const bool keep =
+              rr < p.lo2 || exact_pair_pl(pl, ps, a, slot_index(T, v), b, p.cutoff2);
+          if (keep) hits[m++ * 32] = (uint16_t)v;
         }
-        cnt = cnt > kHitCap ? cnt - (min(cnt, kHitCap) - m) : m;
+        cnt = m;
       }
     }
     const int rw = rw0[blockIdx.x] + w;
