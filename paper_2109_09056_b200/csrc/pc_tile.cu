@@ -721,11 +721,12 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st,
                                          bool nz, const pc_box& b, const TileForceParams& p,
                                          double& fx, double& fy, double& fz, float& pe,
                                          bool& overlap) {
-  const int G = (R + 7) >> 3;     // 8-round groups; the open group is padded with dummies
+  const int G = R >> 3;           // full 8-round groups
+  const int tail = R & 7;         // rounds of the open group (padded with dummies: skipped)
   uint4 nxt = first;
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
-    if (gi + 1 < G) nxt = ld_stream(lp + (gi + 1) * 32);
+    if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -734,6 +735,15 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st,
       tile_pair<MI, UNIT_SIGMA>(st, w[h] >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
                                 overlap);
     }
+  }
+  // open group: pairs in twos (warp-uniform count)
+  for (int j = 0; j < tail; j += 2) {
+    const uint32_t w = (j >> 1) == 0 ? nxt.x : ((j >> 1) == 1 ? nxt.y : ((j >> 1) == 2 ? nxt.z : nxt.w));
+    tile_pair<MI, UNIT_SIGMA>(st, w & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+                              overlap);
+    if (j + 1 < tail)
+      tile_pair<MI, UNIT_SIGMA>(st, w >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+                                overlap);
   }
 }
 
