@@ -590,6 +590,9 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     const bool act = u < T.H;
     int cnt = 0, a = -1, pos = -1, nband = 0;
     if (act) {
+      int ho = 0;                                // hit-list word offset (k * 32)
+      const int hlast = (kHitCap - 1) * 32;
+      float mx = 0.f;
       int c = 0;
 #pragma unroll
       for (int q = 1; q < kBX * kBY; ++q) c += (u >= T.home_pre[q]) ? 1 : 0;
@@ -621,24 +624,55 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
           const int mid = (hi + h3) >> 1;
           if (cz[mid].z <= zhi) hi = mid + 1; else h3 = mid;
         }
-        // the three pieces are one run unless a periodic z wrap splits them
+        // the three pieces are one run unless a periodic z wrap splits them;
+        // the row's own slot splits its own column's run
         const bool one = (e1 == b2) && (e2 == b3);
-        for (int piece = 0; piece < (one ? 1 : 3); ++piece) {
-          const int s0 = piece == 0 ? lo : (piece == 1 ? b2 : b3);
-          const int s1 = one ? hi : (piece == 0 ? e1 : (piece == 1 ? e2 : hi));
-#pragma unroll 4
-          for (int i = s0; i < s1; ++i) {
+        for (int piece = 0; piece < (one ? 2 : 4); ++piece) {
+          int s0, s1;
+          if (one) {
+            s0 = piece == 0 ? lo : max(lo, pos + 1);
+            s1 = piece == 0 ? min(hi, pos) : hi;
+          } else {
+            s0 = piece == 0 ? lo : (piece == 1 ? b2 : (piece == 2 ? max(b2, pos + 1) : b3));
+            s1 = piece == 0 ? e1 : (piece == 1 ? min(e2, pos) : (piece == 2 ? e2 : hi));
+          }
+          // four candidates per step: independent tests, then stores at the
+          // running hit offset (a non-hit's store is overwritten by the next
+          // hit); one short dependency chain per step instead of per candidate
+          int i = s0;
+          for (; i + 4 <= s1; i += 4) {
+            bool h[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4 q = cz[i + u];
+              const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
+              const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+              h[u] = rr < p.hi2;
+              mx = fmaxf(mx, h[u] ? rr : 0.f);
+            }
+            const int o1 = ho + (h[0] ? 32 : 0);
+            const int o2 = o1 + (h[1] ? 32 : 0);
+            const int o3 = o2 + (h[2] ? 32 : 0);
+            hits[ho] = (uint16_t)i;
+            hits[min(o1, hlast)] = (uint16_t)(i + 1);
+            hits[min(o2, hlast)] = (uint16_t)(i + 2);
+            hits[min(o3, hlast)] = (uint16_t)(i + 3);
+            ho = min(o3 + (h[3] ? 32 : 0), hlast);
+          }
+          for (; i < s1; ++i) {
             const float4 q = cz[i];
             const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
             const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            // unconditional store: slot cnt is overwritten unless this is a hit
-            hits[min(cnt, kHitCap - 1) * 32] = (uint16_t)i;
-            const bool hit = rr < p.hi2 && i != pos;
-            nband += (hit && rr >= p.lo2) ? 1 : 0;
-            cnt += hit ? 1 : 0;
+            hits[ho] = (uint16_t)i;
+            const bool hit = rr < p.hi2;
+            mx = fmaxf(mx, hit ? rr : 0.f);
+            ho = min(ho + (hit ? 32 : 0), hlast);
           }
         }
       }
+      cnt = ho >> 5;
+      if (cnt >= kHitCap - 1) cnt = kHitCap;        // (possible) overflow
+      nband = mx >= p.lo2 ? 1 : 0;
       a = slot_index(T, pos);
     }
     // hits inside the FP32 band: the reference's FP64 predicate decides (rare)
