@@ -533,9 +533,16 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   uint16_t* hits_all = reinterpret_cast<uint16_t*>(cz + p.max_stage);
   tile_setup<true>(blockIdx.x, g, b, cs, T);
   if (T.S > p.max_stage) {
+    // flag it; leave an empty plan so that a speculatively launched force
+    // pass stays in bounds (the caller discards it and falls back)
     if (threadIdx.x == 0) {
       atomicOr(flag, kFlagStage);
       atomicMax(flag + 1, T.S);
+      int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
+      pg[0] = 0;
+      pg[1] = 0;
+      pg[2] = 0;
+      pg[3] = rw0[blockIdx.x];
     }
     return;
   }
@@ -699,6 +706,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       if (lane == 0) {
         atomicOr(flag, kFlagOverflow);
         atomicMax(flag + 2, 1 << 20);
+        rounds[rw] = 0;           // keep a speculative force pass in bounds
       }
       __syncwarp();
       continue;
@@ -711,7 +719,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
                                  : schedule_rows(hits, cnt, lane, p.max_stage, lout, cap,
                                                  p.sched == 1);
     if (lane == 0) {
-      rounds[rw] = R;
+      rounds[rw] = ((R + 7) & ~7) > cap ? 0 : R;
       if (((R + 7) & ~7) > cap) {
         atomicOr(flag, kFlagOverflow);
         atomicMax(flag + 2, R);

@@ -253,10 +253,9 @@ class MDDriver:
         self.mode = "sell"
         self._tlist = None
         self._tplan = None
-        # tile list capacity: rounds per row-warp (in groups of 8), grown on
-        # demand by the build
-        k_est = 4.0 / 3.0 * np.pi * self.search ** 3 * n / np.prod(self.box.lengths)
-        self._q8 = max(2, -(-int(k_est * 1.45 + 8) // 8))
+        self._spec = False              # tile build issued, flags not yet checked
+        self.tile_failures = 0
+        self._q8 = 14                   # 112 rounds: the tile build's row capacity
         # planar x|y|z copy (stride _ps: a multiple of 16 elements, NaN rows
         # from cap on) -- the TMA staging source of the tile path and the
         # gather source of the SELL force kernel (24 B in 8-B items)
@@ -281,7 +280,7 @@ class MDDriver:
         # the lattice lies in [0, L): the reference's initial migrate wrap
         # (decomp.py:90-91) is the identity on it
         self._rebuild()
-        self._force(kick_dtm=0.0)
+        self._force_step(kick_dtm=0.0)
         self._timer.reset()
 
     # -- phases ------------------------------------------------------------
@@ -330,10 +329,14 @@ class MDDriver:
         self._t1("sort", e0)
         e0 = self._t0()
         self._cell_start = srt.cell_start
-        if self.tile and self._tile_build(srt.cell_start):
-            self._t1("neighbor", e0)
-            self.rebuilds += 1
-            return
+        if not (self.tile and self._tile_build(srt.cell_start)):
+            self._sell_build(srt.cell_start)
+        self._t1("neighbor", e0)
+        self.rebuilds += 1
+
+    def _sell_build(self, cell_start):
+        """SELL Verlet build (staged, or per particle for dense grids)."""
+        n, s = self.n, stream()
         self.mode = "half" if self.half_list else "sell"
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(n))
         used = ctypes.c_int32(0)
@@ -342,12 +345,12 @@ class MDDriver:
         while True:
             self.build_flag.zero_()
             if staged:
-                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(cell_start), self._grid,
                      self._pbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
                      ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s, None, None,
                      half)
             else:
-                call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                call("pc_nbr_build", ptr(self.pos), n, ptr(cell_start), self._grid,
                      self._pbox, self._search2, half, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
                      ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s, None,
                      None)
@@ -362,12 +365,15 @@ class MDDriver:
             self.ell_width = -(-(int(self.cnt[:n].max().item()) + 8) // 4) * 4
             self.nbr = self._new_nbr()
         self.used_staged = bool(used.value)
-        self._t1("neighbor", e0)
-        self.rebuilds += 1
 
     def _tile_build(self, cell_start) -> bool:
-        """Tile round-list build (pc_tile.cu); False when this grid or density
-        does not fit the tile path (the SELL path then runs)."""
+        """Issue the tile round-list build (pc_tile.cu) without a host sync.
+        Capacities are static (row-warps bounded by n/32 + tiles, rounds by
+        the build's row capacity), so the only failures are a neighbourhood
+        beyond the staging area or a row beyond the hit capacity; the build
+        flags are checked after the (speculative) force launch of the same
+        step, `_verify_tile_build`, which falls back to the SELL path.
+        False when this grid does not fit the tile path at all."""
         g = self._grid
         if min(g.nc[0], g.nc[1], g.nc[2]) < 3 or g.ndim != 3:
             return False
@@ -376,37 +382,54 @@ class MDDriver:
         rw = torch.empty(nt, dtype=torch.int32, device=dev)
         call("pc_tile_rows", ptr(cell_start), g, ptr(rw), s)
         self._rw0 = _kernels.scan_i32(rw)
-        total = int(self._rw0[nt].item())
+        bound = self.n // 32 + nt + 1
         self._ntiles = nt
-        if self._tlist is None or self._rounds.numel() < total:
-            grow = int(total * 1.05) + 16
-            self._rounds = torch.empty(grow, dtype=torch.int32, device=dev)
-            self._rowidx = torch.empty(grow * 32, dtype=torch.int32, device=dev)
+        if self._tlist is None or self._rounds.numel() < bound:
+            self._rounds = torch.empty(bound, dtype=torch.int32, device=dev)
+            self._rowidx = torch.empty(bound * 32, dtype=torch.int32, device=dev)
+            self._tlist = torch.empty(bound * self._q8 * 512, dtype=torch.uint8, device=dev)
         if self._tplan is None or self._tplan.numel() < nt * int(lib.pc_tile_plan_ints()):
             self._tplan = torch.empty(nt * int(lib.pc_tile_plan_ints()), dtype=torch.int32,
                                       device=dev)
-        while True:
-            need = total * self._q8 * 512
-            if self._tlist is None or self._tlist.numel() < need:
-                self._tlist = torch.empty(int(need * 1.05) + 512, dtype=torch.uint8, device=dev)
-            self.build_flag.zero_()
-            call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
-                 self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
-                 ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
-            fl, need_stage, need_rounds = (int(v) for v in self.build_flag.cpu())
-            if fl & _lib.FLAG_STAGE:           # neighbourhood beyond the smem staging area
-                return False
-            if fl & _lib.FLAG_OVERFLOW:
-                if need_rounds >= 1 << 20:      # a row beyond the build's hit capacity
-                    return False
-                self._q8 = -(-(need_rounds + 8) // 8)
-                continue
-            break
+        if self.partial.shape[0] < bound:
+            self.partial = torch.zeros((bound, 5), dtype=torch.float64, device=dev)
+        else:
+            self.partial.zero_()           # row-warps beyond this build's total stay 0
+        self.build_flag.zero_()
+        call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
+             self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
+             ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
         self.mode = "tile"
-        self._nblk = total
-        if self._nblk > self.partial.shape[0]:
-            self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
+        self._nblk = bound
+        self._spec = True
         return True
+
+    def _verify_tile_build(self, saved):
+        """Host check of the tile build flags after the speculative force was
+        launched (the GPU keeps running meanwhile); on failure restore the
+        state the force touched and redo the step's list + force on the SELL
+        path."""
+        self._spec = False
+        fl = int(self.build_flag[0].item())
+        if not fl & (_lib.FLAG_STAGE | _lib.FLAG_OVERFLOW):
+            return
+        vel, flag, kick_dtm = saved
+        self.vel.copy_(vel)
+        self.flag.copy_(flag)
+        self._advanced = False
+        self.tile_failures += 1
+        self._sell_build(self._cell_start)
+        self._force(kick_dtm)
+
+    def _force_step(self, kick_dtm):
+        """Force of this step; after a tile build, speculative (see
+        _verify_tile_build)."""
+        if self._spec:
+            saved = (self.vel.clone(), self.flag.clone(), kick_dtm)
+            self._force(kick_dtm)
+            self._verify_tile_build(saved)
+        else:
+            self._force(kick_dtm)
 
     def _force(self, kick_dtm):
         e0 = self._t0()
@@ -467,7 +490,7 @@ class MDDriver:
         self._integrate()
         if step_index % self.cfg.rebuild_stride == 0:
             self._rebuild()
-        self._force(kick_dtm=self._dtm)
+        self._force_step(kick_dtm=self._dtm)
 
     def check_errors(self):
         fl = int(self.flag.item())
