@@ -592,17 +592,25 @@ class MDDriver:
             self._timer.totals[k] = float(v)
 
 
-def run_md(cfg: MDConfig):
+def run_md(cfg: MDConfig, state=None, time_phases: bool = True):
     """Run the NVE loop; returns (per-step diagnostic rows, phase timings)
-    (ref md.py:295-307)."""
-    drv = MDDriver(cfg)
+    (ref md.py:295-307).  The per-step energies are reduced on the device
+    into a history buffer and read back once after the loop (the reference
+    returns the rows only at the end as well), so the step loop never waits
+    for the host.  An overlap detected in any step raises FloatingPointError
+    after the loop.  `state`: optional host (x, v) in global-id order."""
+    drv = MDDriver(cfg, state=state, time_phases=time_phases)
     drv.timings = {k: 0.0 for k in PHASES}
-    d = drv.diagnostics()
-    rows = [dict(step=0, KE=d["KE"], PE=d["PE"], E_total=d["E_total"],
-                 temperature=d["temperature"])]
+    hist = torch.empty((cfg.steps + 1, 5), dtype=torch.float64, device=drv.device)
+    hist[0].copy_(drv.device_diagnostics())
     for s in range(1, cfg.steps + 1):
         drv.step(s)
-        d = drv.diagnostics()
-        rows.append(dict(step=s, KE=d["KE"], PE=d["PE"], E_total=d["E_total"],
-                         temperature=d["temperature"]))
+        hist[s].copy_(drv.device_diagnostics())
+    h = hist.cpu().numpy()
+    drv.check_errors()
+    rows = []
+    for s in range(cfg.steps + 1):
+        ke, pe = float(h[s, 0]), float(h[s, 1])
+        rows.append(dict(step=s, KE=ke, PE=pe, E_total=ke + pe,
+                         temperature=2.0 * ke / (3.0 * drv.n)))
     return rows, drv.timings
