@@ -227,7 +227,8 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
  * reference's rounding order (minimum image on rows within mi_guard of a
  * periodic face), FP32 LJ magnitude, FP64 accumulation; writes f (planar,
  * f_stride), applies the final half kick v += dtm*f when d_v != NULL and
- * writes per-row-warp (KE, PE, px, py, pz) partials.  Overlap
+ * writes (KE, PE, px, py, pz) partials, pc_tile_force_partials(ntiles) of
+ * them (one per warp of the persistent grid).  Overlap
  * (r^2 < overlap2) sets d_flag bit 2.  With d_planar_next != NULL the next
  * step's integrate block (v' = v + dtm_next f, x' = wrap(x + dt v'), ref
  * md.py:219-231) is fused into the epilogue and written to d_planar_next /
@@ -239,6 +240,7 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
                   double dtm, double mass, double* d_partial, int32_t* d_flag,
                   double* d_planar_next, double* d_v_next, double dtm_next, double dt,
                   void* stream);
+int32_t pc_tile_force_partials(int32_t ntiles);
 /* pos4 x, y, z <- planar rows [0, n) (tags untouched). */
 int pc_pos_from_planar(const double* d_planar, int64_t planar_stride, int32_t n, double* d_pos4,
                        void* stream);

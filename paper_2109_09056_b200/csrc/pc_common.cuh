@@ -78,6 +78,17 @@ __device__ __forceinline__ double wrap_axis(double x, double low, double high, d
   return w >= high ? low : w;
 }
 
+// The same for a particle that moved less than one box length out of
+// [low, high) (every MD step): fmod(a, L) is a for a in [0, L) and the exact
+// a - L (Sterbenz) for a in [L, 2L); a in (-L, 0) takes numpy's +L fix.
+__device__ __forceinline__ double wrap_axis_near(double x, double low, double high, double L) {
+  const double a = __dsub_rn(x, low);
+  if (!(a > -L && a < 2.0 * L)) return wrap_axis(x, low, high, L);
+  const double m = a >= L ? __dsub_rn(a, L) : (a < 0.0 ? __dadd_rn(a, L) : a);
+  const double w = __dadd_rn(low, m == 0.0 ? 0.0 : m);
+  return w >= high ? low : w;
+}
+
 // numpy einsum order on this build: (x*x + z*z) + y*y, no FMA.
 __device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dz, dz)), __dmul_rn(dy, dy));

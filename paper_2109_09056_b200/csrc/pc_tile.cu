@@ -917,16 +917,19 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
                   double dtm_next, double dt) {
   extern __shared__ double dyn[];
   double* stage = dyn;                                             // nbuf x (x|y|z)
-  int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
   __shared__ ForceShared F;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
+  int* rwbk = pre + K + 1;                                              // first row-warp per k
   if (warp == 0) {
     // row-warp prefix over this CTA's tiles
     int carry = 0;
     for (int k0 = 0; k0 < K; k0 += 32) {
       const int k = k0 + lane;
-      const int c = k < K ? plan[(int64_t)(blockIdx.x + k * gridDim.x) * kPlanInts + 2] : 0;
+      const int* gpk = plan + (int64_t)(blockIdx.x + k * gridDim.x) * kPlanInts;
+      const int c = k < K ? gpk[2] : 0;
+      if (k < K) rwbk[k] = gpk[3];
       int inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -957,6 +960,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
   }
   __syncthreads();
   const int items = F.items;
+  double ake = 0.0, ape = 0.0, apx = 0.0, apy = 0.0, apz = 0.0;   // this lane's rows
 
   for (;;) {
     int i = 0;
@@ -970,8 +974,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       if (pre[mid] <= i) lo = mid; else hi = mid - 1;
     }
     const int k = lo;
-    const int tile = blockIdx.x + k * gridDim.x;
-    const int rw = plan[(int64_t)tile * kPlanInts + 3] + (i - pre[k]);
+    const int rw = rwbk[k] + (i - pre[k]);
     // prefetch everything that does not depend on the staged tile
     const int a = rowidx[(int64_t)rw * 32 + lane];
     const int R = rounds[rw];
@@ -1055,9 +1058,9 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
           double nx_ = __dadd_rn(xi, __dmul_rn(dt, ux));
           double ny_ = __dadd_rn(yi, __dmul_rn(dt, uy));
           double nz_ = __dadd_rn(zi, __dmul_rn(dt, uz));
-          if (b.periodic[0]) nx_ = wrap_axis(nx_, b.low[0], b.high[0], b.length[0]);
-          if (b.periodic[1]) ny_ = wrap_axis(ny_, b.low[1], b.high[1], b.length[1]);
-          if (b.periodic[2]) nz_ = wrap_axis(nz_, b.low[2], b.high[2], b.length[2]);
+          if (b.periodic[0]) nx_ = wrap_axis_near(nx_, b.low[0], b.high[0], b.length[0]);
+          if (b.periodic[1]) ny_ = wrap_axis_near(ny_, b.low[1], b.high[1], b.length[1]);
+          if (b.periodic[2]) nz_ = wrap_axis_near(nz_, b.low[2], b.high[2], b.length[2]);
           v_next[a] = ux;
           v_next[vs + a] = uy;
           v_next[2 * vs + a] = uz;
@@ -1067,16 +1070,22 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
         }
       }
     }
-    if (partial) {
-      ke = warp_sum(ke);
-      ped = warp_sum(ped);
-      px = warp_sum(px);
-      py = warp_sum(py);
-      pz = warp_sum(pz);
-      if (lane == 0) {
-        double* o = partial + (int64_t)rw * 5;
-        o[0] = ke; o[1] = ped; o[2] = px; o[3] = py; o[4] = pz;
-      }
+    ake += ke;
+    ape += ped;
+    apx += px;
+    apy += py;
+    apz += pz;
+  }
+  // one (KE, PE, px, py, pz) partial per warp of the grid
+  if (partial) {
+    ake = warp_sum(ake);
+    ape = warp_sum(ape);
+    apx = warp_sum(apx);
+    apy = warp_sum(apy);
+    apz = warp_sum(apz);
+    if (lane == 0) {
+      double* o = partial + ((int64_t)blockIdx.x * kForceWarps + warp) * 5;
+      o[0] = ake; o[1] = ape; o[2] = apx; o[3] = apy; o[4] = apz;
     }
   }
 }
@@ -1124,6 +1133,22 @@ int g_build_smem = 0, g_force_smem = 0;
 extern "C" {
 
 int32_t pc_tile_count(const pc_grid* grid) { return tile_dims(*grid).ntiles; }
+
+static int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int32_t pc_tile_force_partials(int32_t ntiles) {
+  const int grid = ntiles < sm_count() ? ntiles : sm_count();
+  return (grid > 0 ? grid : 1) * kForceWarps;
+}
 int32_t pc_tile_plan_ints(void) { return kPlanInts; }
 int32_t pc_tile_stage_cap(void) { return kStageCap; }
 
@@ -1221,13 +1246,7 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
   p.guard = mi_guard;
   p.Q8 = q8;
   p.ps = planar_stride;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = sm_count();
   const int grid = ntiles < sms ? ntiles : sms;
   const int K = (ntiles + grid - 1) / grid;
   // as many staging buffers as fit next to the item prefix (2..kNBuf)
@@ -1239,11 +1258,11 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
     if (smem_max <= 0) smem_max = 227 * 1024;
   }
   const int buf_bytes = 3 * kStageStride * (int)sizeof(double);
-  const int pre_bytes = (K + 1) * (int)sizeof(int);
+  const int pre_bytes = (2 * K + 1) * (int)sizeof(int);
   const int static_bytes = 512;
   int nbuf = kNBuf;
   while (nbuf > 2 && nbuf * buf_bytes + pre_bytes + static_bytes > smem_max) --nbuf;
-  const int smem = nbuf * buf_bytes + pre_bytes;
+  const int smem = nbuf * buf_bytes + pre_bytes + K * (int)sizeof(int);
   if (smem + static_bytes > smem_max) {
     set_error("pc_tile_force: %d tiles per CTA do not fit in shared memory", K);
     return PC_ERR_CAPACITY;

@@ -391,16 +391,15 @@ class MDDriver:
         if self._tplan is None or self._tplan.numel() < nt * int(lib.pc_tile_plan_ints()):
             self._tplan = torch.empty(nt * int(lib.pc_tile_plan_ints()), dtype=torch.int32,
                                       device=dev)
-        if self.partial.shape[0] < bound:
-            self.partial = torch.zeros((bound, 5), dtype=torch.float64, device=dev)
-        else:
-            self.partial.zero_()           # row-warps beyond this build's total stay 0
+        npart = int(lib.pc_tile_force_partials(nt))
+        if self.partial.shape[0] < npart:
+            self.partial = torch.zeros((npart, 5), dtype=torch.float64, device=dev)
         self.build_flag.zero_()
         call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
              ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
         self.mode = "tile"
-        self._nblk = bound
+        self._nblk = npart
         self._spec = True
         return True
 
