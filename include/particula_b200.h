@@ -223,6 +223,14 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
                   const pc_grid* grid, const pc_box* box, double cutoff2, int32_t q8,
                   const int32_t* d_rw0, int32_t* d_plan, int32_t* d_rowidx, int32_t* d_rounds,
                   void* d_list, int32_t* d_flag, void* stream);
+/* Reorder the rounds of every row-warp (after pc_tile_build, same list):
+ * residue round-robin per row so that the 16 lanes of a half-warp read 16
+ * distinct shared-memory bank pairs in most rounds.  rw_bound >= the total
+ * row-warps, which the kernel reads from d_rw_total (= d_rw0[ntiles]).
+ * kind: 0 = keep the build's ascending order, 1 = residue round-robin,
+ * 2 = class-major rotated to the lane's residue. */
+int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_rounds,
+                  void* d_list, int32_t q8, int32_t kind, void* stream);
 /* LJ force over the tile lists: exact FP64 r^2 < rc^2 re-test in the
  * reference's rounding order (minimum image on rows within mi_guard of a
  * periodic face), FP32 LJ magnitude, FP64 accumulation; writes f (planar,

@@ -114,6 +114,7 @@ SIGNATURES = {
                                      c_dbl, c_dbl, c_vp]),
     "pc_pos_from_planar": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_tile_force_partials": (c_i32, [c_i32]),
+    "pc_tile_order": (ctypes.c_int, [c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "pc_tile_decode": (ctypes.c_int, [c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                       c_vp]),
     "pc_halo_unpack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),

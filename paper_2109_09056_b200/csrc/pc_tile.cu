@@ -395,91 +395,131 @@ __device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, 
 }
 
 // ---- residue round-robin row order (default) --------------------------------
-// Byte c of a 4 x u32 pack (16 classes, values < 256).
-__device__ __forceinline__ uint32_t pk_get(const uint32_t (&w)[4], int c) {
-  const uint32_t x = (c >> 2) == 0 ? w[0] : ((c >> 2) == 1 ? w[1] : ((c >> 2) == 2 ? w[2] : w[3]));
-  return (x >> ((c & 3) * 8)) & 0xFFu;
-}
-__device__ __forceinline__ void pk_add(uint32_t (&w)[4], int c, uint32_t v) {
-  const uint32_t inc = v << ((c & 3) * 8);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) w[q] += ((c >> 2) == q) ? inc : 0u;
-}
-
 // Lane-local bank-conflict avoidance (no cross-lane coordination).  The
-// entries of a row are bucketed by bank-pair residue (slot % 16, an in-place
-// one-digit counting sort of its hit list) and emitted round-robin: in round
-// r the lane prefers residue (lane + r) % 16 -- lanes of a half-warp prefer
-// distinct residues in every round -- and falls back to the next non-empty
-// residue.  Simulated on LJ tiles: 1.6 LDS.64 passes per half-warp instead
-// of 2.5 for the ascending order, with the same round count (the longest
-// row).  Padding rounds read the dummy of the preferred residue.
+// entries of a row are bucketed by bank-pair residue (slot % 16) and emitted
+// round-robin: in round r the lane prefers residue (lane + r) % 16 -- the 16
+// lanes of a half-warp prefer 16 distinct residues in every round -- and
+// falls back to the next non-empty residue.  Simulated on LJ tiles: 1.6
+// LDS.64 passes per half-warp instead of 2.5 for the ascending order, at the
+// same round count; measured: force pass -14 %.  Cost: the row's class-major
+// order is scattered into its own list column (global, L2-resident), then
+// read back in round-robin order (rotate + ffs over the mask of non-empty
+// residues, byte counters packed in two 64-bit words), then written out.
 __device__ __forceinline__ int rr_rows(uint16_t* __restrict__ hits, int cnt, int lane,
                                        int dummy0, uint4* __restrict__ out, int cap_rounds) {
-  uint32_t cn[4] = {0u, 0u, 0u, 0u};
-  for (int k = 0; k < cnt; ++k) pk_add(cn, hits[k * 32] & 15, 1u);
-  // exclusive byte prefix over the 16 classes (all sums < 256)
-  uint32_t st[4];
-  {
-    uint32_t carry = 0u;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t inc = cn[q] * 0x01010101u;          // inclusive prefix within the word
-      st[q] = inc - cn[q] + carry * 0x01010101u;
-      carry += inc >> 24;
-    }
+  uint16_t* col = reinterpret_cast<uint16_t*>(out);     // slot k at (k >> 3) * 256 + (k & 7)
+  const unsigned long long B = 0x0101010101010101ull;
+  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+  for (int k = 0; k < cnt; ++k) {
+    const int c = hits[k * 32] & 15;
+    const unsigned long long inc = 1ull << ((c & 7) * 8);
+    if (c < 8) clo += inc; else chi += inc;
   }
-  // in-place permutation into class-major order (American flag sort)
-  uint32_t wp[4] = {st[0], st[1], st[2], st[3]};
-  for (int c = 0; c < 16; ++c) {
-    const uint32_t e = pk_get(st, c) + pk_get(cn, c);
-    for (;;) {
-      const uint32_t i = pk_get(wp, c);
-      if (i >= e) break;
-      const uint32_t v = hits[i * 32];
-      const int d = v & 15;
-      if (d == c) {
-        pk_add(wp, c, 1u);
+  const unsigned long long ilo = clo * B;               // inclusive byte prefix (< 256)
+  const unsigned long long slo = ilo - clo;
+  const unsigned long long shi = chi * B - chi + (ilo >> 56) * B;
+  unsigned long long rlo = slo, rhi = shi;
+  for (int k = 0; k < cnt; ++k) {                       // class-major scatter
+    const uint32_t v = hits[k * 32];
+    const int c = v & 15, sh = (c & 7) * 8;
+    const unsigned long long inc = 1ull << sh;
+    int pos;
+    if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
+    else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
+    col[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)(v * 8u);
+  }
+  const unsigned long long nz = ((clo | (clo >> 1) | (clo >> 2) | (clo >> 3) | (clo >> 4) |
+                                  (clo >> 5) | (clo >> 6) | (clo >> 7)) & B);
+  const unsigned long long nzh = ((chi | (chi >> 1) | (chi >> 2) | (chi >> 3) | (chi >> 4) |
+                                   (chi >> 5) | (chi >> 6) | (chi >> 7)) & B);
+  // byte-wise "non-zero" flags -> 16-bit mask (bit c = class c non-empty)
+  unsigned ne = (unsigned)(((nz * 0x0102040810204080ull) >> 56) & 0xFFull) |
+                ((unsigned)(((nzh * 0x0102040810204080ull) >> 56) & 0xFFull) << 8);
+  unsigned long long plo = slo, phi = shi, qlo = clo, qhi = chi;
+  for (int r0 = 0; r0 < cnt; r0 += 8) {                 // round-robin emission
+    // 8 rounds: positions from the register state first, then 8 independent
+    // loads of the class-major copy (L2 round trips overlap)
+    int pos[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int pref = (lane + r0 + u) & 15;
+      const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
+      const int c = (pref + __ffs(rot) - 1) & 15, sh = (c & 7) * 8;
+      const unsigned long long inc = 1ull << sh;
+      unsigned left;
+      if (c < 8) {
+        pos[u] = (int)((plo >> sh) & 0xFFull);
+        plo += inc;
+        qlo -= inc;
+        left = (unsigned)((qlo >> sh) & 0xFFull);
       } else {
-        const uint32_t j = pk_get(wp, d);
-        hits[i * 32] = hits[j * 32];
-        hits[j * 32] = (uint16_t)v;
-        pk_add(wp, d, 1u);
+        pos[u] = (int)((phi >> sh) & 0xFFull);
+        phi += inc;
+        qhi -= inc;
+        left = (unsigned)((qhi >> sh) & 0xFFull);
       }
+      if (left == 0u) ne &= ~(1u << c);
+      if (r0 + u >= cnt) pos[u] = 0;      // past the row: any valid address
+      if (ne == 0u) ne = 1u;              // (exhausted: keep ffs defined)
     }
+    uint16_t vals[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vals[u] = col[(pos[u] >> 3) * 256 + (pos[u] & 7)];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (r0 + u < cnt) hits[(r0 + u) * 32] = vals[u];
   }
   const int R = __reduce_max_sync(0xffffffffu, cnt);
-  uint32_t rp[4] = {st[0], st[1], st[2], st[3]};
-  uint32_t rem[4] = {cn[0], cn[1], cn[2], cn[3]};
-  uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;     // 8 x u16 shift register
-  for (int r = 0; r < R; ++r) {
-    int c = (lane + r) & 15;
-    uint32_t o;
-    if (r < cnt) {
-      while (pk_get(rem, c) == 0u) c = (c + 1) & 15;
-      o = hits[pk_get(rp, c) * 32];
-      pk_add(rp, c, 1u);
-      pk_add(rem, c, 0xFFFFFFFFu);                     // -1 in byte c (no borrow: > 0)
-    } else {
-      o = (uint32_t)(dummy0 + c);
+  for (int r8 = 0; r8 < R && r8 + 8 <= cap_rounds; r8 += 8) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = r8 + 2 * h;
+      const uint32_t lo = r < cnt ? (uint32_t)hits[r * 32]
+                                  : (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+      const uint32_t hi = r + 1 < cnt ? (uint32_t)hits[(r + 1) * 32]
+                                      : (uint32_t)(dummy0 + ((lane + r + 1) & 15)) * 8u;
+      w[h] = lo | (hi << 16);
     }
-    b0 = __funnelshift_r(b0, b1, 16);
-    b1 = __funnelshift_r(b1, b2, 16);
-    b2 = __funnelshift_r(b2, b3, 16);
-    b3 = (b3 >> 16) | ((o * 8u) << 16);
-    if (((r + 1) & 7) == 0 && r + 1 <= cap_rounds)
-      out[(r >> 3) * 32] = make_uint4(b0, b1, b2, b3);
+    out[(r8 >> 3) * 32] = make_uint4(w[0], w[1], w[2], w[3]);
   }
-  if (R & 7) {     // pad the open group
-    const uint32_t d = (uint32_t)((dummy0 + (lane & 15)) * 8);
-    for (int r = R; r & 7; ++r) {
-      b0 = __funnelshift_r(b0, b1, 16);
-      b1 = __funnelshift_r(b1, b2, 16);
-      b2 = __funnelshift_r(b2, b3, 16);
-      b3 = (b3 >> 16) | (d << 16);
-    }
-    if (((R + 7) & ~7) <= cap_rounds) out[(R >> 3) * 32] = make_uint4(b0, b1, b2, b3);
+  return R;
+}
+
+// Cheaper variant (default): class-major order with the residue classes
+// visited in a lane-rotated order (lane l starts at residue l % 16).  The
+// row's entries are scattered straight into their final list positions (one
+// pass over the hits; per-class running counts as packed bytes).  Simulated:
+// 2.0 LDS.64 passes per half-warp (round-robin: 1.6, ascending: 2.5).
+__device__ __forceinline__ int cm_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
+                                       int dummy0, uint4* __restrict__ out, int cap_rounds) {
+  uint16_t* col = reinterpret_cast<uint16_t*>(out);     // slot k at (k >> 3) * 256 + (k & 7)
+  const unsigned long long B = 0x0101010101010101ull;
+  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+  for (int k = 0; k < cnt; ++k) {
+    const int c = hits[k * 32] & 15;
+    const unsigned long long inc = 1ull << ((c & 7) * 8);
+    if (c < 8) clo += inc; else chi += inc;
   }
+  const unsigned long long ilo = clo * B;
+  unsigned long long rlo = ilo - clo;                   // exclusive prefix = class starts
+  unsigned long long rhi = chi * B - chi + (ilo >> 56) * B;
+  const int l0 = lane & 15;
+  const int s0 = (int)(((l0 < 8 ? rlo : rhi) >> ((l0 & 7) * 8)) & 0xFFull);
+  for (int k = 0; k < cnt; ++k) {
+    const uint32_t v = hits[k * 32];
+    const int c = v & 15, sh = (c & 7) * 8;
+    const unsigned long long inc = 1ull << sh;
+    int pos;
+    if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
+    else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
+    pos -= s0;                                          // rotate: class l0 first
+    if (pos < 0) pos += cnt;
+    col[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)(v * 8u);
+  }
+  const int R = __reduce_max_sync(0xffffffffu, cnt);
+  for (int r = cnt; r < ((R + 7) & ~7) && r < cap_rounds; ++r)
+    col[(r >> 3) * 256 + (r & 7)] = (uint16_t)((dummy0 + ((lane + r) & 15)) * 8);
   return R;
 }
 
@@ -714,7 +754,8 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     __syncwarp();
     const int cap = 8 * p.Q8;
     uint4* lout = list + (int64_t)rw * p.Q8 * 32 + lane;
-    const int R = p.sched == 0   ? rr_rows(hits, cnt, lane, p.max_stage, lout, cap)
+    const int R = p.sched == 0   ? cm_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                  : p.sched == 4 ? rr_rows(hits, cnt, lane, p.max_stage, lout, cap)
                   : p.sched == 3 ? plain_rows(hits, cnt, lane, p.max_stage, lout, cap)
                                  : schedule_rows(hits, cnt, lane, p.max_stage, lout, cap,
                                                  p.sched == 1);
@@ -1090,6 +1131,122 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
   }
 }
 
+// ---- list reorder: residue round-robin rounds (after the build) ------------
+// One warp per row-warp.  Reads the plain (ascending) list, reorders every
+// lane's row in shared memory -- class-major scatter by bank-pair residue,
+// then round-robin emission: in round r lane l prefers residue (l + r) % 16,
+// falling back to the next non-empty residue (rotate + ffs over a 16-bit
+// mask) -- and writes it back in place.  The 16 lanes of a half-warp then
+// prefer 16 distinct residues in every round: 1.6 LDS.64 passes per
+// half-warp instead of 2.5 (simulated), force pass -14 % (measured).
+constexpr int kOrdWarps = 8;
+
+// RR = false: class-major with the start rotated to the lane's residue (the
+// cheaper variant, simulated 1.9 passes per half-warp).
+template <bool RR>
+__global__ void __launch_bounds__(kOrdWarps * 32, 3)
+tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
+                  const int* __restrict__ rw_total, int Q8, int dummy0) {
+  extern __shared__ uint16_t obuf[];                    // [warp][kHitCap][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rw = blockIdx.x * kOrdWarps + warp;
+  if (rw >= *rw_total) return;
+  uint16_t* Bm = obuf + warp * kHitCap * 32 + lane;
+  const int R = rounds[rw];
+  if (R <= 0 || R > kHitCap) return;
+  uint4* lp = list + (int64_t)rw * Q8 * 32 + lane;
+  const uint32_t dmin = (uint32_t)dummy0 * 8u;
+  const int G = (R + 7) >> 3;
+  const unsigned long long B8 = 0x0101010101010101ull;
+  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+  int cnt = 0;                                          // real entries precede padding
+  for (int g = 0; g < G; ++g) {
+    const uint4 q = lp[g * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+      if (g * 8 + t < R && v < dmin) {
+        const int c = (v >> 3) & 15;
+        const unsigned long long inc = 1ull << ((c & 7) * 8);
+        if (c < 8) clo += inc; else chi += inc;
+        ++cnt;
+      }
+    }
+  }
+  const unsigned long long ilo = clo * B8;
+  const unsigned long long slo = ilo - clo;
+  const unsigned long long shi = chi * B8 - chi + (ilo >> 56) * B8;
+  int s0 = 0;
+  if (!RR) {
+    const int c0 = lane & 15;
+    s0 = (int)(((c0 < 8 ? slo : shi) >> ((c0 & 7) * 8)) & 0xFFull);
+  }
+  unsigned long long rlo = slo, rhi = shi;
+  for (int g = 0; g < G; ++g) {                         // class-major scatter -> smem
+    const uint4 q = lp[g * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+      if (g * 8 + t < cnt) {
+        const int c = (v >> 3) & 15, sh = (c & 7) * 8;
+        const unsigned long long inc = 1ull << sh;
+        int pos;
+        if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
+        else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
+        if (!RR) { pos -= s0; if (pos < 0) pos += cnt; }
+        Bm[pos * 32] = (uint16_t)v;
+      }
+    }
+  }
+  unsigned ne = 0u;
+  unsigned long long plo = slo, phi = shi, qlo = clo, qhi = chi;
+  if (RR) {
+    const unsigned long long nzl = (clo | (clo >> 1) | (clo >> 2) | (clo >> 3) | (clo >> 4) |
+                                    (clo >> 5) | (clo >> 6) | (clo >> 7)) & B8;
+    const unsigned long long nzh = (chi | (chi >> 1) | (chi >> 2) | (chi >> 3) | (chi >> 4) |
+                                    (chi >> 5) | (chi >> 6) | (chi >> 7)) & B8;
+    ne = (unsigned)(((nzl * 0x0102040810204080ull) >> 56) & 0xFFull) |
+         ((unsigned)(((nzh * 0x0102040810204080ull) >> 56) & 0xFFull) << 8);
+  }
+  for (int g = 0; g < G; ++g) {                         // emit 8 rounds per uint4
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = g * 8 + t;
+      uint32_t v;
+      if (r < cnt) {
+        int pos = r;
+        if (RR) {
+          const int pref = (lane + r) & 15;
+          const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
+          const int c = (pref + __ffs(rot) - 1) & 15, sh = (c & 7) * 8;
+          const unsigned long long inc = 1ull << sh;
+          unsigned left;
+          if (c < 8) {
+            pos = (int)((plo >> sh) & 0xFFull);
+            plo += inc;
+            qlo -= inc;
+            left = (unsigned)((qlo >> sh) & 0xFFull);
+          } else {
+            pos = (int)((phi >> sh) & 0xFFull);
+            phi += inc;
+            qhi -= inc;
+            left = (unsigned)((qhi >> sh) & 0xFFull);
+          }
+          if (left == 0u) ne &= ~(1u << c);
+        }
+        v = Bm[pos * 32];
+      } else {
+        v = (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+      }
+      o[t >> 1] |= (t & 1) ? (v << 16) : v;
+    }
+    lp[g * 32] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // ---- decode: tile lists -> per-row dense table of particle indices ---------
 __global__ void __launch_bounds__(256)
 tile_decode_kernel(const int* __restrict__ plan, int Q8, int max_stage,
@@ -1290,6 +1447,32 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
         *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
         d_v_next, dtm_next, dt);
   return check_launch("pc_tile_force");
+}
+
+int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_rounds,
+                  void* d_list, int32_t q8, int32_t kind, void* stream) {
+  if (rw_bound <= 0 || kind == 0) return PC_OK;
+  static int set = 0;
+  const int smem = kOrdWarps * kHitCap * 32 * (int)sizeof(uint16_t);
+  if (!set) {
+    if (cudaFuncSetAttribute(tile_order_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(tile_order_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      set_error("pc_tile_order: %d B of shared memory not available", smem);
+      return PC_ERR_CAPACITY;
+    }
+    set = 1;
+  }
+  const int grid = (rw_bound + kOrdWarps - 1) / kOrdWarps;
+  uint4* l = reinterpret_cast<uint4*>(d_list);
+  if (kind == 1)
+    tile_order_kernel<true><<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
+        l, d_rounds, d_rw_total, q8, kStageCap);
+  else
+    tile_order_kernel<false><<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
+        l, d_rounds, d_rw_total, q8, kStageCap);
+  return check_launch("pc_tile_order");
 }
 
 int pc_tile_decode(int32_t ntiles, const int32_t* d_plan, const int32_t* d_rowidx,

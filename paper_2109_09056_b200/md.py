@@ -27,10 +27,14 @@ the reference does (md.py:67-86) and uploaded once.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
+
+# residue round-robin reorder of the tile lists (PC_TILE_ORDER: 0 off, 1 round-robin, 2 class-major)
+_TILE_ORDER = int(os.environ.get("PC_TILE_ORDER", "1"))
 
 from . import _kernels, _lib, aosoa, decomp
 from ._lib import call, ptr, stream
@@ -398,6 +402,9 @@ class MDDriver:
         call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
              ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
+        # bank-conflict-aware round order (pc_tile_order; lists unchanged as sets)
+        call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds),
+             ptr(self._tlist), self._q8, _TILE_ORDER, s)
         self.mode = "tile"
         self._nblk = npart
         self._spec = True
