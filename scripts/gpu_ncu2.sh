@@ -5,3 +5,4 @@ T=${1:-t}
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_force -s 3 -c 1 -o gpurun_out/${T}_force python bench.py --steps 12 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${T}_force.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_build -s 0 -c 1 -o gpurun_out/${T}_build python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${T}_build.log 2>&1
 ls -la gpurun_out/*.ncu-rep
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_order -s 0 -c 1 -o gpurun_out/${T}_order python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${T}_order.log 2>&1
