@@ -13,8 +13,10 @@ events on the launching stream, barrier + synchronize on both sides, max over
 ranks.  The working set (Verlet list ~330 MB at 1M atoms) exceeds the 126 MB
 L2, so no explicit L2 flush is done between steps.
 
-Under torchrun (N > 1) every rank runs its own 64^3 domain replica
-(weak scaling, no data-path collective yet -- see DESIGN.md).
+Under torchrun (N > 1) the global system is N 64^3-cell blocks decomposed
+over rank_dims 2x1x1 / 2x2x1 / 2x2x2 (weak scaling): one rank per GPU, tile
+path on every rank's local grid, ghost refresh every step and migrate + halo
+rebuild every 20 steps over NCCL (paper_2109_09056_b200.dist).
 
 ``--impl reference`` times the CPU oracle port of the reference
 (oracle/particula_oracle.py: numpy, single-threaded like the reference) on a
@@ -233,12 +235,8 @@ def run_ours(args):
     diag = drv.diagnostics()
     force_ms = [a.elapsed_time(b) for a, b in eng.force_events]
     eng.force_events = None
-    n_rows = eng.n_total if world > 1 else n          # rows this rank's force kernel sweeps
     n_local = eng.n_owned if world > 1 else n
-    if world > 1:
-        kmean = float(eng.cnt[:n_rows].float().sum().item()) / max(1, n_local)
-    else:
-        kmean = eng.mean_neighbors()
+    kmean = eng.mean_neighbors()
     # algorithmic bytes per force launch per atom (SURVEY §8d
     # K6 + the fused final kick): a 4-B neighbour index per list entry (k)
     # + row length 4 + position read once 24 + FP64 force write 24 + final

@@ -129,6 +129,19 @@ int pc_scan_i32_i64(const int32_t* d_in, int64_t* d_out, int64_t n,
                     void* d_tmp, int64_t tmp_bytes, void* stream);
 int64_t pc_scan_tmp_bytes(int64_t n);
 
+/* Stable partition of n keys in [0, nbins), nbins <= 256 (grouping by owner
+ * rank, ref decomp.py:97-99; key digits of bin_by_key, ref binning.py:49-55).
+ * pc_partition_hist writes hist[b * C + c] = count of key b in chunk c of
+ * 1024 elements (C = pc_partition_chunks(n)); the caller scans it
+ * (pc_scan_i32: off, nbins * C + 1 entries; bin b starts at off[b * C]);
+ * pc_partition_place writes order[dst] = src, equal keys in ascending src.
+ * O(n) at any bin occupancy (pc_bin_place is for small linked cells). */
+int64_t pc_partition_chunks(int64_t n);
+int pc_partition_hist(const int32_t* d_keys, int64_t n, int32_t nbins, int32_t* d_hist,
+                      void* stream);
+int pc_partition_place(const int32_t* d_keys, int64_t n, int32_t nbins, const int32_t* d_off,
+                       int32_t* d_order, void* stream);
+
 /* Stable counting-sort placement: order[dst] = src with equal cells kept in
  * ascending src order (ref binning.py:49-55 argsort(kind="stable")).
  * d_cell_fill (ncells) must be zeroed by the caller. */
@@ -223,6 +236,19 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
                   const pc_grid* grid, const pc_box* box, double cutoff2, int32_t q8,
                   const int32_t* d_rw0, int32_t* d_plan, int32_t* d_rowidx, int32_t* d_rounds,
                   void* d_list, int32_t* d_flag, void* stream);
+/* pc_tile_build for a decomposed domain (owned + ghost rows, ref
+ * md.py:176-188): cells, tiles and the FP32 prefilter use d_bplanar (ghosts
+ * shifted by their periodic image into the local frame; grid/box = the local
+ * grid and box), the exact FP64 predicate uses the raw positions d_planar and
+ * the global box_exact (the reference's ghost convention), and rows i with
+ * d_skip[i] != 0 (ghosts) get empty lists.  NULL d_bplanar / box_exact /
+ * d_skip: pc_tile_build. */
+int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
+                         const int32_t* d_cell_start, const pc_grid* grid, const pc_box* box,
+                         double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
+                         int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
+                         void* stream, const double* d_bplanar, const pc_box* box_exact,
+                         const int32_t* d_skip);
 /* Reorder the rounds of every row-warp (after pc_tile_build, same list):
  * residue round-robin per row so that the 16 lanes of a half-warp read 16
  * distinct shared-memory bank pairs in most rounds.  rw_bound >= the total

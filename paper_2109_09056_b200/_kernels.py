@@ -52,6 +52,24 @@ def scan_i32(counts, out_dtype=torch.int32):
     return out
 
 
+def stable_partition(keys, nbins):
+    """Stable partition of int32 keys in [0, nbins), nbins <= 256
+    (pc_partition_hist -> scan -> pc_partition_place): (order[dst] = src,
+    bin starts on the device, nbins + 1 entries)."""
+    n = keys.numel()
+    dev = keys.device
+    nch = int(_lib.load().pc_partition_chunks(n))
+    hist = torch.zeros(max(nbins * nch, 1), dtype=torch.int32, device=dev)
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if n == 0:
+        return order[:0], torch.zeros(nbins + 1, dtype=torch.int32, device=dev)
+    keys = keys.contiguous()
+    call("pc_partition_hist", ptr(keys), n, nbins, ptr(hist), stream())
+    off = scan_i32(hist[:nbins * nch])
+    call("pc_partition_place", ptr(keys), n, nbins, ptr(off), ptr(order), stream())
+    return order[:n], off[::nch][: nbins + 1]
+
+
 class CellSort:
     """Stable counting sort of particles into a linked-cell grid.
 

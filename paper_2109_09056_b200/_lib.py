@@ -76,6 +76,9 @@ SIGNATURES = {
     "pc_scan_i32_i64": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "pc_scan_tmp_bytes": (c_i64, [c_i64]),
     "pc_bin_place": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pc_partition_chunks": (c_i64, [c_i64]),
+    "pc_partition_hist": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "pc_partition_place": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "pc_invert_order": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "pc_nbr_build": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.POINTER(PcGrid),
                                     ctypes.POINTER(PcBox), c_dbl, c_i32, c_i32, c_i32,
@@ -108,6 +111,10 @@ SIGNATURES = {
     "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
                                      ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_vp]),
+    "pc_tile_build_domain": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
+                                            ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp,
+                                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                            ctypes.POINTER(PcBox), c_vp]),
     "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl, c_vp,
                                      c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp,

@@ -65,19 +65,6 @@ class CellBinning:
         return int(np.prod(self.cells))
 
 
-def _order_from_cells(cell_of, counts, n):
-    """Stable counting-sort order[dst] = src for precomputed cell ids."""
-    dev = cell_of.device
-    ncells = counts.numel()
-    start = _kernels.scan_i32(counts)
-    fill = torch.zeros(max(ncells, 1), dtype=torch.int32, device=dev)
-    tmp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    call("pc_bin_place", ptr(cell_of), n, ptr(start), ncells, ptr(fill), ptr(tmp), ptr(order),
-         stream())
-    return order, start
-
-
 def bin_by_key(keys) -> Permutation:
     """Stable sort permutation of integer keys (ref binning.py:49-55)."""
     k = keys if isinstance(keys, torch.Tensor) else torch.as_tensor(np.asarray(keys))
@@ -90,15 +77,16 @@ def bin_by_key(keys) -> Permutation:
     span = int(k.max().item()) - kmin          # unsigned span of (key - kmin)
     perm = None                                # current order[dst] = src (int32)
     shift = 0
-    digit_bits = 16
+    # LSD passes of 8-bit digits, each a stable partition (O(n) however many
+    # keys share a digit -- pc_bin_place's cell stabilisation is for small cells)
+    digit_bits = 8
     while True:
         cell_of = torch.empty(n, dtype=torch.int32, device=dev)
         ncells = 1 << digit_bits
         counts = torch.zeros(ncells, dtype=torch.int32, device=dev)
         call("pc_key_digits", ptr(k), ptr(perm), n, kmin, shift, ncells - 1, ptr(cell_of),
              ptr(counts), stream())
-        order, _ = _order_from_cells(cell_of, counts, n)
-        order = order[:n]
+        order, _ = _kernels.stable_partition(cell_of, ncells)
         perm = order if perm is None else _kernels.gather_rows(perm, order, n)
         shift += digit_bits
         if shift >= 64 or (span >> shift) == 0:

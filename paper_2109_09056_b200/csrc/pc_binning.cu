@@ -378,6 +378,85 @@ int pc_csr_to_dense(const int64_t* d_offsets, int32_t n, const int32_t* d_index,
   return check_launch("pc_csr_to_dense");
 }
 
+// ---- stable partition into few bins (<= 256) ------------------------------
+// The atomic placement + per-cell stabilisation above is built for linked
+// cells of ~20 particles (rank counting is O(m^2) per cell).  Grouping by
+// owner rank (ref decomp.py:97-99) or by a key digit puts up to n elements in
+// one bin, so these use a chunked stable partition instead: per 1024-element
+// chunk a histogram (bin-major hist[b * nchunks + c]), one exclusive scan
+// (pc_scan_i32: off = global start of chunk c's elements of bin b), then each
+// element's rank among equal keys of its chunk in index order (MATCH.ANY in
+// the warp + per-warp prefix per bin).  O(n), deterministic, stable.
+constexpr int kPartChunk = 1024;
+constexpr int kPartMaxBins = 256;
+
+__global__ void __launch_bounds__(kPartChunk)
+partition_hist_kernel(const int* __restrict__ keys, int64_t n, int nbins, int nchunks,
+                      int* __restrict__ hist) {
+  __shared__ int h[kPartMaxBins];
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kPartChunk + threadIdx.x;
+  if (i < n) atomicAdd(&h[keys[i]], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    hist[(int64_t)b * nchunks + blockIdx.x] = h[b];
+}
+
+__global__ void __launch_bounds__(kPartChunk)
+partition_place_kernel(const int* __restrict__ keys, int64_t n, int nbins, int nchunks,
+                       const int* __restrict__ off, int* __restrict__ order) {
+  __shared__ int wc[kPartChunk / 32][kPartMaxBins];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = lane; b < nbins; b += 32) wc[warp][b] = 0;
+  const int64_t i = (int64_t)blockIdx.x * kPartChunk + threadIdx.x;
+  const int key = i < n ? keys[i] : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int rank = __popc(peers & ((1u << lane) - 1u));
+  __syncwarp();
+  if (key >= 0 && rank == 0) wc[warp][key] = __popc(peers);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) {    // prefix over warps
+    int run = 0;
+    for (int w = 0; w < kPartChunk / 32; ++w) {
+      const int v = wc[w][b];
+      wc[w][b] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (key >= 0)
+    order[off[(int64_t)key * nchunks + blockIdx.x] + wc[warp][key] + rank] = (int)i;
+}
+
+int64_t pc_partition_chunks(int64_t n) { return n > 0 ? (n + kPartChunk - 1) / kPartChunk : 0; }
+
+int pc_partition_hist(const int32_t* d_keys, int64_t n, int32_t nbins, int32_t* d_hist,
+                      void* stream) {
+  if (nbins <= 0 || nbins > kPartMaxBins) {
+    set_error("pc_partition_hist: nbins must be in [1, %d]", kPartMaxBins);
+    return PC_ERR_VALUE;
+  }
+  if (n <= 0) return PC_OK;
+  const int64_t nch = pc_partition_chunks(n);
+  partition_hist_kernel<<<(unsigned)nch, kPartChunk, 0, as_stream(stream)>>>(
+      d_keys, n, nbins, (int)nch, d_hist);
+  return check_launch("pc_partition_hist");
+}
+
+int pc_partition_place(const int32_t* d_keys, int64_t n, int32_t nbins, const int32_t* d_off,
+                       int32_t* d_order, void* stream) {
+  if (nbins <= 0 || nbins > kPartMaxBins) {
+    set_error("pc_partition_place: nbins must be in [1, %d]", kPartMaxBins);
+    return PC_ERR_VALUE;
+  }
+  if (n <= 0) return PC_OK;
+  const int64_t nch = pc_partition_chunks(n);
+  partition_place_kernel<<<(unsigned)nch, kPartChunk, 0, as_stream(stream)>>>(
+      d_keys, n, nbins, (int)nch, d_off, d_order);
+  return check_launch("pc_partition_place");
+}
+
 int64_t pc_scan_tmp_bytes(int64_t n) { return scan_tmp_elems(n) * (int64_t)sizeof(int64_t); }
 
 int pc_scan_i32(const int32_t* d_in, int32_t* d_out, int64_t n, void* d_tmp,

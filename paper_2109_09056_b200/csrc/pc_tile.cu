@@ -51,7 +51,10 @@ constexpr int kSX = kBX + 2, kSY = kBY + 2, kSZ = kTZ + 2;
 constexpr int kSCols = kSX * kSY;
 constexpr int kSegs = kSCols * 3;
 constexpr int kNDummy = 16;
-constexpr int kForceWarps = 32;
+#ifndef PC_FORCE_WARPS
+#define PC_FORCE_WARPS 32
+#endif
+constexpr int kForceWarps = PC_FORCE_WARPS;
 constexpr int kBuildWarps = 10;
 constexpr int kHitCap = 112;
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
@@ -567,7 +570,8 @@ __global__ void __launch_bounds__(kBuildWarps * 32, 2)
 tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
-                  int* __restrict__ flag) {
+                  int* __restrict__ flag, const double* __restrict__ bpl, pc_box e,
+                  const int* __restrict__ skip) {
   extern __shared__ float4 cz[];                 // staged FP32 copy | per-warp hit rows
   __shared__ TileSetup T;
   uint16_t* hits_all = reinterpret_cast<uint16_t*>(cz + p.max_stage);
@@ -622,9 +626,9 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     for (int t = threadIdx.x; t < len; t += blockDim.x) {
       const int j = src + t;
       float4 q;
-      q.x = (float)(pl[j] + sx);
-      q.y = (float)(pl[ps + j] + sy);
-      q.z = (float)(pl[2 * ps + j] + sz);
+      q.x = (float)(bpl[j] + sx);
+      q.y = (float)(bpl[ps + j] + sy);
+      q.z = (float)(bpl[2 * ps + j] + sz);
       q.w = 0.f;
       cz[dst + t] = q;
     }
@@ -648,14 +652,18 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       pos = T.cell_lo[hcol][1] + (u - T.home_pre[c]);
       int k = 1;
       for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
+      a = slot_index(T, pos);
       const float4 me = cz[pos];
+      // rows flagged in `skip` (ghosts of a decomposed domain) keep an empty
+      // list: zero force, and they are never a row of the force pass's pairs
+      const bool scan = !(skip && skip[a]);
       // every stencil column is swept over the same z-window |dz| < h,
       // h = sqrt(hi2) (lateral pruning would only shorten some lanes'
       // windows; the warp runs the longest anyway)
       const float h = sqrtf(p.hi2) * 1.0001f + 1e-4f;
       const float zlo = me.z - h, zhi = me.z + h;
 #pragma unroll 1
-      for (int cc = 0; cc < 9; ++cc) {
+      for (int cc = 0; cc < (scan ? 9 : 0); ++cc) {
         const int col = (hx + cc / 3) * kSY + (hy + cc % 3);
         // [lo, e1) in cell k-1 (suffix), cell k, [b3, hi) in cell k+1 (prefix)
         int lo = T.cell_lo[col][k - 1], h1 = T.cell_hi[col][k - 1];
@@ -720,7 +728,6 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       cnt = ho >> 5;
       if (cnt >= kHitCap - 1) cnt = kHitCap;        // (possible) overflow
       nband = mx >= p.lo2 ? 1 : 0;
-      a = slot_index(T, pos);
     }
     // hits inside the FP32 band: the reference's FP64 predicate decides (rare)
     if (__any_sync(0xffffffffu, nband > 0)) {
@@ -733,7 +740,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
           const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
           const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           const bool keep =
-              rr < p.lo2 || exact_pair_pl(pl, ps, a, slot_index(T, v), b, p.cutoff2);
+              rr < p.lo2 || exact_pair_pl(pl, ps, a, slot_index(T, v), e, p.cutoff2);
           if (keep) hits[m++ * 32] = (uint16_t)v;
         }
         cnt = m;
@@ -1140,49 +1147,54 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
 // prefer 16 distinct residues in every round: 1.6 LDS.64 passes per
 // half-warp instead of 2.5 (simulated), force pass -14 % (measured).
 constexpr int kOrdWarps = 8;
+constexpr int kOrdSmem = kOrdWarps * (kHitCap * 32 * 2 + 16 * 32 * 4);
 
 // RR = false: class-major with the start rotated to the lane's residue (the
-// cheaper variant, simulated 1.9 passes per half-warp).
+// cheaper variant, simulated 1.9 passes per half-warp).  Per-class state
+// lives in a per-lane shared table st[c][lane] (conflict-free: bank = lane).
 template <bool RR>
 __global__ void __launch_bounds__(kOrdWarps * 32, 3)
 tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
                   const int* __restrict__ rw_total, int Q8, int dummy0) {
-  extern __shared__ uint16_t obuf[];                    // [warp][kHitCap][32]
+  extern __shared__ __align__(16) unsigned char osm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rw = blockIdx.x * kOrdWarps + warp;
   if (rw >= *rw_total) return;
-  uint16_t* Bm = obuf + warp * kHitCap * 32 + lane;
+  uint32_t* st = reinterpret_cast<uint32_t*>(osm) + warp * 16 * 32 + lane;   // [c][lane]
+  uint16_t* Bm = reinterpret_cast<uint16_t*>(osm + kOrdWarps * 16 * 32 * 4) +
+                 warp * kHitCap * 32 + lane;                                  // [k][lane]
   const int R = rounds[rw];
   if (R <= 0 || R > kHitCap) return;
   uint4* lp = list + (int64_t)rw * Q8 * 32 + lane;
   const uint32_t dmin = (uint32_t)dummy0 * 8u;
   const int G = (R + 7) >> 3;
-  const unsigned long long B8 = 0x0101010101010101ull;
-  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+#pragma unroll
+  for (int c = 0; c < 16; ++c) st[c * 32] = 0u;
   int cnt = 0;                                          // real entries precede padding
-  for (int g = 0; g < G; ++g) {
+  for (int g = 0; g < G; ++g) {                         // per-class counts
     const uint4 q = lp[g * 32];
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
       if (g * 8 + t < R && v < dmin) {
-        const int c = (v >> 3) & 15;
-        const unsigned long long inc = 1ull << ((c & 7) * 8);
-        if (c < 8) clo += inc; else chi += inc;
+        uint32_t* sc = st + ((v >> 3) & 15) * 32;
+        *sc += 1u;
         ++cnt;
       }
     }
   }
-  const unsigned long long ilo = clo * B8;
-  const unsigned long long slo = ilo - clo;
-  const unsigned long long shi = chi * B8 - chi + (ilo >> 56) * B8;
+  // exclusive prefix -> st[c] = start | start << 16 (next | begin); end = next start
+  uint32_t run = 0u;
   int s0 = 0;
-  if (!RR) {
-    const int c0 = lane & 15;
-    s0 = (int)(((c0 < 8 ? slo : shi) >> ((c0 & 7) * 8)) & 0xFFull);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const uint32_t n = st[c * 32];
+    if (!RR && c == (lane & 15)) s0 = (int)run;
+    st[c * 32] = run | ((run + n) << 16);               // next | end
+    run += n;
   }
-  unsigned long long rlo = slo, rhi = shi;
+  unsigned ne = 0u;
   for (int g = 0; g < G; ++g) {                         // class-major scatter -> smem
     const uint4 q = lp[g * 32];
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
@@ -1190,25 +1202,25 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
     for (int t = 0; t < 8; ++t) {
       const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
       if (g * 8 + t < cnt) {
-        const int c = (v >> 3) & 15, sh = (c & 7) * 8;
-        const unsigned long long inc = 1ull << sh;
-        int pos;
-        if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
-        else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
-        if (!RR) { pos -= s0; if (pos < 0) pos += cnt; }
+        const int c = (v >> 3) & 15;
+        uint32_t* sc = st + c * 32;
+        const uint32_t e = *sc;
+        *sc = e + 1u;
+        int pos = (int)(e & 0xFFFFu);
+        if (RR) ne |= 1u << c;
+        else { pos -= s0; if (pos < 0) pos += cnt; }
         Bm[pos * 32] = (uint16_t)v;
       }
     }
   }
-  unsigned ne = 0u;
-  unsigned long long plo = slo, phi = shi, qlo = clo, qhi = chi;
-  if (RR) {
-    const unsigned long long nzl = (clo | (clo >> 1) | (clo >> 2) | (clo >> 3) | (clo >> 4) |
-                                    (clo >> 5) | (clo >> 6) | (clo >> 7)) & B8;
-    const unsigned long long nzh = (chi | (chi >> 1) | (chi >> 2) | (chi >> 3) | (chi >> 4) |
-                                    (chi >> 5) | (chi >> 6) | (chi >> 7)) & B8;
-    ne = (unsigned)(((nzl * 0x0102040810204080ull) >> 56) & 0xFFull) |
-         ((unsigned)(((nzh * 0x0102040810204080ull) >> 56) & 0xFFull) << 8);
+  if (RR) {                                             // rewind next to begin
+    uint32_t beg = 0u;                                  // begin(c) = end(c - 1)
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const uint32_t end = st[c * 32] >> 16;
+      st[c * 32] = beg | (end << 16);
+      beg = end;
+    }
   }
   for (int g = 0; g < G; ++g) {                         // emit 8 rounds per uint4
     uint32_t o[4] = {0u, 0u, 0u, 0u};
@@ -1219,23 +1231,16 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
       if (r < cnt) {
         int pos = r;
         if (RR) {
+          // in round r lane l prefers residue (l + r) % 16, else the next
+          // non-empty one
           const int pref = (lane + r) & 15;
           const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
-          const int c = (pref + __ffs(rot) - 1) & 15, sh = (c & 7) * 8;
-          const unsigned long long inc = 1ull << sh;
-          unsigned left;
-          if (c < 8) {
-            pos = (int)((plo >> sh) & 0xFFull);
-            plo += inc;
-            qlo -= inc;
-            left = (unsigned)((qlo >> sh) & 0xFFull);
-          } else {
-            pos = (int)((phi >> sh) & 0xFFull);
-            phi += inc;
-            qhi -= inc;
-            left = (unsigned)((qhi >> sh) & 0xFFull);
-          }
-          if (left == 0u) ne &= ~(1u << c);
+          const int c = (pref + __ffs(rot) - 1) & 15;
+          uint32_t* sc = st + c * 32;
+          const uint32_t e = *sc;
+          pos = (int)(e & 0xFFFFu);
+          *sc = e + 1u;
+          if ((uint32_t)pos + 1u == (e >> 16)) ne &= ~(1u << c);
         }
         v = Bm[pos * 32];
       } else {
@@ -1336,6 +1341,17 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
                   const pc_grid* grid, const pc_box* box, double cutoff2, int32_t q8,
                   const int32_t* d_rw0, int32_t* d_plan, int32_t* d_rowidx, int32_t* d_rounds,
                   void* d_list, int32_t* d_flag, void* stream) {
+  return pc_tile_build_domain(d_planar, planar_stride, d_cell_start, grid, box, cutoff2, q8,
+                              d_rw0, d_plan, d_rowidx, d_rounds, d_list, d_flag, stream,
+                              nullptr, nullptr, nullptr);
+}
+
+int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
+                         const int32_t* d_cell_start, const pc_grid* grid, const pc_box* box,
+                         double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
+                         int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
+                         void* stream, const double* d_bplanar, const pc_box* box_exact,
+                         const int32_t* d_skip) {
   if (q8 <= 0 || planar_stride % 16) {
     set_error("pc_tile_build: bad list capacity or planar stride");
     return PC_ERR_VALUE;
@@ -1374,7 +1390,8 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
   const int nt = tile_dims(*grid).ntiles;
   tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
       d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
-      reinterpret_cast<uint4*>(d_list), d_flag);
+      reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
+      box_exact ? *box_exact : *box, d_skip);
   return check_launch("pc_tile_build");
 }
 
@@ -1453,7 +1470,7 @@ int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_
                   void* d_list, int32_t q8, int32_t kind, void* stream) {
   if (rw_bound <= 0 || kind == 0) return PC_OK;
   static int set = 0;
-  const int smem = kOrdWarps * kHitCap * 32 * (int)sizeof(uint16_t);
+  const int smem = kOrdSmem;
   if (!set) {
     if (cudaFuncSetAttribute(tile_order_kernel<true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||

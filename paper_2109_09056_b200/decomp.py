@@ -93,22 +93,12 @@ def _owner_tensor(fabric: DomainFabric, x: torch.Tensor) -> torch.Tensor:
 
 
 def _group_by(keys: torch.Tensor, nbins: int):
-    """Stable counting sort of int32 keys in [0, nbins): (order, starts host)."""
-    n = keys.numel()
-    bits = max(1, int(np.ceil(np.log2(max(nbins, 2)))))
-    cells = 1 << bits
-    dev = keys.device
-    counts = torch.zeros(cells, dtype=torch.int32, device=dev)
-    cell_of = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    k64 = keys.to(torch.int64)
-    call("pc_key_digits", ptr(k64), None, n, 0, 0, cells - 1, ptr(cell_of), ptr(counts), stream())
-    start = _kernels.scan_i32(counts)
-    fill = torch.zeros(cells, dtype=torch.int32, device=dev)
-    tmp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    call("pc_bin_place", ptr(cell_of), n, ptr(start), cells, ptr(fill), ptr(tmp), ptr(order),
-         stream())
-    return order[:n], start.cpu().numpy()[: nbins + 1]
+    """Stable grouping of int32 keys in [0, nbins): (order, starts host)
+    (ref decomp.py:97-99; pc_partition_*, O(n) at any group size)."""
+    if nbins > 256:
+        raise ValueError("at most 256 ranks")
+    order, starts = _kernels.stable_partition(keys.to(torch.int32), nbins)
+    return order, starts.cpu().numpy()[: nbins + 1]
 
 
 def _field_width(pset: ParticleSet, name: str) -> int:

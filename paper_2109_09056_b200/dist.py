@@ -36,8 +36,8 @@ from . import _kernels, _lib
 from ._lib import call, ptr, stream
 from .decomp import DomainFabric, decompose
 from .geometry import Box
-from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, fcc_lattice, \
-    initial_velocities
+from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _TILE_ORDER, _lj_params, _PhaseTimer, \
+    fcc_lattice, initial_velocities
 
 MIG_W = 7     # migrate row: x, y, z, vx, vy, vz, gid (int64 bits)
 HALO_W = 7    # halo row: x, y, z, gid bits, shift x, y, z
@@ -68,7 +68,8 @@ class DomainEngine:
     """One rank's particles and kernels (owned + ghost rows in one array)."""
 
     def __init__(self, cfg: MDConfig, fabric: DomainFabric, rank: int, x, v, gid, device,
-                 ell_width: int = 128, planar_gather: bool = True, time_phases: bool = False):
+                 ell_width: int = 128, planar_gather: bool = True, time_phases: bool = False,
+                 tile: bool = True):
         self.cfg = cfg
         self.fabric = fabric
         self.rank = rank
@@ -86,7 +87,17 @@ class DomainEngine:
         self._search2 = self.search * self.search
         self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
         self.ell_width = -(-int(ell_width) // 4) * 4
-        self.planar_gather = planar_gather
+        self.planar_gather = planar_gather or tile
+        # tile path (pc_tile.cu, as the single-domain engine): local grid,
+        # binpos-staged FP32 prefilter, raw positions + global minimum image
+        # for the exact predicate and the force; SELL when the local grid has
+        # < 3 cells on an axis or a tile build overflows
+        self.tile = bool(tile)
+        self.mode = "sell"
+        self._q8 = 14
+        self._tlist = None
+        self._tplan = None
+        self.tile_failures = 0
         self._time = time_phases
         self.timer = _PhaseTimer()
         self._local_grid()
@@ -101,7 +112,7 @@ class DomainEngine:
             self.vel[:, :n] = v.to(self.device, torch.float64).t()
         self.is_ghost = torch.zeros(self.cap, dtype=torch.int32, device=self.device)
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.build_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.build_flag = torch.zeros(3, dtype=torch.int32, device=self.device)
         self.export_rows = {}     # dest -> int32 sorted rows (per-step pack)
         self.ghost_blocks = []    # [(src, int32 sorted rows)] ascending src
         self.rebuilds = 0
@@ -191,9 +202,11 @@ class DomainEngine:
         slices = -(-self.cap // 32)
         self.nbr = torch.empty(slices * self.ell_width * 32, dtype=torch.int32, device=dev)
         self.pl = None
+        self._ps = -(-(self.cap + 1) // 16) * 16      # planar stride (TMA: 16-element multiple)
         if self.planar_gather:
-            self.pl = torch.empty((3, self.cap + 1), dtype=torch.float64, device=dev)
-            self.pl[:, self.cap] = float("nan")
+            self.pl = torch.empty((3, self._ps), dtype=torch.float64, device=dev)
+            self.pl[:, self.cap:] = float("nan")
+            self.bpl = torch.empty_like(self.pl) if self.tile else None
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(self.cap))
         self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
@@ -221,7 +234,7 @@ class DomainEngine:
         e0 = self._t0()
         call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
              self.cap, self.n_total, self._dtm, float(self.cfg.dt), self._gbox, ptr(self.pl),
-             self.cap + 1, stream())
+             self._ps, stream())
         self._t1("integrate", e0)
 
     def _owned_rows(self):
@@ -387,6 +400,14 @@ class DomainEngine:
         e0 = self._t0()
         srt = _kernels.CellSort(self.binpos[:n], 4, self._grid)
         order = srt.order
+        tile = self.tile and n > 0 and min(self._grid.nc[0], self._grid.nc[1],
+                                           self._grid.nc[2]) >= 3
+        if tile:
+            # z-sorted cells (local frame): the tile path's staged columns and
+            # home rows are z-sorted slot runs (pc_tile.cu)
+            order = torch.empty_like(srt.order)
+            call("pc_cell_zsort", ptr(self.binpos), ptr(srt.cell_start), self._grid.ncells,
+                 ptr(srt.order), ptr(order), s)
         new_pos = torch.empty_like(self.pos)
         new_pos[self.cap] = self.pos[self.cap]
         _kernels.gather_rows(self.pos, order, n, out=new_pos)
@@ -406,9 +427,14 @@ class DomainEngine:
         self.ghost_blocks = [(src, inv32[at:at + m].contiguous())
                              for src, at, m in getattr(self, "_ghost_src", [])]
         if self.pl is not None:
-            call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self.cap + 1, s)
+            call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
         e0 = self._t0()
+        if tile and self._tile_build(srt.cell_start):
+            self.rebuilds += 1
+            self._t1("neighbor", e0)
+            return
+        self.mode = "sell"
         used = ctypes.c_int32(0)
         staged = True
         while True:
@@ -423,7 +449,7 @@ class DomainEngine:
                      self._lbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
                      ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s,
                      ptr(self.binpos), self._gbox)
-            fl = int(self.build_flag.item())
+            fl = int(self.build_flag[0].item())
             if fl & _lib.FLAG_STAGE:
                 staged = False
                 continue
@@ -437,6 +463,44 @@ class DomainEngine:
         self.used_staged = bool(used.value)
         self.rebuilds += 1
         self._t1("neighbor", e0)
+
+    def _tile_build(self, cell_start) -> bool:
+        """Tile round lists of all rows (ghost rows empty, pc_tile_build_domain);
+        False (SELL fallback) when a neighbourhood or a row exceeds the tile
+        capacities."""
+        n, s, dev = self.n_total, stream(), self.device
+        lib, g = _lib.load(), self._grid
+        call("pc_pos_planar", ptr(self.binpos), n, ptr(self.bpl), self._ps, s)
+        nt = int(lib.pc_tile_count(g))
+        rw = torch.empty(nt, dtype=torch.int32, device=dev)
+        call("pc_tile_rows", ptr(cell_start), g, ptr(rw), s)
+        self._rw0 = _kernels.scan_i32(rw)
+        bound = n // 32 + nt + 1
+        self._ntiles = nt
+        if self._tlist is None or self._rounds.numel() < bound:
+            self._rounds = torch.empty(bound, dtype=torch.int32, device=dev)
+            self._rowidx = torch.empty(bound * 32, dtype=torch.int32, device=dev)
+            self._tlist = torch.empty(bound * self._q8 * 512, dtype=torch.uint8, device=dev)
+        pi = int(lib.pc_tile_plan_ints())
+        if self._tplan is None or self._tplan.numel() < nt * pi:
+            self._tplan = torch.empty(nt * pi, dtype=torch.int32, device=dev)
+        self._nblk_tile = int(lib.pc_tile_force_partials(nt))
+        if self.partial.shape[0] < self._nblk_tile:
+            self.partial = torch.zeros((self._nblk_tile, 5), dtype=torch.float64, device=dev)
+        self.build_flag.zero_()
+        call("pc_tile_build_domain", ptr(self.pl), self._ps, ptr(cell_start), g, self._lbox,
+             self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
+             ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s, ptr(self.bpl),
+             self._gbox, ptr(self.is_ghost))
+        fl = int(self.build_flag[0].item())
+        if fl & (_lib.FLAG_STAGE | _lib.FLAG_OVERFLOW):
+            self.tile_failures += 1
+            return False
+        call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds), ptr(self._tlist),
+             self._q8, _TILE_ORDER, s)
+        self.mode = "tile"
+        self.used_staged = True
+        return True
 
     def refresh_out(self):
         """Per-step ghost refresh payload (raw x, y, z of exported rows)."""
@@ -455,7 +519,7 @@ class DomainEngine:
         for src, rows in self.ghost_blocks:
             buf = inbox[src]
             call("pc_halo_unpack", ptr(buf), ptr(rows), rows.numel(), ptr(self.pos),
-                 ptr(self.pl), self.cap + 1, stream())
+                 ptr(self.pl), self._ps, stream())
         self._t1("halo", e0)
 
     def force(self, kick_dtm):
@@ -464,19 +528,64 @@ class DomainEngine:
         if ev is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-        call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self.cap + 1, self.n_total,
-             ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
-             self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap, float(kick_dtm),
-             float(self.cfg.mass), ptr(self.partial), ptr(self.flag), stream())
+        if self.mode == "tile":
+            call("pc_tile_force", ptr(self.pl), self._ps, self._ntiles, ptr(self._tplan),
+                 ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._gbox,
+                 self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag), None,
+                 None, 0.0, 0.0, stream())
+        else:
+            call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self._ps, self.n_total,
+                 ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
+                 self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
+                 stream())
         if ev is not None:
             b.record()
             ev.append((a, b))
         self._t1("force", e0)
 
     def local_diagnostics(self):
-        nb = int(_lib.load().pc_lj_force_sell_partials(self.n_total))
+        nb = self._nblk_tile if self.mode == "tile" else \
+            int(_lib.load().pc_lj_force_sell_partials(self.n_total))
         call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
         return self.diag
+
+    def mean_neighbors(self) -> float:
+        """Mean Verlet-list length over owned rows (ghost rows are empty)."""
+        n = self.n_total
+        if self.mode == "tile":
+            cnt = torch.zeros(n, dtype=torch.int32, device=self.device)
+            table = torch.empty((n, 128), dtype=torch.int32, device=self.device)
+            call("pc_tile_decode", self._ntiles, ptr(self._tplan), ptr(self._rowidx),
+                 ptr(self._rounds), ptr(self._tlist), self._q8, 128, ptr(cnt), ptr(table),
+                 stream())
+            total = float(cnt.double().sum().item())
+        else:
+            total = float(self.cnt[:n].double().sum().item())
+        return total / max(1, self.n_owned)
+
+    def neighbor_rows(self):
+        """Verlet rows of the current build as host lists of local row
+        indices, row = current (cell-sorted) index; ghost rows are empty."""
+        n = self.n_total
+        out = []
+        if self.mode == "tile":
+            w = 128
+            cnt = torch.zeros(n, dtype=torch.int32, device=self.device)
+            table = torch.full((n, w), -1, dtype=torch.int32, device=self.device)
+            call("pc_tile_decode", self._ntiles, ptr(self._tplan), ptr(self._rowidx),
+                 ptr(self._rounds), ptr(self._tlist), self._q8, w, ptr(cnt), ptr(table),
+                 stream())
+            c, t = cnt.cpu().numpy(), table.cpu().numpy()
+            return [t[a, :c[a]] for a in range(n)]
+        Q = self.ell_width // 4
+        cnt = self.cnt[:n].cpu().numpy()
+        words = self.nbr.cpu().numpy()
+        for a in range(n):
+            k = np.arange(cnt[a])
+            out.append(words[((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)])
+        return out
 
     def owned_state(self):
         """(gid, x, v) of owned rows (host numpy)."""
@@ -527,7 +636,7 @@ class FabricMD(_StepLogic):
     reference's in-process fabric (md.py MDDriver with rank_dims), with GPU
     kernels doing every data-sized step."""
 
-    def __init__(self, cfg: MDConfig, device=None):
+    def __init__(self, cfg: MDConfig, device=None, tile: bool = True):
         cfg.validate()
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
@@ -543,11 +652,12 @@ class FabricMD(_StepLogic):
         self.engines = []
         for r in range(self.fabric.n_ranks):
             if r == 0:
-                self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev))
+                self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev, tile=tile))
             else:
                 z = torch.zeros((0, 3), dtype=torch.float64)
                 self.engines.append(DomainEngine(cfg, self.fabric, r, z, z,
-                                                 torch.zeros(0, dtype=torch.int64), dev))
+                                                 torch.zeros(0, dtype=torch.int64), dev,
+                                                 tile=tile))
         self._init_forces()
 
     def _engines(self):

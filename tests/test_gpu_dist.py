@@ -34,14 +34,21 @@ def _run(drv, steps):
     return np.array(out)
 
 
+@pytest.mark.parametrize("tile", [True, False])
 @pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 1)])
-def test_fabric_matches_single_domain(pc, dims):
+def test_fabric_matches_single_domain(pc, dims, tile):
+    """Tile path on every rank (the local grids have >= 3 cells per axis):
+    pair energies are FP32 terms summed per row in staged-slot order, which
+    differs between a domain's local grid and the global one, so the bar is
+    the tile path's energy tolerance (1e-6, as vs the reference); the SELL
+    path (FP64 energies) must agree to 1e-10."""
     kw = dict(lattice_cells=6, density=0.8442, temperature=1.44, cutoff=2.5, skin=0.3,
               rebuild_stride=5, seed=1, steps=0)
-    ref = _run(pc.md.MDDriver(pc.md.MDConfig(**kw)), 30)
-    fab = pc.dist.FabricMD(pc.md.MDConfig(**dict(kw, rank_dims=dims)))
+    ref = _run(pc.md.MDDriver(pc.md.MDConfig(**kw), tile=tile), 30)
+    fab = pc.dist.FabricMD(pc.md.MDConfig(**dict(kw, rank_dims=dims)), tile=tile)
+    assert all(e.mode == ("tile" if tile else "sell") for e in fab.engines)
     got = _run(fab, 30)
-    assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-10
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < (1e-6 if tile else 1e-10)
     # every particle owned exactly once, by the rank containing it
     ids = np.concatenate([e.owned_state()[0] for e in fab.engines])
     assert np.array_equal(np.sort(ids), np.arange(fab.n))
@@ -61,12 +68,15 @@ def test_fabric_reference_series_crit3(pc):
     assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-5
 
 
-def test_fabric_ghost_lists_match_global(pc, oracle):
+@pytest.mark.parametrize("tile", [True, False])
+def test_fabric_ghost_lists_match_global(pc, oracle, tile):
     """Owned rows' Verlet sets on a 2x2x2 fabric (ghosts included, mapped to
-    global ids) equal the single-domain sets, bit-exact."""
+    global ids) equal the single-domain sets, bit-exact -- tile path (local
+    grid, binpos-staged prefilter, raw-position exact predicate) and SELL."""
     cfg = pc.md.MDConfig(lattice_cells=8, density=0.8442, temperature=1.44, cutoff=2.5,
                          skin=0.3, rebuild_stride=20, seed=5, steps=0, rank_dims=(2, 2, 2))
-    fab = pc.dist.FabricMD(cfg)
+    fab = pc.dist.FabricMD(cfg, tile=tile)
+    assert all(e.mode == ("tile" if tile else "sell") for e in fab.engines)
     x, _ = fab.gather_state()
     ref = oracle.build_verlet(x, np.zeros(3), fab.box.high, [True] * 3,
                               (cfg.cutoff + cfg.skin) * (1 + 1e-9))
@@ -74,15 +84,13 @@ def test_fabric_ghost_lists_match_global(pc, oracle):
     seen = 0
     for e in fab.engines:
         n = e.n_total
-        Q = e.ell_width // 4
-        cnt = e.cnt[:n].cpu().numpy()
-        words = e.nbr.cpu().numpy()
         gid = e.pos[:n, 3].contiguous().view(__import__("torch").int64).cpu().numpy()
         ghost = e.is_ghost[:n].cpu().numpy().astype(bool)
-        for a in np.flatnonzero(~ghost):
-            k = np.arange(cnt[a])
-            w = ((a >> 5) * Q + (k >> 2)) * 128 + (a & 31) * 4 + (k & 3)
-            got = np.sort(gid[words[w]])
-            assert np.array_equal(got, rows[gid[a]])
+        nb = e.neighbor_rows()
+        for a in range(n):
+            if ghost[a]:
+                assert nb[a].size == 0
+                continue
+            assert np.array_equal(np.sort(gid[nb[a]]), rows[gid[a]])
             seen += 1
     assert seen == fab.n

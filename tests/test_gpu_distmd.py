@@ -1,7 +1,8 @@
 """Multi-process DistMD (one process per rank, torch.distributed) on one GPU:
 two ranks share cuda:0 with the gloo backend (host-staged blocks; NCCL needs
 distinct GPUs).  The decomposed run must reproduce the single-domain energy
-series -- the same engine code the N-GPU bench runs over NCCL."""
+series (within the tile path's 1e-6 energy tolerance) -- the same engine code
+the N-GPU bench runs over NCCL."""
 
 import os
 import socket
@@ -67,4 +68,4 @@ def test_distmd_two_processes(world):
     owned = sum(o[2] for o in out)
     assert owned == drv.n
     for _, es, _ in out:
-        assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-10
+        assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-6     # tile path: FP32 pair energies summed in slot order

@@ -88,6 +88,27 @@ def test_bin_by_key_stable(pc):
     assert np.array_equal(np.argsort(pw.map), np.argsort(wide, kind="stable"))
 
 
+def test_bin_by_key_large_equal_groups(pc):
+    """Few distinct keys over many elements (every digit bin holds ~n/3):
+    stable and O(n) (pc_partition_*), vs numpy's stable argsort."""
+    keys = np.random.default_rng(4).integers(0, 3, 400_000)
+    p = pc.binning.bin_by_key(keys)
+    assert np.array_equal(np.argsort(p.map), np.argsort(keys, kind="stable"))
+    same = np.full(100_000, 7)
+    assert np.array_equal(pc.binning.bin_by_key(same).map, np.arange(100_000))
+
+
+def test_group_by_owner_ranks_1m(pc):
+    """Grouping 1M particles by owner rank (ref decomp.py:97-99): stable."""
+    import torch
+    from paper_2109_09056_b200.decomp import _group_by
+    own = np.random.default_rng(5).integers(0, 8, 1 << 20).astype(np.int32)
+    order, starts = _group_by(torch.as_tensor(own).cuda(), 8)
+    ref = np.argsort(own, kind="stable")
+    assert np.array_equal(order.cpu().numpy(), ref)
+    assert np.array_equal(starts, np.concatenate(([0], np.cumsum(np.bincount(own, minlength=8)))))
+
+
 def test_cell_indices_rejects_outside(pc):
     box = pc.geometry.Box([0.0], [1.0])
     with pytest.raises(ValueError):
