@@ -399,10 +399,13 @@ int pc_compact(const int32_t* d_flag, const int32_t* d_pos, int64_t n, int32_t* 
  * ref decomp.py:243-246). */
 int pc_gather_shift(const double* d_src, const int32_t* d_idx, int64_t m, int32_t w,
                     const double* d_shift, double* d_dst, void* stream);
-/* Per-step halo refresh: buf[k] = pos4[rows[k]].xyz (pack) and
- * pos4[rows[k]].xyz = buf[k] (+ planar copy) (unpack), buf (m, 3) f64. */
+/* Per-step halo refresh: buf[k] = pos4[rows[k]].xyz (pack; _planar: from
+ * the planar x|y|z copy) and pos4[rows[k]].xyz = buf[k] (+ planar copy; NULL
+ * d_pos: planar only) (unpack), buf (m, 3) f64. */
 int pc_halo_pack(const double* d_pos, const int32_t* d_rows, int64_t m, double* d_buf,
                  void* stream);
+int pc_halo_pack_planar(const double* d_planar, int64_t planar_stride, const int32_t* d_rows,
+                        int64_t m, double* d_buf, void* stream);
 int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double* d_pos,
                    double* d_planar, int64_t planar_stride, void* stream);
 /* dst[idx[k]] += src[k] over rows of w doubles, idx distinct per call

@@ -103,6 +103,7 @@ SIGNATURES = {
     "pc_gather_shift": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "pc_scatter_add": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_halo_pack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "pc_halo_pack_planar": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "pc_tile_count": (c_i32, [ctypes.POINTER(PcGrid)]),
     "pc_tile_plan_ints": (c_i32, []),
     "pc_cell_zsort": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),

@@ -143,6 +143,17 @@ __global__ void halo_pack_kernel(const double* __restrict__ pos, const int* __re
   buf[3 * k + 2] = p.z;
 }
 
+__global__ void halo_pack_planar_kernel(const double* __restrict__ pl, int64_t ps,
+                                        const int* __restrict__ rows, int64_t m,
+                                        double* __restrict__ buf) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int r = rows[k];
+  buf[3 * k] = pl[r];
+  buf[3 * k + 1] = pl[ps + r];
+  buf[3 * k + 2] = pl[2 * ps + r];
+}
+
 __global__ void halo_unpack_kernel(const double* __restrict__ buf, const int* __restrict__ rows,
                                    int64_t m, double* __restrict__ pos,
                                    double* __restrict__ planar, int64_t ps) {
@@ -150,9 +161,11 @@ __global__ void halo_unpack_kernel(const double* __restrict__ buf, const int* __
   if (k >= m) return;
   const int r = rows[k];
   const double x = buf[3 * k], y = buf[3 * k + 1], z = buf[3 * k + 2];
-  pos[4 * (int64_t)r] = x;
-  pos[4 * (int64_t)r + 1] = y;
-  pos[4 * (int64_t)r + 2] = z;
+  if (pos) {
+    pos[4 * (int64_t)r] = x;
+    pos[4 * (int64_t)r + 1] = y;
+    pos[4 * (int64_t)r + 2] = z;
+  }
   if (planar) {
     planar[r] = x;
     planar[ps + r] = y;
@@ -231,6 +244,14 @@ int pc_halo_pack(const double* d_pos, const int32_t* d_rows, int64_t m, double* 
   halo_pack_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(d_pos, d_rows, m,
                                                                                d_buf);
   return check_launch("pc_halo_pack");
+}
+
+int pc_halo_pack_planar(const double* d_planar, int64_t planar_stride, const int32_t* d_rows,
+                        int64_t m, double* d_buf, void* stream) {
+  if (m <= 0) return PC_OK;
+  halo_pack_planar_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_planar, planar_stride, d_rows, m, d_buf);
+  return check_launch("pc_halo_pack_planar");
 }
 
 int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double* d_pos,

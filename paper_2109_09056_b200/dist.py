@@ -98,6 +98,11 @@ class DomainEngine:
         self._tlist = None
         self._tplan = None
         self.tile_failures = 0
+        # tile path: the force epilogue also runs the next step's integrate
+        # block into pl_n / vel_n (as MDDriver); `_advanced` marks them valid,
+        # `_pos_stale` that pos4 xyz lags behind pl
+        self._advanced = False
+        self._pos_stale = False
         self._time = time_phases
         self.timer = _PhaseTimer()
         self._local_grid()
@@ -207,6 +212,8 @@ class DomainEngine:
             self.pl = torch.empty((3, self._ps), dtype=torch.float64, device=dev)
             self.pl[:, self.cap:] = float("nan")
             self.bpl = torch.empty_like(self.pl) if self.tile else None
+            self._pl_n = torch.empty_like(self.pl) if self.tile else None
+            self._vel_n = torch.empty_like(self.vel) if self.tile else None
         self._nblk = int(_lib.load().pc_lj_force_sell_partials(self.cap))
         self.partial = torch.zeros((self._nblk, 5), dtype=torch.float64, device=dev)
         self.diag = torch.zeros(5, dtype=torch.float64, device=dev)
@@ -230,8 +237,22 @@ class DomainEngine:
             self.timer.stop(phase, e0)
 
     # ---- phases --------------------------------------------------------------
+    def _sync_pos4(self):
+        """pos4 x, y, z <- pl (the fused integrate only writes pl)."""
+        if self._pos_stale:
+            call("pc_pos_from_planar", ptr(self.pl), self._ps, self.n_total, ptr(self.pos),
+                 stream())
+            self._pos_stale = False
+
     def integrate(self):
+        if self._advanced:          # done by the previous force epilogue
+            self.pl, self._pl_n = self._pl_n, self.pl
+            self.vel, self._vel_n = self._vel_n, self.vel
+            self._advanced = False
+            self._pos_stale = True
+            return
         e0 = self._t0()
+        self._sync_pos4()
         call("pc_kick_drift_wrap", ptr(self.pos), ptr(self.vel), self.cap, ptr(self.frc),
              self.cap, self.n_total, self._dtm, float(self.cfg.dt), self._gbox, ptr(self.pl),
              self._ps, stream())
@@ -255,6 +276,7 @@ class DomainEngine:
         """Drop ghosts, wrap (done in integrate), owners, stable grouping by
         owner; returns {dest: (m, 7) rows} for dest != self (decomp.py:77-99)."""
         e0 = self._t0()
+        self._sync_pos4()
         rows = self._owned_rows()
         if rows is not None:
             n = rows.numel()
@@ -509,7 +531,11 @@ class DomainEngine:
         for dst, rows in self.export_rows.items():
             m = rows.numel()
             buf = torch.empty((m, 3), dtype=torch.float64, device=self.device)
-            call("pc_halo_pack", ptr(self.pos), ptr(rows), m, ptr(buf), stream())
+            if self.pl is not None:
+                call("pc_halo_pack_planar", ptr(self.pl), self._ps, ptr(rows), m, ptr(buf),
+                     stream())
+            else:
+                call("pc_halo_pack", ptr(self.pos), ptr(rows), m, ptr(buf), stream())
             out[dst] = buf
         self._t1("halo", e0)
         return out
@@ -532,8 +558,9 @@ class DomainEngine:
             call("pc_tile_force", ptr(self.pl), self._ps, self._ntiles, ptr(self._tplan),
                  ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._gbox,
                  self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
-                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag), None,
-                 None, 0.0, 0.0, stream())
+                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
+                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), stream())
+            self._advanced = True
         else:
             call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self._ps, self.n_total,
                  ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
@@ -589,6 +616,7 @@ class DomainEngine:
 
     def owned_state(self):
         """(gid, x, v) of owned rows (host numpy)."""
+        self._sync_pos4()
         n = self.n_total
         g = self.is_ghost[:n].cpu().numpy().astype(bool)
         p = self.pos[:n].cpu().numpy()
@@ -713,14 +741,20 @@ class NCCLTransport:
         self.dist.all_gather(allc, send, group=self.group)
         return torch.stack(allc).cpu().numpy()        # [src, dst]
 
-    def exchange(self, outbox, width, device, dtype=torch.float64):
-        c = self.counts(outbox, device)
+    def exchange(self, outbox, width, device, dtype=torch.float64, recv_counts=None):
+        """recv_counts ({src: rows}, e.g. the ghost blocks of the current halo
+        plan for the per-step refresh) skips the counts all_gather."""
+        c = self.counts(outbox, device) if recv_counts is None else None
         ops, inbox = [], {}
         for peer in range(self.world):
             if peer == self.rank:
                 continue
-            m_out = int(c[self.rank, peer])
-            m_in = int(c[peer, self.rank])
+            if c is None:
+                m_out = int(outbox[peer].shape[0]) if peer in outbox else 0
+                m_in = int(recv_counts.get(peer, 0))
+            else:
+                m_out = int(c[self.rank, peer])
+                m_in = int(c[peer, self.rank])
             if m_out:
                 ops.append(self.dist.P2POp(self.dist.isend,
                                            self._wire(outbox[peer].contiguous()), peer,
@@ -806,7 +840,10 @@ class DistMD(_StepLogic):
 
     def _exchange(self, out_name, in_name, width):
         out = getattr(self.engine, out_name)()
-        inbox = self.transport.exchange(out, width, self.device)
+        recv = None
+        if out_name == "refresh_out":   # sizes fixed by the halo plan until the next rebuild
+            recv = {src: int(rows.numel()) for src, rows in self.engine.ghost_blocks}
+        inbox = self.transport.exchange(out, width, self.device, recv_counts=recv)
         getattr(self.engine, in_name)(inbox)
 
     def diagnostics(self):

@@ -42,6 +42,12 @@ def _worker(rank, world, port, q):
             out.pop(0, None)          # a rank that sends nothing to rank 0
         inbox = t.exchange(out, 3, torch.device("cpu"))
         got = {s: b.numpy().copy() for s, b in inbox.items()}
+        # the per-step ghost refresh path: receive sizes known, no counts round
+        recv = {s: b.shape[0] for s, b in inbox.items()}
+        again = t.exchange(out, 3, torch.device("cpu"), recv_counts=recv)
+        assert sorted(again) == sorted(inbox)
+        for s_ in again:
+            assert torch.equal(again[s_], inbox[s_])
         red = t.allreduce(torch.tensor([float(rank), 1.0], dtype=torch.float64))
         q.put((rank, got, red.numpy().copy()))
     finally:
