@@ -197,6 +197,24 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
                       const double* d_posb, const pc_box* box_exact,
                       int32_t half /* keep one entry per unordered pair (Newton 3) */);
 
+/* ---- Ewald real-space pass (pc_longrange.cu) ------------------------------ */
+/* Replaces ref longrange.py:47-72 (_real_space) over a pair list (the half
+ * Verlet list of longrange.spme, longrange.py:142-146, expanded to (i, j)):
+ * dx = x[j] - x[i] with the exact minimum image on periodic axes, r^2 in the
+ * einsum order, pairs with r^2 < r_cut^2 contribute E = q_i q_j erfc(alpha r)/r
+ * and f[j] += s dx, f[i] -= s dx, s = q_i q_j (erfc(alpha r)/r^2 +
+ * 2 alpha/sqrt(pi) exp(-(alpha r)^2)/r)/r (FP64 atomics; d_f (n, 3) zeroed by
+ * the caller).  d_epart gets pc_ewald_real_blocks(npairs) energy partials;
+ * d_flag bit 4: a selected pair with r < 1e-10 (ValueError in the ref). */
+int64_t pc_ewald_real_blocks(int64_t npairs);
+/* Row index of every CSR entry (ref VerletList.pairs, neighbors.py:39-46):
+ * d_pi[k] = i for k in [offsets[i], offsets[i+1]). */
+int pc_csr_pairs(const int64_t* d_offsets, int32_t n, int32_t* d_pi, void* stream);
+int pc_ewald_real_pairs(const double* d_x, const double* d_q, const int32_t* d_pi,
+                        const int32_t* d_pj, int64_t npairs, const pc_box* box, double alpha,
+                        double r_cut, double* d_f, double* d_epart, int32_t* d_flag,
+                        void* stream);
+
 /* ---- tile-staged MD hot path (pc_tile.cu) -------------------------------- */
 /* MD-engine replacement of ref neighbors.py:49-97 (Verlet build) +
  * md.py:99-126 (forces) + md.py:251-257 (final half kick) for a 3-D box with

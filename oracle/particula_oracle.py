@@ -347,6 +347,43 @@ def lj_forces(x, ids, owned, pair_i, pair_j, length, periodic, eps, sigma,
     return forces, pe
 
 
+# ---------------------------------------------------------------------------
+# Ewald real-space pass (ref: longrange.py) -- SURVEY §8(f3), the only other
+# consumer of the half Verlet list.  erfc is scipy.special.erfc, the
+# reference's own third-party dependency (longrange.py:14; scipy 1.18.1 here).
+# ---------------------------------------------------------------------------
+
+
+def ewald_real_space(x, q, length, alpha, r_cut, pair_i=None, pair_j=None):
+    """erfc-screened Coulomb pair sum over half-list pairs (or all pairs)
+    -- ref longrange.py:47-72.  Returns (energy, forces)."""
+    from scipy.special import erfc
+    x = np.asarray(x, np.float64)
+    q = np.asarray(q, np.float64)
+    n = x.shape[0]
+    if pair_i is None:
+        ii, jj = np.triu_indices(n, k=1)
+    else:
+        ii, jj = np.asarray(pair_i, np.int64), np.asarray(pair_j, np.int64)
+    dx = x[jj] - x[ii]
+    dx -= length * np.round(dx / length)
+    r2 = sqnorm(dx)
+    sel = r2 < r_cut * r_cut
+    ii, jj, dx, r2 = ii[sel], jj[sel], dx[sel], r2[sel]
+    r = np.sqrt(r2)
+    if r.size and r.min() < 1e-10:
+        raise ValueError("overlapping charges in real-space sum")
+    qq = q[ii] * q[jj]
+    er = erfc(alpha * r)
+    energy = float(np.sum(qq * er / r))
+    mag = qq * (er / r2 + 2 * alpha / np.sqrt(np.pi) * np.exp(-(alpha * r) ** 2) / r)
+    fvec = (mag / r)[:, None] * dx
+    forces = np.zeros_like(x)
+    np.add.at(forces, jj, fvec)
+    np.add.at(forces, ii, -fvec)
+    return energy, forces
+
+
 def fcc_lattice(cells, spacing):
     """4-atom FCC basis on a cells^3 grid, ij meshgrid order -- ref md.py:67-74."""
     basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0],

@@ -11,7 +11,7 @@ from . import _lib  # noqa: F401  (fails loudly if the library is missing)
 
 _lib.load()
 
-from . import aosoa, binning, decomp, geometry, md, neighbors  # noqa: E402
+from . import aosoa, binning, decomp, geometry, longrange, md, neighbors  # noqa: E402
 
-__all__ = ["aosoa", "binning", "decomp", "geometry", "md", "neighbors"]
+__all__ = ["aosoa", "binning", "decomp", "geometry", "longrange", "md", "neighbors"]
 __version__ = "0.1.0"

@@ -51,6 +51,9 @@ constexpr int kSX = kBX + 2, kSY = kBY + 2, kSZ = kTZ + 2;
 constexpr int kSCols = kSX * kSY;
 constexpr int kSegs = kSCols * 3;
 constexpr int kNDummy = 16;
+#ifndef PC_FORCE_SLEEP
+#define PC_FORCE_SLEEP 64
+#endif
 #ifndef PC_FORCE_WARPS
 #define PC_FORCE_WARPS 32
 #endif
@@ -1042,7 +1045,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       for (int q = 0; q < kNBuf; ++q)
         if (F.seq[q] == k) bsel = q;
       if (bsel >= 0) break;
-      __nanosleep(64);
+      __nanosleep(PC_FORCE_SLEEP);
     }
     __threadfence_block();
     mbar_wait(&F.bar[bsel], (uint32_t)F.par[bsel]);

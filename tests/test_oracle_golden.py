@@ -197,3 +197,23 @@ def test_md_c1_series_bit_exact(oracle):
     got = np.array([[r["KE"], r["PE"], r["E_total"], r["temperature"]]
                     for r in rows])
     assert np.array_equal(got, MD["c1_series"][:21])
+
+
+EW = load_flat("ewald.npz")
+
+
+@pytest.mark.parametrize("name", ["rand400", "nacl216"])
+def test_ewald_real_space_bit_exact(oracle, name):
+    """Oracle real-space pass == the reference's _real_space (longrange.py:47-72),
+    on the reference's half-list pairs and on all pairs."""
+    g = lambda k: EW[f"{name}_{k}"]  # noqa: E731
+    e, f = oracle.ewald_real_space(g("x"), g("q"), float(g("L")), float(g("alpha")),
+                                   float(g("rcut")), g("pi"), g("pj"))
+    assert e == float(g("energy"))
+    assert np.array_equal(f, g("forces"))
+    e2, f2 = oracle.ewald_real_space(g("x"), g("q"), float(g("L")), float(g("alpha")),
+                                     float(g("rcut")))
+    assert e2 == float(g("energy_all"))
+    assert np.array_equal(f2, g("forces_all"))
+    # the half list covers every pair within r_cut: same physics either way
+    assert abs(e - e2) <= 1e-12 * abs(e2)
