@@ -484,3 +484,31 @@ def test_md_engine_forces_vs_oracle(pc, oracle, cells, temp, steps):
     assert np.abs(f.sum(0)).max() < 1e-9
     d = drv.diagnostics()
     assert abs(d["PE"] - peref.sum()) <= ENERGY_TOL * abs(peref.sum())
+
+
+def test_md_engine_empty_tiles(pc, oracle):
+    """A lattice at the usual density filling half the box volume (a corner
+    cube; the rest vacuum): whole tiles have no rows (28^3 cells: ~5 tiles per
+    CTA, many empty).  The staging ring must pass over them (they are never
+    waited on) and the forces must match the oracle's on the tile path."""
+    import torch
+    cells = 28
+    a = (4.0 / 0.8442) ** (1.0 / 3.0)
+    x = pc.md.fcc_lattice(cells, a)
+    v = pc.md.initial_velocities(x.shape[0], 1.44, 1.0, 3)
+    cfg = pc.md.MDConfig(lattice_cells=cells, density=0.4221, temperature=1.44, cutoff=2.5,
+                         skin=0.3, rebuild_stride=10, seed=3, steps=0)
+    drv = pc.md.MDDriver(cfg, state=(x, v))
+    assert drv.mode == "tile"
+    assert x.max() + 2.8 < drv.box.high[0]          # vacuum wider than the search radius
+    for s in range(1, 16):
+        drv.step(s)
+    xs, _ = drv.gather_state()
+    ids = drv.pos[: drv.n, 3].contiguous().view(torch.int64).cpu().numpy()
+    f = np.empty((drv.n, 3))
+    f[ids] = drv.frc[:, : drv.n].cpu().numpy().T
+    pi, pj = oracle.neighbor_pairs(xs, drv.box.low, drv.box.high, [True] * 3, 2.5 * 1.0000001)
+    fref, _ = oracle.lj_forces(xs, np.arange(drv.n), drv.n, pi, pj, drv.box.lengths,
+                               [True] * 3, 1.0, 1.0, 2.5)
+    assert force_err_ratio(f, fref) < 1.0
+    assert drv.tile_failures == 0
