@@ -720,6 +720,13 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st,
 __device__ __forceinline__ int ring_alloc(ForceShared& F, const int* __restrict__ sz) {
   const int k0 = F.issued;
   for (;;) {
+    // release finished tiles in order first (tiles without rows finish at
+    // allocation: a run of them must not fill the window of kRing)
+    while (F.released < F.issued && F.fin[F.released & (kRing - 1)]) {
+      const int e = F.end_v[F.released & (kRing - 1)];
+      if (e >= 0) F.tail_v = e;
+      F.released += 1;
+    }
     const int k = F.issued;
     if (k >= F.K || k - F.released >= kRing) break;
     const int q = k & (kRing - 1);
@@ -790,11 +797,6 @@ __device__ void ring_release(ForceShared& F, double* __restrict__ ring, int k,
     while (atomicCAS(&F.lock, 0, 1) != 0) __nanosleep(32);
     __threadfence_block();
     F.fin[k & (kRing - 1)] = 1;
-    while (F.released < F.issued && F.fin[F.released & (kRing - 1)]) {
-      const int e = F.end_v[F.released & (kRing - 1)];
-      if (e >= 0) F.tail_v = e;
-      F.released += 1;
-    }
     k0 = ring_alloc(F, sz);
     k1 = F.issued;
     __threadfence_block();
