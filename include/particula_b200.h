@@ -197,6 +197,21 @@ int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n, const int32_t* d_ce
                       const double* d_posb, const pc_box* box_exact,
                       int32_t half /* keep one entry per unordered pair (Newton 3) */);
 
+/* ---- device neighbor traversal consumers (pc_traverse.cu) ----------------- */
+/* Built on include/particula_b200_traverse.cuh (for_each_neighbor /
+ * for_each_neighbor2 as device functors, ref neighbors.py:137-154) over a CSR
+ * list (int64 offsets, int32 index), rows [begin, end), team != 0: one warp
+ * per row.  d_x (n, 3) f64; the minimum image on box's periodic axes.
+ * coordination: d_out[i] += #{stored j : |x_j - x_i|^2 < r_inner^2};
+ * angle_sum (full list): d_out[i] += sum over stored pairs j before k of
+ * cos(angle j-i-k).  d_out (n) zeroed by the caller. */
+int pc_traverse_coordination(const double* d_x, const pc_box* box, const int64_t* d_offsets,
+                             const int32_t* d_index, int32_t n, int32_t begin, int32_t end,
+                             double r_inner, int32_t team, double* d_out, void* stream);
+int pc_traverse_angle_sum(const double* d_x, const pc_box* box, const int64_t* d_offsets,
+                          const int32_t* d_index, int32_t n, int32_t begin, int32_t end,
+                          int32_t team, double* d_out, void* stream);
+
 /* ---- Ewald real-space pass (pc_longrange.cu) ------------------------------ */
 /* Replaces ref longrange.py:47-72 (_real_space) over a pair list (the half
  * Verlet list of longrange.spme, longrange.py:142-146, expanded to (i, j)):

@@ -112,6 +112,10 @@ SIGNATURES = {
     "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
                                      ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_vp]),
+    "pc_traverse_coordination": (ctypes.c_int, [c_vp, ctypes.POINTER(PcBox), c_vp, c_vp, c_i32,
+                                                c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp]),
+    "pc_traverse_angle_sum": (ctypes.c_int, [c_vp, ctypes.POINTER(PcBox), c_vp, c_vp, c_i32,
+                                             c_i32, c_i32, c_i32, c_vp, c_vp]),
     "pc_ewald_real_blocks": (c_i64, [c_i64]),
     "pc_csr_pairs": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
     "pc_ewald_real_pairs": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(PcBox),

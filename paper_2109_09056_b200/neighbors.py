@@ -209,3 +209,47 @@ def for_each_neighbor2(vlist: VerletList, i_range, kernel) -> None:
         for a in range(js.size):
             for b in range(a + 1, js.size):
                 kernel(i, int(js[a]), int(js[b]))
+
+
+# ---- device functor traversals (include/particula_b200_traverse.cuh) -------
+# the GPU form of for_each_neighbor / for_each_neighbor2 is a
+# C++ device functor (a Python callable cannot run on the device); these two
+# consumers ship with the library and back the parity tests.
+
+
+def _traverse_args(vlist: VerletList, positions, box: Box, periodic, i_range):
+    x = _kernels.as_device(positions).to(torch.float64).contiguous()
+    if x.dim() != 2 or x.shape[1] != 3:
+        raise ValueError("positions must be (n, 3)")
+    counts, offsets, index = vlist.device_csr()
+    n = int(counts.numel())
+    if x.shape[0] != n:
+        raise ValueError("positions and neighbor list sizes differ")
+    begin, end = (0, n) if i_range is None else (int(i_range[0]), int(i_range[1]))
+    per = np.broadcast_to(np.asarray(periodic, bool), (3,))
+    pbox = _lib.make_box(box.low, box.high, per)
+    out = torch.zeros(max(n, 1), dtype=torch.float64, device=x.device)
+    return x, pbox, offsets, index, n, begin, end, out
+
+
+def coordination(vlist: VerletList, positions, box: Box, periodic, r_inner: float,
+                 i_range=None, team: bool = False) -> np.ndarray:
+    """Per-row count of stored neighbors closer than r_inner (for_each_neighbor
+    with a device pair functor; one thread or one warp per row)."""
+    x, pbox, off, idx, n, b, e, out = _traverse_args(vlist, positions, box, periodic, i_range)
+    call("pc_traverse_coordination", ptr(x), pbox, ptr(off), ptr(idx), n, b, e,
+         float(r_inner), int(team), ptr(out), stream())
+    return out[:n].cpu().numpy()
+
+
+def angle_sums(vlist: VerletList, positions, box: Box, periodic, i_range=None,
+               team: bool = False) -> np.ndarray:
+    """Per-row sum of cos(angle j-i-k) over pairs of stored neighbors j before
+    k (for_each_neighbor2 with a device three-body functor; full lists only,
+    as ref neighbors.py:148-149)."""
+    if vlist.half_or_full != "full":
+        raise ValueError("second-level traversal requires a full list")
+    x, pbox, off, idx, n, b, e, out = _traverse_args(vlist, positions, box, periodic, i_range)
+    call("pc_traverse_angle_sum", ptr(x), pbox, ptr(off), ptr(idx), n, b, e, int(team),
+         ptr(out), stream())
+    return out[:n].cpu().numpy()
