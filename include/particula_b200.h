@@ -230,6 +230,24 @@ int pc_ewald_real_pairs(const double* d_x, const double* d_q, const int32_t* d_p
                         double r_cut, double* d_f, double* d_epart, int32_t* d_flag,
                         void* stream);
 
+/* ---- deterministic mode ------------------------------------ */
+/* pc_sell_sort_by_tag: order every row of a SELL list (pc_nbr_build_sell) by
+ * the neighbours' global ids (int64 tags in d_pos4 .w), so each atom's pair
+ * terms accumulate in one order under any decomposition (rows > 256 entries
+ * set flag bit 2).  pc_lj_force_sell_atoms: pc_lj_force_sell writing one
+ * (KE, PE, px, py, pz) row per atom to d_atom (n_rows x 5) instead of per-warp
+ * partials; the caller scatters owned rows by global id and reduces them in
+ * id order (pc_scatter_rows + pc_reduce_partials): energy series bitwise
+ * equal for any rank grid (ref test_acceptance.py:79-92, criterion 3). */
+int pc_sell_sort_by_tag(const double* d_pos4, int32_t n, const int32_t* d_count,
+                        int32_t* d_index, int32_t width, int32_t* d_flag, void* stream);
+int pc_lj_force_sell_atoms(const double* d_pos, const double* d_planar, int64_t planar_stride,
+                           int32_t n_rows, const int32_t* d_count, const int32_t* d_index,
+                           int32_t width, const pc_box* box, const pc_lj* lj, double mi_guard,
+                           double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
+                           double dtm, double mass, double* d_atom, int32_t* d_flag,
+                           void* stream);
+
 /* ---- tile-staged MD hot path (pc_tile.cu) -------------------------------- */
 /* MD-engine replacement of ref neighbors.py:49-97 (Verlet build) +
  * md.py:99-126 (forces) + md.py:251-257 (final half kick) for a 3-D box with

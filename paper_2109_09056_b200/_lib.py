@@ -116,6 +116,11 @@ SIGNATURES = {
                                                 c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp]),
     "pc_traverse_angle_sum": (ctypes.c_int, [c_vp, ctypes.POINTER(PcBox), c_vp, c_vp, c_i32,
                                              c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "pc_sell_sort_by_tag": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "pc_lj_force_sell_atoms": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32,
+                                              ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl,
+                                              c_vp, c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp,
+                                              c_vp]),
     "pc_ewald_real_blocks": (c_i64, [c_i64]),
     "pc_csr_pairs": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
     "pc_ewald_real_pairs": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(PcBox),

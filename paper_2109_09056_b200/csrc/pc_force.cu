@@ -278,7 +278,7 @@ __device__ __forceinline__ void sell_row(const double* __restrict__ pos,
   }
 }
 
-template <bool PLANAR>
+template <bool PLANAR, bool ATOM = false>
 __global__ void __launch_bounds__(kForceThreads, PLANAR ? 2 : 3)
 lj_force_sell_kernel(const double* __restrict__ pos, const double* __restrict__ pl, int64_t ps,
                      int n_rows, const int* __restrict__ count,
@@ -332,7 +332,14 @@ lj_force_sell_kernel(const double* __restrict__ pos, const double* __restrict__ 
       pz = mass * vz;
     }
   }
-  if (partial) {
+  if (ATOM) {
+    // deterministic mode: one (KE, PE, px, py, pz) row per atom, reduced by
+    // the caller in global-id order
+    if (live) {
+      double* o = partial + (int64_t)i * 5;
+      o[0] = ke; o[1] = pe; o[2] = px; o[3] = py; o[4] = pz;
+    }
+  } else if (partial) {
     // per-warp partials: no block barrier, so fast warps retire early
     ke = warp_sum(ke);
     pe = warp_sum(pe);
@@ -500,6 +507,24 @@ int pc_lj_force_sell(const double* d_pos, const double* d_planar, int64_t planar
         width / 4, *box, c, mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial,
         d_flag);
   return check_launch("pc_lj_force_sell");
+}
+
+int pc_lj_force_sell_atoms(const double* d_pos, const double* d_planar, int64_t planar_stride,
+                           int32_t n_rows, const int32_t* d_count, const int32_t* d_index,
+                           int32_t width, const pc_box* box, const pc_lj* lj, double mi_guard,
+                           double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
+                           double dtm, double mass, double* d_atom, int32_t* d_flag,
+                           void* stream) {
+  if (n_rows < 0 || width % 4 || !d_atom || !d_planar) {
+    set_error("pc_lj_force_sell_atoms: bad rows/width or missing planar/atom arrays");
+    return PC_ERR_VALUE;
+  }
+  LJConst c = make_const(lj);
+  unsigned blocks = (unsigned)pc_lj_force_blocks(n_rows);
+  lj_force_sell_kernel<true, true><<<blocks, kForceThreads, 0, as_stream(stream)>>>(
+      d_pos, d_planar, planar_stride, n_rows, d_count, reinterpret_cast<const int4*>(d_index),
+      width / 4, *box, c, mi_guard, d_f3, f_stride, d_v, v_stride, dtm, mass, d_atom, d_flag);
+  return check_launch("pc_lj_force_sell_atoms");
 }
 
 int pc_lj_force_sell_half(const double* d_pos, int32_t n_rows, const int32_t* d_count,

@@ -369,6 +369,54 @@ namespace pc {
 static int g_stage_bytes = 0;
 }
 
+// Deterministic mode: order every SELL row by the neighbours'
+// global ids (the tag in pos4.w), so a row's pair terms are accumulated in
+// the same order under any decomposition or cell order.  Warp per row: tags
+// into shared memory, rank = number of smaller tags (ids in a row are
+// distinct), scatter back.
+constexpr int kSortRowCap = 256;
+
+__global__ void __launch_bounds__(256)
+sell_sort_by_tag_kernel(const double* __restrict__ pos, int n, const int* __restrict__ count,
+                        int* __restrict__ nbr, int Q, int* __restrict__ flag) {
+  __shared__ long long tag[8][kSortRowCap];
+  __shared__ int idx[8][kSortRowCap];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + w;
+  if (i >= n) return;
+  const int m = count[i];
+  if (m > kSortRowCap) {
+    if (lane == 0) atomicOr(flag, kFlagOverflow);
+    return;
+  }
+  for (int e = lane; e < m; e += 32) {
+    const int j = nbr[sell_word(i, e, Q)];
+    idx[w][e] = j;
+    tag[w][e] = tag_of(pos[4 * (int64_t)j + 3]);
+  }
+  __syncwarp();
+  for (int e = lane; e < m; e += 32) {
+    const long long t = tag[w][e];
+    int r = 0;
+    for (int u = 0; u < m; ++u) r += tag[w][u] < t;
+    nbr[sell_word(i, r, Q)] = idx[w][e];
+  }
+}
+
+extern "C" int pc_sell_sort_by_tag(const double* d_pos, int32_t n, const int32_t* d_count,
+                                   int32_t* d_index, int32_t width, int32_t* d_flag,
+                                   void* stream) {
+  using namespace pc;
+  if (n <= 0) return PC_OK;
+  if (width % 4) {
+    set_error("pc_sell_sort_by_tag: width must be a multiple of 4");
+    return PC_ERR_VALUE;
+  }
+  sell_sort_by_tag_kernel<<<(n + 7) / 8, 256, 0, as_stream(stream)>>>(d_pos, n, d_count, d_index,
+                                                                    width / 4, d_flag);
+  return check_launch("pc_sell_sort_by_tag");
+}
+
 extern "C" int pc_nbr_build_sell(const double* d_pos_sorted, int32_t n,
                                  const int32_t* d_cell_start, const pc_grid* grid,
                                  const pc_box* box, double cutoff2, int32_t width,

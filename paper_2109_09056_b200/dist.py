@@ -69,7 +69,7 @@ class DomainEngine:
 
     def __init__(self, cfg: MDConfig, fabric: DomainFabric, rank: int, x, v, gid, device,
                  ell_width: int = 128, planar_gather: bool = True, time_phases: bool = False,
-                 tile: bool = True):
+                 tile: bool = True, deterministic: bool = False):
         self.cfg = cfg
         self.fabric = fabric
         self.rank = rank
@@ -87,6 +87,11 @@ class DomainEngine:
         self._search2 = self.search * self.search
         self._mi_guard = float(cfg.cutoff) * (1.0 + 1e-6) + 1e-9
         self.ell_width = -(-int(ell_width) // 4) * 4
+        # deterministic mode: SELL rows in global-id order and
+        # per-atom energy rows, reduced in id order by the driver
+        self.deterministic = bool(deterministic)
+        if self.deterministic:
+            tile, planar_gather = False, True
         self.planar_gather = planar_gather or tile
         # tile path (pc_tile.cu, as the single-domain engine): local grid,
         # binpos-staged FP32 prefilter, raw positions + global minimum image
@@ -482,6 +487,11 @@ class DomainEngine:
             self.nbr = torch.empty(slices * self.ell_width * 32, dtype=torch.int32,
                                    device=self.device)
         self.cnt[:n] *= (1 - self.is_ghost[:n])          # ghost rows carry no list
+        if self.deterministic:
+            call("pc_sell_sort_by_tag", ptr(self.pos), n, ptr(self.cnt), ptr(self.nbr),
+                 self.ell_width, ptr(self.build_flag), s)
+            if int(self.build_flag[0].item()) & _lib.FLAG_OVERFLOW:
+                raise RuntimeError("deterministic mode: a Verlet row exceeds 256 entries")
         self.used_staged = bool(used.value)
         self.rebuilds += 1
         self._t1("neighbor", e0)
@@ -561,6 +571,14 @@ class DomainEngine:
                  float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
                  ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), stream())
             self._advanced = True
+        elif self.deterministic:
+            if getattr(self, "_atom", None) is None or self._atom.shape[0] < self.cap:
+                self._atom = torch.zeros((self.cap, 5), dtype=torch.float64, device=self.device)
+            call("pc_lj_force_sell_atoms", ptr(self.pos), ptr(self.pl), self._ps, self.n_total,
+                 ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
+                 self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self._atom), ptr(self.flag),
+                 stream())
         else:
             call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl), self._ps, self.n_total,
                  ptr(self.cnt), ptr(self.nbr), self.ell_width, self._gbox, self._lj,
@@ -577,6 +595,16 @@ class DomainEngine:
             int(_lib.load().pc_lj_force_sell_partials(self.n_total))
         call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
         return self.diag
+
+    def scatter_atom_rows(self, dst, n_global):
+        """Deterministic mode: this rank's per-atom (KE, PE, px, py, pz) rows
+        into dst (n_global + 1, 5) at their global ids (ghost rows -> the
+        dump row n_global)."""
+        n = self.n_total
+        gid = self.pos[:n, 3].contiguous().view(torch.int64)
+        tgt = torch.where(self.is_ghost[:n] != 0, torch.full_like(gid, n_global), gid)
+        tgt = tgt.to(torch.int32).contiguous()
+        call("pc_scatter_rows", ptr(self._atom), ptr(dst), ptr(tgt), n, 40, stream())
 
     def mean_neighbors(self) -> float:
         """Mean Verlet-list length over owned rows (ghost rows are empty)."""
@@ -625,6 +653,12 @@ class DomainEngine:
         return ids[~g], p[~g, :3], v[~g]
 
 
+def _diag_dict(t, n):
+    ke, pe = float(t[0]), float(t[1])
+    return {"KE": ke, "PE": pe, "E_total": ke + pe, "temperature": 2.0 * ke / (3.0 * n),
+            "momentum": t[2:5].copy()}
+
+
 def _route(outboxes):
     """In-process delivery: inbox[dst][src] = outbox[src][dst]."""
     inboxes = [dict() for _ in outboxes]
@@ -664,8 +698,10 @@ class FabricMD(_StepLogic):
     reference's in-process fabric (md.py MDDriver with rank_dims), with GPU
     kernels doing every data-sized step."""
 
-    def __init__(self, cfg: MDConfig, device=None, tile: bool = True):
+    def __init__(self, cfg: MDConfig, device=None, tile: bool = True,
+                 deterministic: bool = False):
         cfg.validate()
+        self.deterministic = bool(deterministic)
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
         self.box = Box(np.zeros(3), np.full(3, cfg.lattice_cells * a))
@@ -680,12 +716,13 @@ class FabricMD(_StepLogic):
         self.engines = []
         for r in range(self.fabric.n_ranks):
             if r == 0:
-                self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev, tile=tile))
+                self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev, tile=tile,
+                                                 deterministic=deterministic))
             else:
                 z = torch.zeros((0, 3), dtype=torch.float64)
                 self.engines.append(DomainEngine(cfg, self.fabric, r, z, z,
                                                  torch.zeros(0, dtype=torch.int64), dev,
-                                                 tile=tile))
+                                                 tile=tile, deterministic=deterministic))
         self._init_forces()
 
     def _engines(self):
@@ -697,6 +734,14 @@ class FabricMD(_StepLogic):
             getattr(e, in_name)(inbox)
 
     def diagnostics(self):
+        if self.deterministic:          # per-atom rows in global-id order, one tree
+            g = torch.zeros((self.n + 1, 5), dtype=torch.float64, device=self.engines[0].device)
+            for e in self.engines:
+                if e.n_total:
+                    e.scatter_atom_rows(g, self.n)
+            d = torch.zeros(5, dtype=torch.float64, device=g.device)
+            call("pc_reduce_partials", ptr(g), self.n, ptr(d), stream())
+            return _diag_dict(d.cpu().numpy(), self.n)
         tot = sum(e.local_diagnostics().cpu().numpy() for e in self.engines)
         ke, pe = float(tot[0]), float(tot[1])
         return {"KE": ke, "PE": pe, "E_total": ke + pe,
@@ -783,7 +828,8 @@ class DistMD(_StepLogic):
     """One rank per GPU under torch.distributed (launch with torchrun)."""
 
     def __init__(self, cfg: MDConfig, cells=None, transport=None, device=None,
-                 local_init: bool = False, time_phases: bool = False):
+                 local_init: bool = False, time_phases: bool = False,
+                 deterministic: bool = False):
         import torch.distributed as dist
         cfg.validate()
         self.cfg = cfg
@@ -800,8 +846,9 @@ class DistMD(_StepLogic):
         self._dtm = 0.5 * cfg.dt / cfg.mass
         self.device = torch.device(device) if device is not None else _lib.device()
         x, v, ids = self._initial(cells, a, rank, local_init)
+        self.deterministic = bool(deterministic)
         self.engine = DomainEngine(cfg, self.fabric, rank, x, v, ids, self.device,
-                                   time_phases=time_phases)
+                                   time_phases=time_phases, deterministic=deterministic)
         self._init_forces()
         del dist
 
@@ -847,6 +894,16 @@ class DistMD(_StepLogic):
         getattr(self.engine, in_name)(inbox)
 
     def diagnostics(self):
+        if self.deterministic:
+            # every rank scatters its owned rows into the global id-ordered
+            # array; the sum over ranks is exact (one nonzero per entry)
+            g = torch.zeros((self.n + 1, 5), dtype=torch.float64, device=self.device)
+            if self.engine.n_total:
+                self.engine.scatter_atom_rows(g, self.n)
+            self.transport.allreduce(g)
+            d = torch.zeros(5, dtype=torch.float64, device=self.device)
+            call("pc_reduce_partials", ptr(g), self.n, ptr(d), stream())
+            return _diag_dict(d.cpu().numpy(), self.n)
         d = self.engine.local_diagnostics().clone()
         self.transport.allreduce(d)
         t = d.cpu().numpy()

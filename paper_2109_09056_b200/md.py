@@ -194,8 +194,14 @@ class MDDriver:
 
     def __init__(self, cfg: MDConfig, device=None, ell_width: int = 128,
                  time_phases: bool = True, state=None, planar_gather: bool = True,
-                 tile: bool = True, half_list: bool = False):
+                 tile: bool = True, half_list: bool = False, deterministic: bool = False):
         cfg.validate()
+        # deterministic mode: SELL rows in global-id order,
+        # per-atom energies reduced in id order -- bitwise equal to FabricMD /
+        # DistMD(deterministic=True) on any rank grid
+        self.deterministic = bool(deterministic)
+        if self.deterministic:
+            tile, half_list = False, False
         self.cfg = cfg
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
         self.box = cube(cfg.lattice_cells * a)
@@ -369,6 +375,12 @@ class MDDriver:
             self.ell_width = -(-(int(self.cnt[:n].max().item()) + 8) // 4) * 4
             self.nbr = self._new_nbr()
         self.used_staged = bool(used.value)
+        if self.deterministic:
+            call("pc_sell_sort_by_tag", ptr(self.pos), n, ptr(self.cnt), ptr(self.nbr),
+                 self.ell_width, ptr(self.build_flag), s)
+            if int(self.build_flag[0].item()) & _lib.FLAG_OVERFLOW:
+                raise RuntimeError("deterministic mode: a Verlet row exceeds 256 entries")
+            self._gid32 = self.pos[:n, 3].contiguous().view(torch.int64).to(torch.int32)
 
     def _tile_build(self, cell_start) -> bool:
         """Issue the tile round-list build (pc_tile.cu) without a host sync.
@@ -456,6 +468,15 @@ class MDDriver:
             call("pc_lj_force_sell_half", ptr(self.pos), self.n, ptr(self.cnt), ptr(self.nbr),
                  self.ell_width, self._pbox, self._lj, self._mi_guard, ptr(self.frc), self.cap,
                  ptr(self.partial), ptr(self.flag), stream())
+        elif self.deterministic:
+            if getattr(self, "_atom", None) is None:
+                self._atom = torch.zeros((self.n, 5), dtype=torch.float64, device=self.device)
+                self._atom_g = torch.zeros_like(self._atom)
+            call("pc_lj_force_sell_atoms", ptr(self.pos), ptr(self.pl), self._ps, self.n,
+                 ptr(self.cnt), ptr(self.nbr), self.ell_width, self._pbox, self._lj,
+                 self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
+                 float(kick_dtm), float(self.cfg.mass), ptr(self._atom), ptr(self.flag),
+                 stream())
         else:
             call("pc_lj_force_sell", ptr(self.pos), ptr(self.pl) if self.planar_gather else None,
                  self._ps, self.n,
@@ -506,6 +527,14 @@ class MDDriver:
     # -- diagnostics --------------------------------------------------------
     def device_diagnostics(self) -> torch.Tensor:
         """(KE, PE, px, py, pz) on the device, no host sync."""
+        if self.deterministic:
+            if not self._ke_fresh:   # per-atom rows again (v unchanged: zero kick)
+                self._force(0.0)
+            # per-atom rows in global-id order, one fixed reduction tree
+            call("pc_scatter_rows", ptr(self._atom), ptr(self._atom_g), ptr(self._gid32),
+                 self.n, 40, stream())
+            call("pc_reduce_partials", ptr(self._atom_g), self.n, ptr(self.diag), stream())
+            return self.diag
         if not self._ke_fresh:       # velocities changed outside a force pass
             call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n, 0.0,
                  float(self.cfg.mass), ptr(self.partial_k), stream())

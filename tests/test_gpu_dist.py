@@ -94,3 +94,24 @@ def test_fabric_ghost_lists_match_global(pc, oracle, tile):
             assert np.array_equal(np.sort(gid[nb[a]]), rows[gid[a]])
             seen += 1
     assert seen == fab.n
+
+
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2)])
+def test_deterministic_mode_bitwise(pc, dims):
+    """SURVEY §8 f2 (GPU analogue of ref test_acceptance.py:79-92): with
+    deterministic=True (Verlet rows in global-id order, per-atom energies
+    reduced in id order) the decomposed run's energy series and trajectory
+    are bitwise equal to the single-domain run's."""
+    kw = dict(lattice_cells=6, density=0.8442, temperature=1.44, cutoff=2.5, skin=0.3,
+              rebuild_stride=5, seed=1, steps=0)
+    one = pc.md.MDDriver(pc.md.MDConfig(**kw), deterministic=True)
+    fab = pc.dist.FabricMD(pc.md.MDConfig(**dict(kw, rank_dims=dims)), deterministic=True)
+    assert one.mode == "sell" and all(e.mode == "sell" for e in fab.engines)
+    a, b = _run(one, 25), _run(fab, 25)
+    assert np.array_equal(a, b)
+    xa, va = one.gather_state()
+    xb, vb = fab.gather_state()
+    assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+    # and the physics is the reference's
+    ref = _run(pc.md.MDDriver(pc.md.MDConfig(**kw), tile=False), 0)
+    assert abs(a[0] - ref[0]) <= 1e-10 * abs(ref[0])

@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, steps):
+def _worker(rank, world, port, q, steps, det=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -35,7 +35,7 @@ def _worker(rank, world, port, q, steps):
         torch.cuda.set_device(0)
         import paper_2109_09056_b200 as pc
         from paper_2109_09056_b200.dist import DistMD
-        drv = DistMD(pc.md.MDConfig(**KW))
+        drv = DistMD(pc.md.MDConfig(**KW), deterministic=det)
         es = [drv.diagnostics()["E_total"]]
         for s in range(1, steps + 1):
             drv.step(s)
@@ -69,3 +69,27 @@ def test_distmd_two_processes(world):
     assert owned == drv.n
     for _, es, _ in out:
         assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-6     # tile path: FP32 pair energies summed in slot order
+
+
+def test_distmd_deterministic_bitwise():
+    """Two processes, deterministic=True: energy series bitwise equal to the
+    single-domain deterministic run."""
+    import paper_2109_09056_b200 as pc
+    steps = 15
+    drv = pc.md.MDDriver(pc.md.MDConfig(**KW), deterministic=True)
+    ref = [drv.diagnostics()["E_total"]]
+    for s in range(1, steps + 1):
+        drv.step(s)
+        ref.append(drv.diagnostics()["E_total"])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, steps, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for _, es, _ in out:
+        assert np.array_equal(es, np.array(ref))
