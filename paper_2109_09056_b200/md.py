@@ -627,14 +627,16 @@ class MDDriver:
             self._timer.totals[k] = float(v)
 
 
-def run_md(cfg: MDConfig, state=None, time_phases: bool = True):
+def run_md(cfg: MDConfig, state=None, time_phases: bool = True, deterministic: bool = False):
     """Run the NVE loop; returns (per-step diagnostic rows, phase timings)
     (ref md.py:295-307).  The per-step energies are reduced on the device
     into a history buffer and read back once after the loop (the reference
     returns the rows only at the end as well), so the step loop never waits
     for the host.  An overlap detected in any step raises FloatingPointError
-    after the loop.  `state`: optional host (x, v) in global-id order."""
-    drv = MDDriver(cfg, state=state, time_phases=time_phases)
+    after the loop.  `state`: optional host (x, v) in global-id order.
+    `deterministic`: the id-ordered engine, bitwise equal to
+    FabricMD / DistMD(deterministic=True) on any rank grid."""
+    drv = MDDriver(cfg, state=state, time_phases=time_phases, deterministic=deterministic)
     drv.timings = {k: 0.0 for k in PHASES}
     hist = torch.empty((cfg.steps + 1, 5), dtype=torch.float64, device=drv.device)
     hist[0].copy_(drv.device_diagnostics())

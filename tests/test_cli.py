@@ -85,3 +85,21 @@ def test_layout_bench_and_fabric(tmp_path):
     assert cli.main(["md", "--steps", "5", "--lattice-cells", "4", "--density", "1.1",
                      "--cutoff", "2.3", "--ranks", "2,2,2", "--output", str(q)]) == 0
     assert len(q.read_text().splitlines()) == 8
+
+
+@pytest.mark.gpu
+def test_ranks_byte_identical_deterministic(tmp_path):
+    """Criterion 3 through the CLI (ref test_acceptance.py:79-92): in the default
+    deterministic mode the physics rows are byte-identical for ranks 1x1x1 and
+    2x2x2; --parallel (tile path) runs too."""
+    outs = []
+    for ranks in ("1,1,1", "2,2,2", "2,1,1"):
+        p = tmp_path / f"r{ranks.replace(',', '')}.csv"
+        assert cli.main(["md", "--steps", "12", "--lattice-cells", "6", "--rebuild-stride", "5",
+                         "--skin", "0.3", "--ranks", ranks, "--output", str(p)]) == 0
+        outs.append(p.read_bytes().split(b"\n", 1)[1])
+    assert outs[0] == outs[1] == outs[2]
+    q = tmp_path / "par.csv"
+    assert cli.main(["md", "--steps", "12", "--lattice-cells", "6", "--parallel", "--output",
+                     str(q)]) == 0
+    assert len(q.read_text().splitlines()) == 2 + 13
