@@ -260,7 +260,8 @@ int pc_lj_force_sell_atoms(const double* d_pos, const double* d_planar, int64_t 
  * elements, >= n + 1).
  *
  * pc_tile_count: number of tiles.  pc_tile_rows: d_rw[tile] = row-warps of
- * the tile (ceil(home rows / 32)); the caller scans them into d_rw0
+ * the tile (max(1, ceil(home rows / 32)): a tile without rows keeps one empty
+ * row-warp); the caller scans them into d_rw0
  * (ntiles + 1 entries; total row-warps RW = d_rw0[ntiles]) and provides
  * d_plan (ntiles * pc_tile_plan_ints() int32), d_rowidx (RW * 32 int32),
  * d_rounds (RW int32), d_partial (RW * 5 doubles) and d_list (RW * q8 * 512

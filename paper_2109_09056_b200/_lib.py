@@ -14,6 +14,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libparticula_b200.so")
+# A/B builds (scripts/): PARTICULA_B200_LIB names another in-tree build of the same ABI
+if os.environ.get("PARTICULA_B200_LIB"):
+    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                            os.path.basename(os.environ["PARTICULA_B200_LIB"]))
 
 PC_OK = 0
 PC_ERR_VALUE = -1

@@ -18,10 +18,9 @@
 // three "segments" -- the z-cell below the grid (periodic wrap, z0 == 0), the
 // in-range cells, the z-cell above the grid (wrap) -- each a contiguous run of
 // the cell-sorted particle arrays.  A segment is copied from its even-aligned
-// start (16-B TMA alignment), so slot = seg_dst + (index - seg_src).  In the
-// force kernel's staging ring a tile's allocation starts with 16 dummy slots
-// (1e30 positions, one per LDS.64 bank pair) used as padding, so list
-// entries are byte offsets (slot + 16) * 8, dummies i * 8 (kSlotBias).
+// start (16-B TMA alignment), so slot = seg_dst + (index - seg_src).  Slots
+// [max_stage, max_stage + 16) hold NaN positions ("dummies", one per
+// LDS.64 bank pair) used as padding: a NaN r^2 fails the cutoff test.
 //
 // List layout: home rows of a tile are numbered column by column and grouped
 // in row-warps of 32.  Row-warp rw (global numbering rw0[tile] + w) holds
@@ -52,7 +51,6 @@ constexpr int kSX = kBX + 2, kSY = kBY + 2, kSZ = kTZ + 2;
 constexpr int kSCols = kSX * kSY;
 constexpr int kSegs = kSCols * 3;
 constexpr int kNDummy = 16;
-constexpr uint32_t kSlotBias = 16;   // list byte offset of staged slot s: (s + 16) * 8
 #ifndef PC_FORCE_SLEEP
 #define PC_FORCE_SLEEP 64
 #endif
@@ -65,6 +63,7 @@ constexpr int kHitCap = 112;
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
 // memory: compile-time so every LDS is [slot*8 + immediate]
 constexpr int kStageCap = 2304;
+constexpr int kStageStride = kStageCap + 16;
 
 struct TileSetup {
   int seg_src[kSegs];          // even-aligned first index of the copied run
@@ -229,7 +228,10 @@ __global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __r
       const int c0 = ((x0 + hx) * g.nc[1] + (y0 + hy)) * g.nc[2] + z0;
       h += cs[c0 + bz] - cs[c0];
     }
-  rw[tile] = (h + 31) >> 5;
+  // at least one row-warp per tile: a tile without home rows still gets an
+  // (empty) item, so the force kernel's warp that takes it releases the
+  // staging buffer the tile was loaded into (nothing else would)
+  rw[tile] = max(1, (h + 31) >> 5);
 }
 
 // ---- TMA / mbarrier helpers ----------------------------------------------
@@ -289,6 +291,7 @@ struct TileBuildParams {
   float lo2, hi2;      // FP32 band: r2f < lo2 -> hit, r2f >= hi2 -> miss, else exact FP64
   int Q8;              // list capacity per row-warp, in 8-round groups
   int max_stage;       // staged slots capacity (multiple of 16); dummies follow
+  int sched;           // 1: bank-conflict-free round schedule, 0: ascending order
   int64_t ps;          // planar stride
 };
 
@@ -301,22 +304,247 @@ __device__ __forceinline__ bool exact_pair_pl(const double* __restrict__ pl, int
   return r2_exact(dx, dy, dz) < cutoff2;
 }
 
-// Rounds of a row-warp: entry k of every row in round k (the build's
-// ascending sweep order; pc_tile_order reorders them), padded with dummies.
-// Encoding (kSlotBias): staged slot s -> byte offset (s + 16) * 8 from the
-// tile's allocation start; i * 8 (i < 16) is one of the tile's 16 dummy slots
-// (1e30 positions in front of the staged slots, one per LDS.64 bank pair).
-__device__ __forceinline__ int plain_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
-                                          uint4* __restrict__ out, int cap_rounds) {
+// Residue-group resolution of one proposal pass (see schedule_rows): lanes
+// of the same half-warp proposing slots of equal residue form a group (one
+// MATCH.ANY); the lowest critical lane of the group, else its lowest lane,
+// wins, and so does every lane proposing the winner's slot.
+__device__ __forceinline__ bool resolve(bool has, int s, unsigned crit, int half, int lane,
+                                        unsigned& taken) {
+  const unsigned FULL = 0xffffffffu;
+  const int r = s & 15;
+  const unsigned g = __match_any_sync(FULL, has ? (unsigned)((half << 4) | r)
+                                                : (unsigned)(32 + lane));
+  const unsigned gc = g & crit;
+  const int wl = __ffs(gc ? gc : g) - 1;
+  const int ws = __shfl_sync(FULL, s, wl);
+  const unsigned all = __reduce_or_sync(FULL, has ? (1u << ((half << 4) + r)) : 0u);
+  taken |= (all >> (half << 4)) & 0xFFFFu;
+  return has && s == ws;
+}
+
+// Bank-conflict-free round schedule of one row-warp.  Every lane holds its
+// row's slots in sweep order (hits[k*32]); in each round each lane takes one
+// entry so that within a half-warp (one LDS.64 pass of 16 lanes; measured,
+// scripts/micro/lds_banks.cu: conflicts across the two halves are free) all
+// lanes read distinct bank pairs (slot % 16) or the very same slot
+// (broadcast).  Two passes per round: every lane proposes its next entry;
+// per residue the lowest "critical" lane (remaining entries >= the warp's
+// maximum - 1: it bounds the round count), else the lowest lane, wins,
+// together with every lane proposing the winner's slot; losers then propose
+// the first entry of their next three whose residue is still free.  Lanes
+// left unassigned read a NaN-free dummy of a free residue.  Simulated on LJ
+// tiles: 1.08x the rounds of the longest row; measured 2.0 LDS wavefronts
+// per LDS.64 (unscheduled sweep order: 4.9).  The 4-entry window lives in two
+// registers of packed u16 (entry removal = two PRMTs).  Emits slot*8 (the
+// byte offset of the slot in one coordinate array).
+__device__ __forceinline__ int schedule_rows(const uint16_t* __restrict__ hits, int cnt,
+                                             int lane, int dummy0, uint4* __restrict__ out,
+                                             int cap_rounds, bool two_pass) {
+  const unsigned FULL = 0xffffffffu;
+  const int half = lane >> 4;
+  auto ld = [&](int k) -> uint32_t { return k < cnt ? (uint32_t)hits[k * 32] : 0xFFFFu; };
+  uint32_t w01 = ld(0) | (ld(1) << 16), w23 = ld(2) | (ld(3) << 16);
+  int ptr = 4;
+  int rem = cnt;
+  int R = 0;
+  uint32_t b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;     // 8 x u16 shift register
+  for (;;) {
+    const int maxrem = __reduce_max_sync(FULL, rem);
+    if (maxrem == 0) break;
+    const unsigned crit = __ballot_sync(FULL, rem > 0 && rem >= maxrem - 1);
+    unsigned taken = 0u;
+    const int e0 = (int)(w01 & 0xFFFFu);
+    int pi = -1, outs = -1;
+    if (resolve(rem > 0, e0, crit, half, lane, taken)) {
+      pi = 0;
+      outs = e0;
+    }
+    if (two_pass && __any_sync(FULL, pi < 0 && rem > 1)) {
+      const int e1 = (int)(w01 >> 16), e2 = (int)(w23 & 0xFFFFu), e3 = (int)(w23 >> 16);
+      int q = -1, qs = 0;
+      if (pi < 0) {
+        if (e3 != 0xFFFF && !((taken >> (e3 & 15)) & 1u)) { q = 3; qs = e3; }
+        if (e2 != 0xFFFF && !((taken >> (e2 & 15)) & 1u)) { q = 2; qs = e2; }
+        if (e1 != 0xFFFF && !((taken >> (e1 & 15)) & 1u)) { q = 1; qs = e1; }
+      }
+      if (resolve(q >= 0, qs, crit, half, lane, taken)) {
+        pi = q;
+        outs = qs;
+      }
+    }
+    if (pi >= 0) {       // drop entry pi, append the next hit
+      const uint32_t nx = ld(ptr);
+      ++ptr;
+      --rem;
+      const uint32_t n01 = pi == 0 ? __byte_perm(w01, w23, 0x5432)
+                                   : (pi == 1 ? __byte_perm(w01, w23, 0x5410) : w01);
+      w23 = __byte_perm(w23, nx, pi == 3 ? 0x5410 : 0x5432);
+      w01 = n01;
+    } else {
+      outs = dummy0 + (__ffs(~taken & 0xFFFFu) - 1);
+    }
+    b0 = __funnelshift_r(b0, b1, 16);
+    b1 = __funnelshift_r(b1, b2, 16);
+    b2 = __funnelshift_r(b2, b3, 16);
+    b3 = (b3 >> 16) | ((uint32_t)(outs * 8) << 16);
+    ++R;
+    if ((R & 7) == 0 && R <= cap_rounds) out[((R >> 3) - 1) * 32] = make_uint4(b0, b1, b2, b3);
+  }
+  if (R & 7) {     // pad the open group with conflict-free dummies
+    const uint32_t d = (uint32_t)((dummy0 + (lane & 15)) * 8);
+    for (int r = R; r & 7; ++r) {
+      b0 = __funnelshift_r(b0, b1, 16);
+      b1 = __funnelshift_r(b1, b2, 16);
+      b2 = __funnelshift_r(b2, b3, 16);
+      b3 = (b3 >> 16) | (d << 16);
+    }
+    if (((R + 7) & ~7) <= cap_rounds) out[(R >> 3) * 32] = make_uint4(b0, b1, b2, b3);
+  }
+  return R;
+}
+
+// ---- residue round-robin row order (default) --------------------------------
+// Lane-local bank-conflict avoidance (no cross-lane coordination).  The
+// entries of a row are bucketed by bank-pair residue (slot % 16) and emitted
+// round-robin: in round r the lane prefers residue (lane + r) % 16 -- the 16
+// lanes of a half-warp prefer 16 distinct residues in every round -- and
+// falls back to the next non-empty residue.  Simulated on LJ tiles: 1.6
+// LDS.64 passes per half-warp instead of 2.5 for the ascending order, at the
+// same round count; measured: force pass -14 %.  Cost: the row's class-major
+// order is scattered into its own list column (global, L2-resident), then
+// read back in round-robin order (rotate + ffs over the mask of non-empty
+// residues, byte counters packed in two 64-bit words), then written out.
+__device__ __forceinline__ int rr_rows(uint16_t* __restrict__ hits, int cnt, int lane,
+                                       int dummy0, uint4* __restrict__ out, int cap_rounds) {
+  uint16_t* col = reinterpret_cast<uint16_t*>(out);     // slot k at (k >> 3) * 256 + (k & 7)
+  const unsigned long long B = 0x0101010101010101ull;
+  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+  for (int k = 0; k < cnt; ++k) {
+    const int c = hits[k * 32] & 15;
+    const unsigned long long inc = 1ull << ((c & 7) * 8);
+    if (c < 8) clo += inc; else chi += inc;
+  }
+  const unsigned long long ilo = clo * B;               // inclusive byte prefix (< 256)
+  const unsigned long long slo = ilo - clo;
+  const unsigned long long shi = chi * B - chi + (ilo >> 56) * B;
+  unsigned long long rlo = slo, rhi = shi;
+  for (int k = 0; k < cnt; ++k) {                       // class-major scatter
+    const uint32_t v = hits[k * 32];
+    const int c = v & 15, sh = (c & 7) * 8;
+    const unsigned long long inc = 1ull << sh;
+    int pos;
+    if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
+    else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
+    col[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)(v * 8u);
+  }
+  const unsigned long long nz = ((clo | (clo >> 1) | (clo >> 2) | (clo >> 3) | (clo >> 4) |
+                                  (clo >> 5) | (clo >> 6) | (clo >> 7)) & B);
+  const unsigned long long nzh = ((chi | (chi >> 1) | (chi >> 2) | (chi >> 3) | (chi >> 4) |
+                                   (chi >> 5) | (chi >> 6) | (chi >> 7)) & B);
+  // byte-wise "non-zero" flags -> 16-bit mask (bit c = class c non-empty)
+  unsigned ne = (unsigned)(((nz * 0x0102040810204080ull) >> 56) & 0xFFull) |
+                ((unsigned)(((nzh * 0x0102040810204080ull) >> 56) & 0xFFull) << 8);
+  unsigned long long plo = slo, phi = shi, qlo = clo, qhi = chi;
+  for (int r0 = 0; r0 < cnt; r0 += 8) {                 // round-robin emission
+    // 8 rounds: positions from the register state first, then 8 independent
+    // loads of the class-major copy (L2 round trips overlap)
+    int pos[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int pref = (lane + r0 + u) & 15;
+      const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
+      const int c = (pref + __ffs(rot) - 1) & 15, sh = (c & 7) * 8;
+      const unsigned long long inc = 1ull << sh;
+      unsigned left;
+      if (c < 8) {
+        pos[u] = (int)((plo >> sh) & 0xFFull);
+        plo += inc;
+        qlo -= inc;
+        left = (unsigned)((qlo >> sh) & 0xFFull);
+      } else {
+        pos[u] = (int)((phi >> sh) & 0xFFull);
+        phi += inc;
+        qhi -= inc;
+        left = (unsigned)((qhi >> sh) & 0xFFull);
+      }
+      if (left == 0u) ne &= ~(1u << c);
+      if (r0 + u >= cnt) pos[u] = 0;      // past the row: any valid address
+      if (ne == 0u) ne = 1u;              // (exhausted: keep ffs defined)
+    }
+    uint16_t vals[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vals[u] = col[(pos[u] >> 3) * 256 + (pos[u] & 7)];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (r0 + u < cnt) hits[(r0 + u) * 32] = vals[u];
+  }
   const int R = __reduce_max_sync(0xffffffffu, cnt);
-  const uint32_t d = (uint32_t)((lane & 15) * 8);
   for (int r8 = 0; r8 < R && r8 + 8 <= cap_rounds; r8 += 8) {
     uint32_t w[4];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const int r = r8 + 2 * h;
-      const uint32_t lo = r < cnt ? ((uint32_t)hits[r * 32] + kSlotBias) * 8u : d;
-      const uint32_t hi = r + 1 < cnt ? ((uint32_t)hits[(r + 1) * 32] + kSlotBias) * 8u : d;
+      const uint32_t lo = r < cnt ? (uint32_t)hits[r * 32]
+                                  : (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+      const uint32_t hi = r + 1 < cnt ? (uint32_t)hits[(r + 1) * 32]
+                                      : (uint32_t)(dummy0 + ((lane + r + 1) & 15)) * 8u;
+      w[h] = lo | (hi << 16);
+    }
+    out[(r8 >> 3) * 32] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  return R;
+}
+
+// Cheaper variant (default): class-major order with the residue classes
+// visited in a lane-rotated order (lane l starts at residue l % 16).  The
+// row's entries are scattered straight into their final list positions (one
+// pass over the hits; per-class running counts as packed bytes).  Simulated:
+// 2.0 LDS.64 passes per half-warp (round-robin: 1.6, ascending: 2.5).
+__device__ __forceinline__ int cm_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
+                                       int dummy0, uint4* __restrict__ out, int cap_rounds) {
+  uint16_t* col = reinterpret_cast<uint16_t*>(out);     // slot k at (k >> 3) * 256 + (k & 7)
+  const unsigned long long B = 0x0101010101010101ull;
+  unsigned long long clo = 0ull, chi = 0ull;            // per-class counts (bytes)
+  for (int k = 0; k < cnt; ++k) {
+    const int c = hits[k * 32] & 15;
+    const unsigned long long inc = 1ull << ((c & 7) * 8);
+    if (c < 8) clo += inc; else chi += inc;
+  }
+  const unsigned long long ilo = clo * B;
+  unsigned long long rlo = ilo - clo;                   // exclusive prefix = class starts
+  unsigned long long rhi = chi * B - chi + (ilo >> 56) * B;
+  const int l0 = lane & 15;
+  const int s0 = (int)(((l0 < 8 ? rlo : rhi) >> ((l0 & 7) * 8)) & 0xFFull);
+  for (int k = 0; k < cnt; ++k) {
+    const uint32_t v = hits[k * 32];
+    const int c = v & 15, sh = (c & 7) * 8;
+    const unsigned long long inc = 1ull << sh;
+    int pos;
+    if (c < 8) { pos = (int)((rlo >> sh) & 0xFFull); rlo += inc; }
+    else       { pos = (int)((rhi >> sh) & 0xFFull); rhi += inc; }
+    pos -= s0;                                          // rotate: class l0 first
+    if (pos < 0) pos += cnt;
+    col[(pos >> 3) * 256 + (pos & 7)] = (uint16_t)(v * 8u);
+  }
+  const int R = __reduce_max_sync(0xffffffffu, cnt);
+  for (int r = cnt; r < ((R + 7) & ~7) && r < cap_rounds; ++r)
+    col[(r >> 3) * 256 + (r & 7)] = (uint16_t)((dummy0 + ((lane + r) & 15)) * 8);
+  return R;
+}
+
+// Unscheduled rounds: entry k of every row in round k (sweep order), padded
+// with dummies -- the cheap alternative to schedule_rows (PC_TILE_NOSCHED).
+__device__ __forceinline__ int plain_rows(const uint16_t* __restrict__ hits, int cnt, int lane,
+                                          int dummy0, uint4* __restrict__ out, int cap_rounds) {
+  const int R = __reduce_max_sync(0xffffffffu, cnt);
+  const uint32_t d = (uint32_t)((dummy0 + (lane & 15)) * 8);
+  for (int r8 = 0; r8 < R && r8 + 8 <= cap_rounds; r8 += 8) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int r = r8 + 2 * h;
+      const uint32_t lo = r < cnt ? (uint32_t)hits[r * 32] * 8u : d;
+      const uint32_t hi = r + 1 < cnt ? (uint32_t)hits[(r + 1) * 32] * 8u : d;
       w[h] = lo | (hi << 16);
     }
     out[(r8 >> 3) * 32] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -369,7 +597,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     return;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nrw = (T.H + 31) >> 5;
+  const int nrw = max(1, (T.H + 31) >> 5);      // as tile_rows_kernel
   const int bz = T.bz;
   if (warp == 0) {                       // compacted plan of this tile
     int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
@@ -539,7 +767,11 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     __syncwarp();
     const int cap = 8 * p.Q8;
     uint4* lout = list + (int64_t)rw * p.Q8 * 32 + lane;
-    const int R = plain_rows(hits, cnt, lane, lout, cap);
+    const int R = p.sched == 0   ? cm_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                  : p.sched == 4 ? rr_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                  : p.sched == 3 ? plain_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                                 : schedule_rows(hits, cnt, lane, p.max_stage, lout, cap,
+                                                 p.sched == 1);
     if (lane == 0) {
       rounds[rw] = ((R + 7) & ~7) > cap ? 0 : R;
       if (((R + 7) & ~7) > cap) {
@@ -590,25 +822,15 @@ cell_zsort_kernel(const double* __restrict__ pos4, const int* __restrict__ cs, i
 
 // ---- force ------------------------------------------------------------------
 // Persistent kernel: one CTA of kForceWarps warps per SM walks its tiles
-// (blockIdx.x + k*gridDim.x) through a shared-memory staging RING.  Row-warps
-// of all its tiles form one queue (item i -> tile k by the prefix of row-warp
-// counts); a warp takes the next item, prefetches the row's list / position /
-// index words, waits until tile k is staged and sweeps the rounds.
-//
-// The ring is three equal planes (x | y | z, kRingSlots doubles each, so a
-// slot's y and z are immediate offsets from its x).  Tile k occupies S_k + 16
-// contiguous slots -- 16 dummies (1e30) then its staged slots -- allocated in
-// tile order, wrapping to the ring start when the tail does not fit, and
-// released in tile order once all its row-warps are done.  Sizing exactly
-// (instead of fixed 2320-slot buffers) keeps ~4.7 tiles in flight: a tile is
-// held from its first row-warp's start to its last one's end, about
-// 1 + warps/row-warps-per-tile = 4.2 tiles at 32 warps, and warps waited
-// ~15 % of the time with 4 fixed buffers (profiles/r01d).  The warp
-// releasing a tile issues the TMA bulk copies of as many next tiles as fit,
-// under a shared-memory lock; per-tile mbarriers live in a ring of kRing
-// (parity from k).
-constexpr int kRing = 8;            // tiles in flight at most (mbarriers, per-tile state)
-constexpr int kRingSlots = 9600;    // slots per plane: 3 x 9600 x 8 B = 225 KB
+// (blockIdx.x + k*gridDim.x) through a ring of kNBuf shared-memory staging
+// buffers.  Row-warps of all its tiles form one queue (item i -> tile k by
+// the prefix of row-warp counts); a warp takes the next item, prefetches the
+// row's list / position / index words, waits on the buffer's mbarrier and
+// sweeps the rounds.  The warp finishing a tile's last row-warp frees its
+// buffer and immediately issues the TMA bulk copies of the next unloaded
+// tile into it, so staging overlaps the compute of the tiles in flight and
+// no warp idles at a tile boundary.
+constexpr int kNBuf = 4;       // max staging buffers (runtime: as many as fit)
 
 struct TileForceParams {
   double cutoff2, overlap2;
@@ -620,17 +842,13 @@ struct TileForceParams {
 };
 
 struct ForceShared {
-  uint64_t bar[kRing];
-  int base[kRing];           // first slot of tile k's allocation (k % kRing)
-  int end_v[kRing];          // virtual end of the allocation (-1: none)
-  int done[kRing];           // finished row-warps of tile k
-  int fin[kRing];            // tile k finished (all row-warps)
-  volatile int ready[kRing]; // k once tile k's copies are issued (k % kRing), else older
-  int issued;                // tiles 0..issued-1 have ring space
-  int released;              // tiles 0..released-1 released, in order
-  int head_v, tail_v;        // virtual ring positions (slots, monotonic)
-  int lock;
+  uint64_t bar[kNBuf];
+  volatile int seq[kNBuf];   // tile sequence index held by each buffer (-1: none)
+  int par[kNBuf];            // mbarrier parity of the current use
+  int uses[kNBuf];
+  int done[kNBuf];           // finished row-warps of the current tile
   int next_item;
+  int loaded;                // tickets: next tile sequence index to load
   int K;                     // tiles of this CTA
   int items;                 // row-warps of this CTA
 };
@@ -655,8 +873,8 @@ __device__ __forceinline__ void tile_pair(const char* __restrict__ st, uint32_t 
                                           double& fy, double& fz, float& pe, bool& overlap) {
   const double* q = reinterpret_cast<const double*>(st + off);
   double dx = __dsub_rn(q[0], xi);
-  double dy = __dsub_rn(q[kRingSlots], yi);
-  double dz = __dsub_rn(q[2 * kRingSlots], zi);
+  double dy = __dsub_rn(q[kStageStride], yi);
+  double dz = __dsub_rn(q[2 * kStageStride], zi);
   if (MI) {
     // staged coordinates are wrapped into the box: |d| < L, so the exact
     // threshold form needs no division fallback (dummies: 1e30 stays huge)
@@ -714,98 +932,32 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st,
   }
 }
 
-// Lane 0, ring lock held: allocate ring space for as many next tiles as fit
-// (in tile order); returns the first tile allocated, F.issued is one past the
-// last.  `sz` = staged slots per tile (0: no rows, nothing to stage).
-__device__ __forceinline__ int ring_alloc(ForceShared& F, const int* __restrict__ sz) {
-  const int k0 = F.issued;
-  for (;;) {
-    // release finished tiles in order first (tiles without rows finish at
-    // allocation: a run of them must not fill the window of kRing)
-    while (F.released < F.issued && F.fin[F.released & (kRing - 1)]) {
-      const int e = F.end_v[F.released & (kRing - 1)];
-      if (e >= 0) F.tail_v = e;
-      F.released += 1;
-    }
-    const int k = F.issued;
-    if (k >= F.K || k - F.released >= kRing) break;
-    const int q = k & (kRing - 1);
-    const int S = sz[k];
-    if (S > 0) {
-      const int A = S + (int)kSlotBias;          // even: segments are even-aligned
-      int h = F.head_v;
-      const int pos = h % kRingSlots;
-      if (pos + A > kRingSlots) h += kRingSlots - pos;      // wrap: skip the ring tail
-      if (h + A - F.tail_v > kRingSlots) break;            // no room yet
-      F.base[q] = h % kRingSlots;
-      F.head_v = h + A;
-      F.end_v[q] = h + A;
-      F.fin[q] = 0;
-    } else {
-      F.base[q] = 0;
-      F.end_v[q] = -1;
-      F.fin[q] = 1;                               // no rows: never waited on
-    }
-    F.done[q] = 0;
-    F.issued = k + 1;
-  }
-  return k0;
-}
-
-// Whole warp: issue the TMA copies of tiles [k0, k1) (space allocated) and
-// publish each as ready.
-__device__ void ring_stage(ForceShared& F, double* __restrict__ ring, int k0, int k1,
-                           const int* __restrict__ plan, const double* __restrict__ pl,
-                           int64_t ps, int lane) {
-  for (int k = k0; k < k1; ++k) {
-    const int q = k & (kRing - 1);
-    const int tile = blockIdx.x + k * gridDim.x;
-    const int* gp = plan + (int64_t)tile * kPlanInts;
-    const bool rows = F.end_v[q] >= 0;
-    const int m = rows ? gp[0] : 0, S = rows ? gp[1] : 0;
-    if (lane == 0) mbar_expect_tx(&F.bar[q], (uint32_t)S * 24u);   // S = 0: plain arrive
-    __syncwarp();
-    if (rows) {
-      double* st = ring + F.base[q];
-      if (lane < kNDummy)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) st[a * kRingSlots + lane] = 1e30;
-      for (int e = lane; e < m; e += 32) {
-        const int src = gp[4 + 3 * e], len = gp[5 + 3 * e];
-        const int dst = gp[6 + 3 * e] + (int)kSlotBias;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-          bulk_g2s(st + a * kRingSlots + dst, pl + a * ps + src, (uint32_t)len * 8u, &F.bar[q]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      F.ready[q] = k;
-    }
+// whole warp: stage tile sequence k of this CTA into buffer b
+__device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ stage, int b,
+                                           int k, const int* __restrict__ plan,
+                                           const double* __restrict__ pl, int64_t ps, int lane) {
+  const int tile = blockIdx.x + k * gridDim.x;
+  const int* gp = plan + (int64_t)tile * kPlanInts;
+  const int m = gp[0], S = gp[1];
+  double* st = stage + (int64_t)b * 3 * kStageStride;
+  if (lane == 0) {
+    F.done[b] = 0;
+    F.par[b] = F.uses[b] & 1;
+    F.uses[b] += 1;
+    mbar_expect_tx(&F.bar[b], (uint32_t)S * 24u);
   }
   __syncwarp();
-}
-
-// Whole warp: tile k finished -- release finished tiles in order, allocate
-// and stage the next ones (copies issued outside the lock).
-__device__ void ring_release(ForceShared& F, double* __restrict__ ring, int k,
-                             const int* __restrict__ plan, const int* __restrict__ sz,
-                             const double* __restrict__ pl, int64_t ps, int lane) {
-  int k0 = 0, k1 = 0;
-  if (lane == 0) {
-    while (atomicCAS(&F.lock, 0, 1) != 0) __nanosleep(32);
-    __threadfence_block();
-    F.fin[k & (kRing - 1)] = 1;
-    k0 = ring_alloc(F, sz);
-    k1 = F.issued;
-    __threadfence_block();
-    atomicExch(&F.lock, 0);
+  for (int e = lane; e < m; e += 32) {
+    const int src = gp[4 + 3 * e], len = gp[5 + 3 * e], dst = gp[6 + 3 * e];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      bulk_g2s(st + a * kStageStride + dst, pl + a * ps + src, (uint32_t)len * 8u, &F.bar[b]);
   }
-  k0 = __shfl_sync(0xffffffffu, k0, 0);
-  k1 = __shfl_sync(0xffffffffu, k1, 0);
-  __threadfence_block();
-  ring_stage(F, ring, k0, k1, plan, pl, ps, lane);
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    F.seq[b] = k;
+  }
 }
 
 template <bool UNIT_SIGMA>
@@ -815,19 +967,15 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
                   const int* __restrict__ rounds, const uint4* __restrict__ list, pc_box b,
                   double* __restrict__ f3, int64_t fs, double* __restrict__ v, int64_t vs,
                   double dtm, double mass, double* __restrict__ partial, int* __restrict__ flag,
-                  double* __restrict__ x_next, double* __restrict__ v_next,
-                  double dtm_next, double dt, int* __restrict__ scratch) {
+                  int nbuf, double* __restrict__ x_next, double* __restrict__ v_next,
+                  double dtm_next, double dt) {
   extern __shared__ double dyn[];
-  double* ring = dyn;                                              // x | y | z planes
+  double* stage = dyn;                                             // nbuf x (x|y|z)
   __shared__ ForceShared F;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  // item prefix (K + 1) and first row-warp (K) per tile of this CTA: global
-  // scratch (L1-resident), so the whole shared memory is staging ring
-  const int Kmax = (ntiles + (int)gridDim.x - 1) / (int)gridDim.x;   // same stride for all CTAs
-  int* pre = scratch + (int64_t)blockIdx.x * (3 * Kmax + 1);
-  int* rwbk = pre + K + 1;
-  int* sz = rwbk + K;                                                 // staged slots per tile
+  int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
+  int* rwbk = pre + K + 1;                                              // first row-warp per k
   if (warp == 0) {
     // row-warp prefix over this CTA's tiles
     int carry = 0;
@@ -835,10 +983,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       const int k = k0 + lane;
       const int* gpk = plan + (int64_t)(blockIdx.x + k * gridDim.x) * kPlanInts;
       const int c = k < K ? gpk[2] : 0;
-      if (k < K) {
-        rwbk[k] = gpk[3];
-        sz[k] = c > 0 ? gpk[1] : 0;
-      }
+      if (k < K) rwbk[k] = gpk[3];
       int inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -853,28 +998,20 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       F.items = carry;
       F.K = K;
       F.next_item = 0;
-      F.issued = 0;
-      F.released = 0;
-      F.head_v = 0;
-      F.tail_v = 0;
-      F.lock = 0;
-      for (int q = 0; q < kRing; ++q) {
+      for (int q = 0; q < kNBuf; ++q) {
+        F.seq[q] = -1;
+        F.uses[q] = 0;
         mbar_init(&F.bar[q], 1);
-        F.ready[q] = -1;
       }
+      F.loaded = min(K, nbuf);
     }
     __syncwarp();
-    __threadfence_block();
-    int k1 = 0;
-    if (lane == 0) {                                      // no other warp runs yet
-      ring_alloc(F, sz);
-      k1 = F.issued;
-    }
-    k1 = __shfl_sync(0xffffffffu, k1, 0);
-    __threadfence_block();
-    ring_stage(F, ring, 0, k1, plan, pl, p.ps, lane);
+    for (int q = 0; q < min(K, nbuf); ++q) force_load(F, stage, q, q, plan, pl, p.ps, lane);
+  } else if (warp == 1) {
+    for (int q = 0; q < nbuf; ++q)
+      if (lane < kNDummy)
+        for (int a = 0; a < 3; ++a) stage[(q * 3 + a) * kStageStride + kStageCap + lane] = 1e30;
   }
-  __threadfence_block();
   __syncthreads();
   const int items = F.items;
   double ake = 0.0, ape = 0.0, apx = 0.0, apy = 0.0, apz = 0.0;   // this lane's rows
@@ -904,12 +1041,18 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       yi = pl[p.ps + a];
       zi = pl[2 * p.ps + a];
     }
-    // tile k: wait until its copies are issued (tile order), then complete
-    const int q = k & (kRing - 1);
-    while (F.ready[q] != k) __nanosleep(PC_FORCE_SLEEP);
+    // buffer holding tile k (loaded in ticket order; spin until published)
+    int bsel = -1;
+    for (;;) {
+#pragma unroll
+      for (int q = 0; q < kNBuf; ++q)
+        if (F.seq[q] == k) bsel = q;
+      if (bsel >= 0) break;
+      __nanosleep(PC_FORCE_SLEEP);
+    }
     __threadfence_block();
-    mbar_wait(&F.bar[q], (uint32_t)((k / kRing) & 1));
-    const char* st = reinterpret_cast<const char*>(ring + F.base[q]);
+    mbar_wait(&F.bar[bsel], (uint32_t)F.par[bsel]);
+    const char* st = reinterpret_cast<const char*>(stage + (int64_t)bsel * 3 * kStageStride);
 
     const bool nx = act && b.periodic[0] && (xi - b.low[0] < p.guard || b.high[0] - xi <= p.guard);
     const bool ny = act && b.periodic[1] && (yi - b.low[1] < p.guard || b.high[1] - yi <= p.guard);
@@ -923,11 +1066,19 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     else
       tile_row<false, UNIT_SIGMA>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
                                   overlap);
-    // the tile's last row-warp releases it (in tile order) and refills the ring
+    // release the buffer when this was the tile's last row-warp; refill it
     int last = 0;
-    if (lane == 0) last = atomicAdd(&F.done[q], 1) + 1 == pre[k + 1] - pre[k];
+    if (lane == 0) last = atomicAdd(&F.done[bsel], 1) + 1 == pre[k + 1] - pre[k];
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) ring_release(F, ring, k, plan, sz, pl, p.ps, lane);
+    if (last) {
+      int kn = 0;
+      if (lane == 0) {
+        F.seq[bsel] = -1;
+        kn = atomicAdd(&F.loaded, 1);
+      }
+      kn = __shfl_sync(0xffffffffu, kn, 0);
+      if (kn < K) force_load(F, stage, bsel, kn, plan, pl, p.ps, lane);
+    }
     if (overlap) atomicOr(flag, kFlagOverlap);
     double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0, ped = 0.0;
     if (act) {
@@ -1010,7 +1161,7 @@ constexpr int kOrdSmem = kOrdWarps * (kHitCap * 32 * 2 + 16 * 32 * 4);
 template <bool RR>
 __global__ void __launch_bounds__(kOrdWarps * 32, 3)
 tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
-                  const int* __restrict__ rw_total, int Q8) {
+                  const int* __restrict__ rw_total, int Q8, int dummy0) {
   extern __shared__ __align__(16) unsigned char osm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rw = blockIdx.x * kOrdWarps + warp;
@@ -1021,7 +1172,7 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
   const int R = rounds[rw];
   if (R <= 0 || R > kHitCap) return;
   uint4* lp = list + (int64_t)rw * Q8 * 32 + lane;
-  const uint32_t dmin = kSlotBias * 8u;                 // real entries: v >= dmin
+  const uint32_t dmin = (uint32_t)dummy0 * 8u;
   const int G = (R + 7) >> 3;
 #pragma unroll
   for (int c = 0; c < 16; ++c) st[c * 32] = 0u;
@@ -1032,7 +1183,7 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
-      if (g * 8 + t < R && v >= dmin) {
+      if (g * 8 + t < R && v < dmin) {
         uint32_t* sc = st + ((v >> 3) & 15) * 32;
         *sc += 1u;
         ++cnt;
@@ -1099,7 +1250,7 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
         }
         v = Bm[pos * 32];
       } else {
-        v = (uint32_t)((lane + r) & 15) * 8u;
+        v = (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
       }
       o[t >> 1] |= (t & 1) ? (v << 16) : v;
     }
@@ -1127,8 +1278,8 @@ tile_decode_kernel(const int* __restrict__ plan, int Q8, int max_stage,
     const uint16_t* lp = reinterpret_cast<const uint16_t*>(list + (int64_t)rw * Q8 * 32 + lane);
     int cnt = 0;
     for (int r = 0; r < R; ++r) {
-      const int s = (lp[(r >> 3) * 32 * 8 + (r & 7)] >> 3) - (int)kSlotBias;
-      if (s < 0) continue;                    // dummy
+      const int s = lp[(r >> 3) * 32 * 8 + (r & 7)] >> 3;
+      if (s >= max_stage) continue;
       int e = 0;
       while (e < m - 1 && !(s >= pg[6 + 3 * e] && s < pg[6 + 3 * e] + pg[5 + 3 * e])) ++e;
       const int j = pg[4 + 3 * e] + (s - pg[6 + 3 * e]);
@@ -1230,6 +1381,7 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   p.hi2 = nextafterf((float)(cutoff2 + margin), INFINITY);
   p.Q8 = q8;
   p.max_stage = kStageCap;
+  p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 3;
   p.ps = planar_stride;
   const int smem = kStageCap * (int)sizeof(float4) +
                    kBuildWarps * 32 * kHitCap * (int)sizeof(uint16_t);
@@ -1277,7 +1429,7 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
   const int sms = sm_count();
   const int grid = ntiles < sms ? ntiles : sms;
   const int K = (ntiles + grid - 1) / grid;
-  // the staging ring in dynamic smem; the CTAs' item prefixes in scratch
+  // as many staging buffers as fit next to the item prefix (2..kNBuf)
   static int smem_max = 0;
   if (smem_max == 0) {
     int dev = 0;
@@ -1285,24 +1437,15 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (smem_max <= 0) smem_max = 227 * 1024;
   }
-  const int static_bytes = 2048;                           // ForceShared + reserve
-  const int smem = 3 * kRingSlots * (int)sizeof(double);
+  const int buf_bytes = 3 * kStageStride * (int)sizeof(double);
+  const int pre_bytes = (2 * K + 1) * (int)sizeof(int);
+  const int static_bytes = 512;
+  int nbuf = kNBuf;
+  while (nbuf > 2 && nbuf * buf_bytes + pre_bytes + static_bytes > smem_max) --nbuf;
+  const int smem = nbuf * buf_bytes + pre_bytes + K * (int)sizeof(int);
   if (smem + static_bytes > smem_max) {
-    set_error("pc_tile_force: the staging ring does not fit in shared memory");
+    set_error("pc_tile_force: %d tiles per CTA do not fit in shared memory", K);
     return PC_ERR_CAPACITY;
-  }
-  static int* scratch = nullptr;
-  static int64_t scratch_n = 0;
-  const int64_t need = (int64_t)grid * (3 * K + 1);
-  if (need > scratch_n) {
-    if (scratch) cudaFree(scratch);
-    scratch = nullptr;
-    scratch_n = 0;
-    if (cudaMalloc(&scratch, need * sizeof(int)) != cudaSuccess) {
-      set_error("pc_tile_force: scratch allocation of %lld ints failed", (long long)need);
-      return PC_ERR_CAPACITY;
-    }
-    scratch_n = need;
   }
   const bool unit = lj->sigma == 1.0;
   if (smem > g_force_smem) {
@@ -1319,13 +1462,13 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
   if (unit)
     tile_force_kernel<true><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
-        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, d_planar_next,
-        d_v_next, dtm_next, dt, scratch);
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
+        d_v_next, dtm_next, dt);
   else
     tile_force_kernel<false><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
-        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, d_planar_next,
-        d_v_next, dtm_next, dt, scratch);
+        *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
+        d_v_next, dtm_next, dt);
   return check_launch("pc_tile_force");
 }
 
@@ -1348,10 +1491,10 @@ int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_
   uint4* l = reinterpret_cast<uint4*>(d_list);
   if (kind == 1)
     tile_order_kernel<true><<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
-        l, d_rounds, d_rw_total, q8);
+        l, d_rounds, d_rw_total, q8, kStageCap);
   else
     tile_order_kernel<false><<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
-        l, d_rounds, d_rw_total, q8);
+        l, d_rounds, d_rw_total, q8, kStageCap);
   return check_launch("pc_tile_order");
 }
 
