@@ -51,7 +51,8 @@ def parse_args():
     ap.add_argument("--list", choices=["full", "half"], default="full")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="steps of the end-to-end leg (0: the same K as the device leg)")
     ap.add_argument("--path", choices=["tile", "sell"], default="tile",
                     help="MD force/list path: TMA-staged tile rounds (default) or the "
                          "per-particle SELL list")
@@ -264,7 +265,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(pc, kw, args.e2e_steps, world)
+        e2e = run_e2e(pc, kw, args.e2e_steps or K, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

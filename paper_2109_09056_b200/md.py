@@ -525,28 +525,35 @@ class MDDriver:
             raise FloatingPointError("overlapping particles in LJ kernel")
 
     # -- diagnostics --------------------------------------------------------
-    def device_diagnostics(self) -> torch.Tensor:
-        """(KE, PE, px, py, pz) on the device, no host sync."""
+    def device_diagnostics(self, out=None) -> torch.Tensor:
+        """(KE, PE, px, py, pz) on the device, no host sync; `out`: a 5-double
+        device row to reduce into (run_md's history) instead of self.diag."""
         if self.deterministic:
             if not self._ke_fresh:   # per-atom rows again (v unchanged: zero kick)
                 self._force(0.0)
             # per-atom rows in global-id order, one fixed reduction tree
             call("pc_scatter_rows", ptr(self._atom), ptr(self._atom_g), ptr(self._gid32),
                  self.n, 40, stream())
-            call("pc_reduce_partials", ptr(self._atom_g), self.n, ptr(self.diag), stream())
-            return self.diag
+            d = self.diag if out is None else out
+            call("pc_reduce_partials", ptr(self._atom_g), self.n, ptr(d), stream())
+            return d
         if not self._ke_fresh:       # velocities changed outside a force pass
             call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n, 0.0,
                  float(self.cfg.mass), ptr(self.partial_k), stream())
             self._ke_in_k = True
             self._ke_fresh = True
-        call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(self.diag), stream())
         if self._ke_in_k:            # KE / momentum from the kick partials, PE from force
+            call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(self.diag), stream())
             nk = int(_lib.load().pc_lj_force_blocks(self.n))
             call("pc_reduce_partials", ptr(self.partial_k), nk, ptr(self.diag_k), stream())
             self.diag_k[1] = self.diag[1]
+            if out is not None:
+                out.copy_(self.diag_k)
+                return out
             return self.diag_k
-        return self.diag
+        d = self.diag if out is None else out
+        call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(d), stream())
+        return d
 
     def diagnostics(self):
         """Global energies (ref md.py:261-277)."""
@@ -639,10 +646,10 @@ def run_md(cfg: MDConfig, state=None, time_phases: bool = True, deterministic: b
     drv = MDDriver(cfg, state=state, time_phases=time_phases, deterministic=deterministic)
     drv.timings = {k: 0.0 for k in PHASES}
     hist = torch.empty((cfg.steps + 1, 5), dtype=torch.float64, device=drv.device)
-    hist[0].copy_(drv.device_diagnostics())
+    drv.device_diagnostics(out=hist[0])
     for s in range(1, cfg.steps + 1):
         drv.step(s)
-        hist[s].copy_(drv.device_diagnostics())
+        drv.device_diagnostics(out=hist[s])
     h = hist.cpu().numpy()
     drv.check_errors()
     rows = []
