@@ -1153,7 +1153,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
 // prefer 16 distinct residues in every round: 1.6 LDS.64 passes per
 // half-warp instead of 2.5 (simulated), force pass -14 % (measured).
 constexpr int kOrdWarps = 8;
-constexpr int kOrdSmem = kOrdWarps * (kHitCap * 32 * 2 + 16 * 32 * 4);
+constexpr int kOrdSmem = kOrdWarps * ((kHitCap + 1) * 32 * 2 + 16 * 32 * 4);
 
 // RR = false: class-major with the start rotated to the lane's residue (the
 // cheaper variant, simulated 1.9 passes per half-warp).  Per-class state
@@ -1168,7 +1168,7 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
   if (rw >= *rw_total) return;
   uint32_t* st = reinterpret_cast<uint32_t*>(osm) + warp * 16 * 32 + lane;   // [c][lane]
   uint16_t* Bm = reinterpret_cast<uint16_t*>(osm + kOrdWarps * 16 * 32 * 4) +
-                 warp * kHitCap * 32 + lane;                                  // [k][lane]
+                 warp * (kHitCap + 1) * 32 + lane;    // [k][lane], row kHitCap: dump
   const int R = rounds[rw];
   if (R <= 0 || R > kHitCap) return;
   uint4* lp = list + (int64_t)rw * Q8 * 32 + lane;
@@ -1183,11 +1183,12 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
-      if (g * 8 + t < R && v < dmin) {
-        uint32_t* sc = st + ((v >> 3) & 15) * 32;
-        *sc += 1u;
-        ++cnt;
-      }
+      // branch-free: a padding entry (v >= dmin; the groups past R are
+      // padding too) adds 0 to its residue's count
+      const uint32_t real = v < dmin ? 1u : 0u;
+      uint32_t* sc = st + ((v >> 3) & 15) * 32;
+      *sc += real;
+      cnt += (int)real;
     }
   }
   // exclusive prefix -> st[c] = start | start << 16 (next | begin); end = next start
@@ -1207,16 +1208,16 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
-      if (g * 8 + t < cnt) {
-        const int c = (v >> 3) & 15;
-        uint32_t* sc = st + c * 32;
-        const uint32_t e = *sc;
-        *sc = e + 1u;
-        int pos = (int)(e & 0xFFFFu);
-        if (RR) ne |= 1u << c;
-        else { pos -= s0; if (pos < 0) pos += cnt; }
-        Bm[pos * 32] = (uint16_t)v;
-      }
+      // branch-free: padding entries leave the state and land in the dump row
+      const bool real = v < dmin;
+      const int c = (v >> 3) & 15;
+      uint32_t* sc = st + c * 32;
+      const uint32_t e = *sc;
+      *sc = e + (real ? 1u : 0u);
+      int pos = (int)(e & 0xFFFFu);
+      if (RR) ne |= real ? 1u << c : 0u;
+      else { pos -= s0; if (pos < 0) pos += cnt; }
+      Bm[(real ? pos : kHitCap) * 32] = (uint16_t)v;
     }
   }
   if (RR) {                                             // rewind next to begin
@@ -1233,25 +1234,22 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int r = g * 8 + t;
-      uint32_t v;
-      if (r < cnt) {
-        int pos = r;
-        if (RR) {
-          // in round r lane l prefers residue (l + r) % 16, else the next
-          // non-empty one
-          const int pref = (lane + r) & 15;
-          const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
-          const int c = (pref + __ffs(rot) - 1) & 15;
-          uint32_t* sc = st + c * 32;
-          const uint32_t e = *sc;
-          pos = (int)(e & 0xFFFFu);
-          *sc = e + 1u;
-          if ((uint32_t)pos + 1u == (e >> 16)) ne &= ~(1u << c);
-        }
-        v = Bm[pos * 32];
-      } else {
-        v = (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+      const bool real = r < cnt;
+      int pos = r;
+      if (RR) {
+        // in round r lane l prefers residue (l + r) % 16, else the next
+        // non-empty one (branch-free: past cnt the state is left unchanged)
+        const int pref = (lane + r) & 15;
+        const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
+        const int c = (pref + __ffs(rot) - 1) & 15;
+        uint32_t* sc = st + c * 32;
+        const uint32_t e = *sc;
+        pos = (int)(e & 0xFFFFu);
+        *sc = e + (real ? 1u : 0u);
+        if (real && (uint32_t)pos + 1u == (e >> 16)) ne &= ~(1u << c);
       }
+      const uint32_t vb = Bm[(real ? pos : kHitCap) * 32];
+      const uint32_t v = real ? vb : (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
       o[t >> 1] |= (t & 1) ? (v << 16) : v;
     }
     lp[g * 32] = make_uint4(o[0], o[1], o[2], o[3]);
