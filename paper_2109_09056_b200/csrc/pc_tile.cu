@@ -60,6 +60,7 @@ constexpr int kNDummy = 16;
 constexpr int kForceWarps = PC_FORCE_WARPS;
 constexpr int kBuildWarps = 10;
 constexpr int kHitCap = 112;
+constexpr int kHitSlack = 3;   // spare rows per hit column (unclamped 4-candidate stores)
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
 // memory: compile-time so every LDS is [slot*8 + immediate]
 constexpr int kStageCap = 2304;
@@ -237,6 +238,10 @@ __global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __r
 // ---- TMA / mbarrier helpers ----------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -643,14 +648,16 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
   __syncthreads();
 
-  uint16_t* hits = hits_all + warp * kHitCap * 32 + lane;     // [k][lane]
+  uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
   for (int w = warp; w < nrw; w += kBuildWarps) {
     const int u = w * 32 + lane;
     const bool act = u < T.H;
     int cnt = 0, a = -1, pos = -1, nband = 0;
     if (act) {
-      int ho = 0;                                // hit-list word offset (k * 32)
-      const int hlast = (kHitCap - 1) * 32;
+      // hit list: entry k of this lane's row at shared byte address hbase + 64 k
+      const uint32_t hbase = smem_u32(hits);
+      const uint32_t hend = hbase + (uint32_t)(kHitCap - 1) * 64u;
+      uint32_t ha = hbase;
       float mx = 0.f;
       int c = 0;
 #pragma unroll
@@ -713,27 +720,29 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
               h[u] = rr < p.hi2;
               mx = fmaxf(mx, h[u] ? rr : 0.f);
             }
-            const int o1 = ho + (h[0] ? 32 : 0);
-            const int o2 = o1 + (h[1] ? 32 : 0);
-            const int o3 = o2 + (h[2] ? 32 : 0);
-            hits[ho] = (uint16_t)i;
-            hits[min(o1, hlast)] = (uint16_t)(i + 1);
-            hits[min(o2, hlast)] = (uint16_t)(i + 2);
-            hits[min(o3, hlast)] = (uint16_t)(i + 3);
-            ho = min(o3 + (h[3] ? 32 : 0), hlast);
+            // absolute shared addresses; one clamp per step (the column's
+            // kHitSlack spare rows take o1..o3 past the last row)
+            const uint32_t o1 = ha + (h[0] ? 64u : 0u);
+            const uint32_t o2 = o1 + (h[1] ? 64u : 0u);
+            const uint32_t o3 = o2 + (h[2] ? 64u : 0u);
+            st_shared_u16(ha, (uint16_t)i);
+            st_shared_u16(o1, (uint16_t)(i + 1));
+            st_shared_u16(o2, (uint16_t)(i + 2));
+            st_shared_u16(o3, (uint16_t)(i + 3));
+            ha = min(o3 + (h[3] ? 64u : 0u), hend);
           }
           for (; i < s1; ++i) {
             const float4 q = cz[i];
             const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
             const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            hits[ho] = (uint16_t)i;
+            st_shared_u16(ha, (uint16_t)i);
             const bool hit = rr < p.hi2;
             mx = fmaxf(mx, hit ? rr : 0.f);
-            ho = min(ho + (hit ? 32 : 0), hlast);
+            ha = min(ha + (hit ? 64u : 0u), hend);
           }
         }
       }
-      cnt = ho >> 5;
+      cnt = (int)((ha - hbase) >> 6);
       if (cnt >= kHitCap - 1) cnt = kHitCap;        // (possible) overflow
       nband = mx >= p.lo2 ? 1 : 0;
     }
@@ -1384,7 +1393,7 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 3;
   p.ps = planar_stride;
   const int smem = kStageCap * (int)sizeof(float4) +
-                   kBuildWarps * 32 * kHitCap * (int)sizeof(uint16_t);
+                   kBuildWarps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t);
   if (smem > g_build_smem) {
     if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess) {
