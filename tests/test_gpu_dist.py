@@ -115,3 +115,30 @@ def test_deterministic_mode_bitwise(pc, dims):
     # and the physics is the reference's
     ref = _run(pc.md.MDDriver(pc.md.MDConfig(**kw), tile=False), 0)
     assert abs(a[0] - ref[0]) <= 1e-10 * abs(ref[0])
+
+
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 2)])
+def test_criterion3_256_atoms_200_steps(pc, dims):
+    """ref test_acceptance.py:79-92 at its size: 256 atoms, 200 steps, serial vs
+    2x1x1 / 2x2x2, bitwise (deterministic mode)."""
+    kw = dict(lattice_cells=4, density=0.8442, temperature=1.44, cutoff=2.5, skin=0.3,
+              rebuild_stride=10, seed=1, steps=0)
+    one = _run(pc.md.MDDriver(pc.md.MDConfig(**kw), deterministic=True), 200)
+    fab = _run(pc.dist.FabricMD(pc.md.MDConfig(**dict(kw, rank_dims=dims)),
+                                deterministic=True), 200)
+    assert np.array_equal(one, fab)
+
+
+def test_strides_transparent(pc):
+    """ref test_md.py:94-105: rebuild/skin and sort strides change nothing
+    physical (within 1e-9; bitwise in deterministic mode, where a skin pair
+    beyond rc adds an exact zero)."""
+    kw = dict(lattice_cells=6, density=0.8442, temperature=1.44, cutoff=2.5, seed=2, steps=0)
+    base = _run(pc.md.MDDriver(pc.md.MDConfig(**dict(kw, skin=0.0, rebuild_stride=1)),
+                               deterministic=True), 40)
+    for extra in (dict(skin=0.3, rebuild_stride=5), dict(skin=0.3, rebuild_stride=5,
+                                                          sort_stride=10)):
+        got = _run(pc.md.MDDriver(pc.md.MDConfig(**dict(kw, **extra)), deterministic=True), 40)
+        assert np.max(np.abs(got - base) / np.abs(base)) <= 1e-9
+    tile = _run(pc.md.MDDriver(pc.md.MDConfig(**dict(kw, skin=0.3, rebuild_stride=5))), 40)
+    assert np.max(np.abs(tile - base) / np.abs(base)) <= 1e-6
