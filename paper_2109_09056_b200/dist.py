@@ -329,24 +329,36 @@ class DomainEngine:
         return buf
 
     def migrate_in(self, inbox):
-        """Arrivals by ascending source rank, own stayers at position rank."""
+        """Arrivals by ascending source rank, own stayers at position rank
+        (decomp.py:100-112); stayers are gathered straight into place."""
         e0 = self._t0()
         order, starts = self._mig_order, self._mig_starts
-        blocks = []
+        parts = []                                 # (src, rows or None, m)
         for src in range(self.fabric.n_ranks):
             if src == self.rank:
-                a, b = int(starts[src]), int(starts[src + 1])
-                if b > a:
-                    blocks.append(self._pack_mig(order[a:b]))
+                m = int(starts[src + 1]) - int(starts[src])
+                if m:
+                    parts.append((src, None, m))
             elif src in inbox and inbox[src].shape[0]:
-                blocks.append(inbox[src])
-        rows = torch.cat(blocks) if blocks else torch.empty((0, MIG_W), dtype=torch.float64,
-                                                             device=self.device)
-        n = rows.shape[0]
+                parts.append((src, inbox[src], int(inbox[src].shape[0])))
+        n = sum(m for _, _, m in parts)
         self._ensure(n + 1)
-        self.pos[:n, :3] = rows[:, 0:3]
-        self.pos[:n, 3] = rows[:, 6]
-        self.vel[:, :n] = rows[:, 3:6].t()
+        new_pos = torch.empty_like(self.pos)
+        new_pos[self.cap] = self.pos[self.cap]
+        new_vel = torch.empty_like(self.vel)
+        at = 0
+        for src, rows, m in parts:
+            if rows is None:
+                idx = order[int(starts[src]):int(starts[src + 1])].contiguous()
+                _kernels.gather_rows(self.pos, idx, m, out=new_pos[at:at + m])
+                for a in range(3):
+                    _kernels.gather_rows(self.vel[a], idx, m, out=new_vel[a, at:at + m])
+            else:
+                new_pos[at:at + m, :3] = rows[:, 0:3]
+                new_pos[at:at + m, 3] = rows[:, 6]
+                new_vel[:, at:at + m] = rows[:, 3:6].t()
+            at += m
+        self.pos, self.vel = new_pos, new_vel
         self.n_owned = self.n_total = n
         self.is_ghost[: self.cap].zero_()
         self._t1("migrate", e0)
