@@ -263,6 +263,10 @@ def run_ours(args):
             traffic = json.load(f).get("bytes_per_launch_per_atom")
             traffic = None if traffic is None else traffic * n
 
+    # the device leg's engine goes back to PyTorch's caching allocator, so the
+    # end-to-end leg (a fresh engine through the public API) allocates from a
+    # warm pool, as a process calling run_md repeatedly does
+    del drv, eng
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(pc, kw, args.e2e_steps or K, world)
