@@ -384,9 +384,12 @@ class DomainEngine:
              ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
         table = torch.as_tensor(o["shift"]).to(self.device)
         per_dest = {}
+        # all offsets' scans first, then one device->host read of the totals
+        scans = [_kernels.scan_i32(flags[k]) for k in range(ns)]
+        totals = torch.stack([sc[n] for sc in scans]).cpu().tolist()
         for k, dst in enumerate(o["dests"]):           # offsets in product order
-            pos = _kernels.scan_i32(flags[k])
-            m = int(pos[n].item())
+            pos = scans[k]
+            m = int(totals[k])
             if m == 0:
                 continue
             ix = torch.empty(m, dtype=torch.int32, device=self.device)
