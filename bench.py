@@ -293,7 +293,10 @@ def run_ours(args):
                              "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                              "kernel": kname,
                              "bytes_per_atom": bytes_per_atom, "peak_kind": peak_kind,
-                             "avg_launch_us": force_avg_s * 1e6},
+                             "avg_launch_us": force_avg_s * 1e6,
+                             "limiter": "not HBM: instruction issue (~64 % active) and "
+                                        "shared-memory wavefronts (~55 %) of the exact "
+                                        "FP64 pair test (ncu, profiles/, DESIGN.md §5)"},
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu,
