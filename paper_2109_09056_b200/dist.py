@@ -36,7 +36,7 @@ from . import _kernels, _lib
 from ._lib import call, ptr, stream
 from .decomp import DomainFabric, decompose
 from .geometry import Box
-from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _TILE_ORDER, _lj_params, _PhaseTimer, \
+from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, _tile_order_kind, \
     fcc_lattice, initial_velocities
 
 MIG_W = 7     # migrate row: x, y, z, vx, vy, vz, gid (int64 bits)
@@ -544,7 +544,7 @@ class DomainEngine:
             self.tile_failures += 1
             return False
         call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds), ptr(self._tlist),
-             self._q8, _TILE_ORDER, s)
+             self._q8, _tile_order_kind(self.cfg.rebuild_stride), s)
         self.mode = "tile"
         self.used_staged = True
         return True
