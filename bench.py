@@ -269,7 +269,9 @@ def run_ours(args):
     del drv, eng
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(pc, kw, args.e2e_steps or K, world)
+        e2e = run_e2e(pc, kw, args.e2e_steps or K, world,
+                      dict(tile=args.path == "tile", half_list=args.list == "half",
+                           planar_gather=args.gather == "planar"))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -306,7 +308,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(pc, kw, steps, world):
+def run_e2e(pc, kw, steps, world, driver_options=None):
     """Same metric through the public API with host buffers: pinned host x, v
     uploaded inside the timed region, then `pc.md.run_md` (the reference's
     run_md contract: every step's KE/PE/E_total/temperature row, returned to
@@ -321,7 +323,7 @@ def run_e2e(pc, kw, steps, world):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    rows, _ = pc.md.run_md(cfg, state=(x, v), time_phases=False)
+    rows, _ = pc.md.run_md(cfg, state=(x, v), time_phases=False, **(driver_options or {}))
     e1.record()
     e1.synchronize()
     assert len(rows) == steps + 1

@@ -645,7 +645,8 @@ class MDDriver:
             self._timer.totals[k] = float(v)
 
 
-def run_md(cfg: MDConfig, state=None, time_phases: bool = True, deterministic: bool = False):
+def run_md(cfg: MDConfig, state=None, time_phases: bool = True, deterministic: bool = False,
+           **driver_options):
     """Run the NVE loop; returns (per-step diagnostic rows, phase timings)
     (ref md.py:295-307).  The per-step energies are reduced on the device
     into a history buffer and read back once after the loop (the reference
@@ -653,8 +654,10 @@ def run_md(cfg: MDConfig, state=None, time_phases: bool = True, deterministic: b
     for the host.  An overlap detected in any step raises FloatingPointError
     after the loop.  `state`: optional host (x, v) in global-id order.
     `deterministic`: the id-ordered engine, bitwise equal to
-    FabricMD / DistMD(deterministic=True) on any rank grid."""
-    drv = MDDriver(cfg, state=state, time_phases=time_phases, deterministic=deterministic)
+    FabricMD / DistMD(deterministic=True) on any rank grid.  `driver_options`:
+    MDDriver's engine choices (tile, half_list, planar_gather)."""
+    drv = MDDriver(cfg, state=state, time_phases=time_phases, deterministic=deterministic,
+                   **driver_options)
     drv.timings = {k: 0.0 for k in PHASES}
     hist = torch.empty((cfg.steps + 1, 5), dtype=torch.float64, device=drv.device)
     drv.device_diagnostics(out=hist[0])
