@@ -512,3 +512,26 @@ def test_md_engine_empty_tiles(pc, oracle):
                                [True] * 3, 1.0, 1.0, 2.5)
     assert force_err_ratio(f, fref) < 1.0
     assert drv.tile_failures == 0
+
+
+def test_md_engine_non_unit_sigma_epsilon(pc, oracle):
+    """sigma != 1 takes the tile force kernel's general-sigma instantiation;
+    epsilon scales forces and energies (ref md.py:89-96) -- vs the oracle's
+    FP64 lj_forces on the same positions."""
+    import torch
+    cfg = pc.md.MDConfig(lattice_cells=12, density=0.7, temperature=1.2, cutoff=2.6, skin=0.3,
+                         rebuild_stride=10, seed=4, steps=0, sigma=1.05, epsilon=0.8)
+    drv = pc.md.MDDriver(cfg)
+    assert drv.mode == "tile"
+    for s in range(1, 13):
+        drv.step(s)
+    x, _ = drv.gather_state()
+    ids = drv.pos[: drv.n, 3].contiguous().view(torch.int64).cpu().numpy()
+    f = np.empty((drv.n, 3))
+    f[ids] = drv.frc[:, : drv.n].cpu().numpy().T
+    pi, pj = oracle.neighbor_pairs(x, drv.box.low, drv.box.high, [True] * 3, 2.6 * 1.0000001)
+    fref, peref = oracle.lj_forces(x, np.arange(drv.n), drv.n, pi, pj, drv.box.lengths,
+                                   [True] * 3, 0.8, 1.05, 2.6)
+    assert force_err_ratio(f, fref) < 1.0
+    d = drv.diagnostics()
+    assert abs(d["PE"] - peref.sum()) <= ENERGY_TOL * abs(peref.sum())
