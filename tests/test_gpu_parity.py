@@ -535,3 +535,27 @@ def test_md_engine_non_unit_sigma_epsilon(pc, oracle):
     assert force_err_ratio(f, fref) < 1.0
     d = drv.diagnostics()
     assert abs(d["PE"] - peref.sum()) <= ENERGY_TOL * abs(peref.sum())
+
+
+def test_md_engine_tile_overflow_falls_back(pc, oracle):
+    """Dense system (rho = 1.4, ~3000-slot tile neighbourhoods > the 2304-slot
+    staging capacity): the speculatively launched tile force is discarded, the
+    velocities restored and the step redone on the SELL path -- forces still
+    match the oracle."""
+    import torch
+    cfg = pc.md.MDConfig(lattice_cells=12, density=1.4, temperature=1.0, cutoff=2.5, skin=0.3,
+                         rebuild_stride=10, seed=6, steps=0)
+    drv = pc.md.MDDriver(cfg)
+    assert drv.tile_failures >= 1 and drv.mode == "sell"
+    e0 = drv.diagnostics()["E_total"]
+    for s in range(1, 21):
+        drv.step(s)
+    x, _ = drv.gather_state()
+    ids = drv.pos[: drv.n, 3].contiguous().view(torch.int64).cpu().numpy()
+    f = np.empty((drv.n, 3))
+    f[ids] = drv.frc[:, : drv.n].cpu().numpy().T
+    pi, pj = oracle.neighbor_pairs(x, drv.box.low, drv.box.high, [True] * 3, 2.5 * 1.0000001)
+    fref, _ = oracle.lj_forces(x, np.arange(drv.n), drv.n, pi, pj, drv.box.lengths,
+                               [True] * 3, 1.0, 1.0, 2.5)
+    assert force_err_ratio(f, fref) < 1.0
+    assert abs(drv.diagnostics()["E_total"] - e0) < 1e-2 * abs(e0)
