@@ -409,6 +409,12 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride,
                        double dtm, double dt, const pc_box* box,
                        double* d_planar /* optional x|y|z planar copy, or NULL */,
                        int64_t planar_stride, void* stream);
+/* Rebuild permutation in one pass: row k of d_pos4_out / d_v_out (planar
+ * velocities, stride v_stride) <- row d_order[k] of d_pos4 / d_v, and the
+ * planar x | y | z copy of the new rows into d_planar (planar_stride). */
+int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_pos4, double* d_pos4_out,
+                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar,
+                  int64_t planar_stride, void* stream);
 /* planar[a*stride + i] = pos4[i].a for a = x, y, z. */
 int pc_pos_planar(const double* d_pos, int32_t n, double* d_planar, int64_t planar_stride,
                   void* stream);

@@ -42,6 +42,26 @@ __global__ void pos_planar_kernel(const double* __restrict__ pos, int n,
   planar[2 * ps + i] = p.z;
 }
 
+// Rebuild permutation in one pass (ref md.py:169-188 sort + the planar copy):
+// dst row k <- src row order[k] for pos4 (x, y, z, id) and the planar
+// velocities, and the planar x | y | z staging copy of the new pos4.
+__global__ void md_permute_kernel(const int* __restrict__ order, int n,
+                                  const double* __restrict__ pos4, double* __restrict__ pos4_out,
+                                  const double* __restrict__ v, double* __restrict__ v_out,
+                                  int64_t vs, double* __restrict__ pl, int64_t ps) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int j = order[k];
+  const double4 p = ld_pos4(pos4 + 4 * (int64_t)j);
+  reinterpret_cast<double4*>(pos4_out)[k] = p;
+  pl[k] = p.x;
+  pl[ps + k] = p.y;
+  pl[2 * ps + k] = p.z;
+  v_out[k] = v[j];
+  v_out[vs + k] = v[vs + j];
+  v_out[2 * vs + k] = v[2 * vs + j];
+}
+
 __global__ void __launch_bounds__(kIntThreads)
 kick_kernel(double* __restrict__ v, int64_t vs, const double* __restrict__ f, int64_t fs, int n,
             double dtm, double mass, double* __restrict__ partial) {
@@ -149,6 +169,15 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride, const doubl
                            as_stream(stream)>>>(d_pos, d_v, v_stride, d_f3, f_stride, n, dtm, dt,
                                                 *box, d_planar, planar_stride);
   return check_launch("pc_kick_drift_wrap");
+}
+
+int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_pos4, double* d_pos4_out,
+                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar,
+                  int64_t planar_stride, void* stream) {
+  if (n <= 0) return PC_OK;
+  md_permute_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0, as_stream(stream)>>>(
+      d_order, n, d_pos4, d_pos4_out, d_v, d_v_out, v_stride, d_planar, planar_stride);
+  return check_launch("pc_md_permute");
 }
 
 int pc_pos_planar(const double* d_pos, int32_t n, double* d_planar, int64_t planar_stride,

@@ -341,12 +341,11 @@ class MDDriver:
             order = torch.empty_like(srt.order)
             call("pc_cell_zsort", ptr(self.pos), ptr(srt.cell_start), self._grid.ncells,
                  ptr(srt.order), ptr(order), s)
-        _kernels.gather_rows(self.pos, order, n, out=self._pos_alt)
-        for a in range(3):
-            _kernels.gather_rows(self.vel[a], order, n, out=self._vel_alt[a])
+        # pos4, velocities and the planar staging copy in one pass
+        call("pc_md_permute", ptr(order), n, ptr(self.pos), ptr(self._pos_alt), ptr(self.vel),
+             ptr(self._vel_alt), self.vel.stride(0), ptr(self.pl), self._ps, s)
         self.pos, self._pos_alt = self._pos_alt, self.pos
         self.vel, self._vel_alt = self._vel_alt, self.vel
-        call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
         e0 = self._t0()
         self._cell_start = srt.cell_start
