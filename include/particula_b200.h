@@ -148,6 +148,11 @@ int pc_partition_place(const int32_t* d_keys, int64_t n, int32_t nbins, const in
 int pc_bin_place(const int32_t* d_cell_of, int64_t n, const int32_t* d_cell_start,
                  int32_t ncells, int32_t* d_cell_fill, int32_t* d_order_tmp,
                  int32_t* d_order, void* stream);
+/* pc_bin_place without the within-cell stabilisation (order inside a cell
+ * arbitrary): for callers that re-sort every cell anyway (pc_cell_zsort,
+ * which ranks by (z, particle index)). */
+int pc_bin_place_unstable(const int32_t* d_cell_of, int64_t n, const int32_t* d_cell_start,
+                          int32_t* d_cell_fill, int32_t* d_order, void* stream);
 
 /* map[order[k]] = k  (Permutation.map of ref binning.py:13-33). */
 int pc_invert_order(const int32_t* d_order, int64_t n, int64_t* d_map,

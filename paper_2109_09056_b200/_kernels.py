@@ -78,7 +78,7 @@ class CellSort:
     per-cell stabilisation).  ``order[dst] = src``.
     """
 
-    def __init__(self, x, x_stride, grid, check_inside=False):
+    def __init__(self, x, x_stride, grid, check_inside=False, stable=True):
         dev = x.device
         n = x.numel() // x_stride if x.numel() else 0
         self.n = n
@@ -92,10 +92,14 @@ class CellSort:
         self.counts = counts
         self.cell_start = scan_i32(counts)
         fill = torch.zeros(grid.ncells, dtype=torch.int32, device=dev)
-        tmp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        call("pc_bin_place", ptr(self.cell_of), n, ptr(self.cell_start), grid.ncells,
-             ptr(fill), ptr(tmp), ptr(self.order), s)
+        if stable:
+            tmp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            call("pc_bin_place", ptr(self.cell_of), n, ptr(self.cell_start), grid.ncells,
+                 ptr(fill), ptr(tmp), ptr(self.order), s)
+        else:                        # the caller re-sorts every cell (pc_cell_zsort)
+            call("pc_bin_place_unstable", ptr(self.cell_of), n, ptr(self.cell_start),
+                 ptr(fill), ptr(self.order), s)
 
     def outside(self) -> bool:
         return bool(int(self.flag.item()) & _lib.FLAG_OUTSIDE)

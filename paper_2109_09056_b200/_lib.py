@@ -80,6 +80,7 @@ SIGNATURES = {
     "pc_scan_i32_i64": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "pc_scan_tmp_bytes": (c_i64, [c_i64]),
     "pc_bin_place": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pc_bin_place_unstable": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "pc_partition_chunks": (c_i64, [c_i64]),
     "pc_partition_hist": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_partition_place": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),

@@ -490,6 +490,14 @@ int pc_bin_place(const int32_t* d_cell_of, int64_t n, const int32_t* d_cell_star
   return check_launch("pc_bin_place", 2);
 }
 
+int pc_bin_place_unstable(const int32_t* d_cell_of, int64_t n, const int32_t* d_cell_start,
+                          int32_t* d_cell_fill, int32_t* d_order, void* stream) {
+  if (n <= 0) return PC_OK;
+  bin_place_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_cell_of, n, d_cell_start, d_cell_fill, d_order);
+  return check_launch("pc_bin_place_unstable");
+}
+
 int pc_invert_order(const int32_t* d_order, int64_t n, int64_t* d_map, void* stream) {
   if (n <= 0) return PC_OK;
   invert_order_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_order, n,

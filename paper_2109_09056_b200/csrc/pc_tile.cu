@@ -817,14 +817,18 @@ cell_zsort_kernel(const double* __restrict__ pos4, const int* __restrict__ cs, i
     const int t = t0 + lane;
     const int src = t < m ? order[s0 + t] : 0;
     const double z = t < m ? pos4[4 * (int64_t)src + 2] : 0.0;
+    // rank by (z, particle index): independent of the input order inside
+    // the cell, so the placement before it need not be stable
     int rk = 0;
     for (int u0 = 0; u0 < m; u0 += 32) {
       const int uu = u0 + lane;
-      const double zu_l = uu < m ? pos4[4 * (int64_t)order[s0 + uu] + 2] : 0.0;
+      const int su_l = uu < m ? order[s0 + uu] : 0;
+      const double zu_l = uu < m ? pos4[4 * (int64_t)su_l + 2] : 0.0;
       const int lim = min(32, m - u0);
       for (int v = 0; v < lim; ++v) {
         const double zu = __shfl_sync(0xffffffffu, zu_l, v);
-        rk += (zu < z || (zu == z && u0 + v < t)) ? 1 : 0;
+        const int su = __shfl_sync(0xffffffffu, su_l, v);
+        rk += (zu < z || (zu == z && su < src)) ? 1 : 0;
       }
     }
     if (t < m) out[s0 + rk] = src;

@@ -440,10 +440,10 @@ class DomainEngine:
         n = self.n_total
         s = stream()
         e0 = self._t0()
-        srt = _kernels.CellSort(self.binpos[:n], 4, self._grid)
-        order = srt.order
         tile = self.tile and n > 0 and min(self._grid.nc[0], self._grid.nc[1],
                                            self._grid.nc[2]) >= 3
+        srt = _kernels.CellSort(self.binpos[:n], 4, self._grid, stable=not tile)
+        order = srt.order
         if tile:
             # z-sorted cells (local frame): the tile path's staged columns and
             # home rows are z-sorted slot runs (pc_tile.cu)

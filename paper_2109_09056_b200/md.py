@@ -333,9 +333,11 @@ class MDDriver:
         n, s = self.n, stream()
         e0 = self._t0()
         self._sync_pos4()
-        srt = _kernels.CellSort(self.pos[:n], 4, self._grid)     # excludes the dummy row
+        zsort = self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3
+        # (the z-sort re-ranks every cell: the placement need not be stable)
+        srt = _kernels.CellSort(self.pos[:n], 4, self._grid, stable=not zsort)
         order = srt.order
-        if self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3:
+        if zsort:
             # z-sorted cells: staged columns / home rows of the tile path are
             # z-sorted slot runs (pc_tile.cu)
             order = torch.empty_like(srt.order)
