@@ -397,7 +397,10 @@ partition_hist_kernel(const int* __restrict__ keys, int64_t n, int nbins, int nc
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kPartChunk + threadIdx.x;
-  if (i < n) atomicAdd(&h[keys[i]], 1);
+  if (i < n) {
+    const int k = keys[i];
+    if ((unsigned)k < (unsigned)nbins) atomicAdd(&h[k], 1);     // (out of range: dropped)
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < nbins; b += blockDim.x)
     hist[(int64_t)b * nchunks + blockIdx.x] = h[b];
@@ -410,7 +413,8 @@ partition_place_kernel(const int* __restrict__ keys, int64_t n, int nbins, int n
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int b = lane; b < nbins; b += 32) wc[warp][b] = 0;
   const int64_t i = (int64_t)blockIdx.x * kPartChunk + threadIdx.x;
-  const int key = i < n ? keys[i] : -1;
+  const int kraw = i < n ? keys[i] : -1;
+  const int key = (unsigned)kraw < (unsigned)nbins ? kraw : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, key);
   const int rank = __popc(peers & ((1u << lane) - 1u));
   __syncwarp();

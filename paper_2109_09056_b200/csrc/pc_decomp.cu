@@ -38,6 +38,7 @@ __global__ void owner_kernel(const double* __restrict__ x, int64_t n, int d, pc_
     double q = floor(__ddiv_rn(__dsub_rn(v, g.low[a]), g.width[a]));
     int ci = (int)q;
     if (q >= (double)g.nc[a]) ci = g.nc[a] - 1;
+    if (!(q >= 0.0)) ci = 0;            // outside (flagged): keep the owner a valid rank
     c[a] = ci;
   }
   if (outside) atomicOr(flag, kFlagOutside);

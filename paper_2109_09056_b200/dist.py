@@ -300,10 +300,14 @@ class DomainEngine:
         if n:
             call("pc_owner_of", ptr(x), n, 3, self.fabric.pc_grid(), ptr(owner), ptr(flag),
                  stream())
-            if int(flag.item()):
-                raise ValueError("position outside global box")
-        from .decomp import _group_by
-        order, starts = _group_by(owner[:n], self.fabric.n_ranks)
+        # stable grouping by owner (decomp.py:97-99); the group starts and the
+        # outside-box flag come back in one device->host read
+        nr = self.fabric.n_ranks
+        order, starts_d = _kernels.stable_partition(owner[:n], nr)
+        host = torch.cat([starts_d.to(torch.int32), flag]).cpu().numpy()
+        if host[nr + 1]:
+            raise ValueError("position outside global box")
+        starts = host[: nr + 1].astype(np.int64)
         self._mig_order, self._mig_starts = order, starts
         out = {}
         for dst in range(self.fabric.n_ranks):
