@@ -108,6 +108,11 @@ int pc_bin_count(const double* d_x, int64_t n, int32_t x_stride,
                  const pc_grid* grid, int32_t check_inside, int32_t* d_cell_of,
                  int64_t* d_axis_idx /* (n, ndim) per-axis cells or NULL */,
                  int32_t* d_cell_count, int32_t* d_flag, void* stream);
+/* pc_bin_count of planar x | y | z positions (3-D, no axis indices, no
+ * inside check): the MD engine bins straight from its staging copy. */
+int pc_bin_count_planar(const double* d_planar, int64_t planar_stride, int64_t n,
+                        const pc_grid* grid, int32_t* d_cell_of, int32_t* d_cell_count,
+                        int32_t* d_flag, void* stream);
 
 /* Digit "cells" of int64 keys for the LSD passes of bin_by_key
  * (ref binning.py:49-55): cell = ((key[perm[i]] - kmin) >> shift) & mask. */
@@ -277,8 +282,8 @@ int32_t pc_tile_count(const pc_grid* grid);
  * d_order[cs[c] .. cs[c+1]); d_out lists the same particles ranked by
  * (z of d_pos4 row, position in the cell).  The tile path relies on it:
  * staged columns and home rows become z-sorted runs. */
-int pc_cell_zsort(const double* d_pos4, const int32_t* d_cell_start, int32_t ncells,
-                  const int32_t* d_order, int32_t* d_out, void* stream);
+int pc_cell_zsort(const double* d_z, int64_t z_stride, const int32_t* d_cell_start,
+                  int32_t ncells, const int32_t* d_order, int32_t* d_out, void* stream);
 int32_t pc_tile_plan_ints(void);
 int32_t pc_tile_stage_cap(void);
 int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw,
@@ -414,12 +419,13 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride,
                        double dtm, double dt, const pc_box* box,
                        double* d_planar /* optional x|y|z planar copy, or NULL */,
                        int64_t planar_stride, void* stream);
-/* Rebuild permutation in one pass: row k of d_pos4_out / d_v_out (planar
- * velocities, stride v_stride) <- row d_order[k] of d_pos4 / d_v, and the
- * planar x | y | z copy of the new rows into d_planar (planar_stride). */
-int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_pos4, double* d_pos4_out,
-                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar,
-                  int64_t planar_stride, void* stream);
+/* Rebuild permutation in one pass: row k of d_pos4_out (x, y, z from the
+ * planar d_planar, the id from d_pos4 .w), of d_v_out (planar velocities,
+ * stride v_stride) and of the planar d_planar_out <- row d_order[k]. */
+int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_planar,
+                  int64_t planar_stride, const double* d_pos4, double* d_pos4_out,
+                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar_out,
+                  void* stream);
 /* planar[a*stride + i] = pos4[i].a for a = x, y, z. */
 int pc_pos_planar(const double* d_pos, int32_t n, double* d_planar, int64_t planar_stride,
                   void* stream);

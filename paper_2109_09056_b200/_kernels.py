@@ -78,17 +78,22 @@ class CellSort:
     per-cell stabilisation).  ``order[dst] = src``.
     """
 
-    def __init__(self, x, x_stride, grid, check_inside=False, stable=True):
+    def __init__(self, x, x_stride, grid, check_inside=False, stable=True, planar=None):
         dev = x.device
-        n = x.numel() // x_stride if x.numel() else 0
+        # planar=(pl, ps, n): bin straight from a planar x | y | z copy
+        n = planar[2] if planar is not None else (x.numel() // x_stride if x.numel() else 0)
         self.n = n
         self.grid = grid
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.cell_of = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         counts = torch.zeros(grid.ncells, dtype=torch.int32, device=dev)
         s = stream()
-        call("pc_bin_count", ptr(x), n, x_stride, grid, int(check_inside), ptr(self.cell_of),
-             None, ptr(counts), ptr(self.flag), s)
+        if planar is not None:
+            call("pc_bin_count_planar", ptr(planar[0]), planar[1], n, grid, ptr(self.cell_of),
+                 ptr(counts), ptr(self.flag), s)
+        else:
+            call("pc_bin_count", ptr(x), n, x_stride, grid, int(check_inside),
+                 ptr(self.cell_of), None, ptr(counts), ptr(self.flag), s)
         self.counts = counts
         self.cell_start = scan_i32(counts)
         fill = torch.zeros(grid.ncells, dtype=torch.int32, device=dev)

@@ -97,8 +97,10 @@ SIGNATURES = {
     "pc_lj_force_sell_half": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32,
                                              ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl,
                                              c_vp, c_i64, c_vp, c_vp, c_vp]),
-    "pc_md_permute": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64,
-                                     c_vp]),
+    "pc_md_permute": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                     c_vp, c_vp]),
+    "pc_bin_count_planar": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(PcGrid), c_vp,
+                                           c_vp, c_vp, c_vp]),
     "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
     "pc_owner_of": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_vp,
                                    c_vp]),
@@ -113,7 +115,7 @@ SIGNATURES = {
     "pc_halo_pack_planar": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "pc_tile_count": (c_i32, [ctypes.POINTER(PcGrid)]),
     "pc_tile_plan_ints": (c_i32, []),
-    "pc_cell_zsort": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "pc_cell_zsort": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pc_tile_stage_cap": (c_i32, []),
     "pc_tile_rows": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp]),
     "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),

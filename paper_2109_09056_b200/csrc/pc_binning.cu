@@ -7,9 +7,10 @@ namespace pc {
 
 // ---- K1: cell id + count -------------------------------------------------
 __global__ void __launch_bounds__(256)
-bin_count_kernel(const double* __restrict__ x, int64_t n, int x_stride, pc_grid g,
-                 int check_inside, int* __restrict__ cell_of, int64_t* __restrict__ axis_idx,
-                 int* __restrict__ cell_count, int* __restrict__ flag) {
+bin_count_kernel(const double* __restrict__ x, int64_t n, int x_stride, int64_t a_stride,
+                 pc_grid g, int check_inside, int* __restrict__ cell_of,
+                 int64_t* __restrict__ axis_idx, int* __restrict__ cell_count,
+                 int* __restrict__ flag) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int cell = -1;
   if (i < n) {
@@ -17,7 +18,7 @@ bin_count_kernel(const double* __restrict__ x, int64_t n, int x_stride, pc_grid 
     int c[3] = {0, 0, 0};
     bool outside = false;
     for (int a = 0; a < g.ndim; ++a) {
-      double v = p[a];
+      double v = p[a * a_stride];
       outside |= (v < g.low[a]) || (v > g.high[a]);
       c[a] = cell_coord(v, g.low[a], g.width[a], g.nc[a]);
       if (axis_idx) axis_idx[i * g.ndim + a] = c[a];
@@ -318,10 +319,25 @@ int pc_bin_count(const double* d_x, int64_t n, int32_t x_stride, const pc_grid* 
     return PC_ERR_VALUE;
   }
   unsigned blocks = (unsigned)((n + 255) / 256);
-  bin_count_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_x, n, x_stride, *grid, check_inside,
-                                                          d_cell_of, d_axis_idx, d_cell_count,
-                                                          d_flag);
+  bin_count_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_x, n, x_stride, 1, *grid,
+                                                          check_inside, d_cell_of, d_axis_idx,
+                                                          d_cell_count, d_flag);
   return check_launch("pc_bin_count");
+}
+
+int pc_bin_count_planar(const double* d_planar, int64_t planar_stride, int64_t n,
+                        const pc_grid* grid, int32_t* d_cell_of, int32_t* d_cell_count,
+                        int32_t* d_flag, void* stream) {
+  if (n <= 0) return PC_OK;
+  if (grid->ndim != 3) {
+    set_error("pc_bin_count_planar: 3-D only");
+    return PC_ERR_VALUE;
+  }
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  bin_count_kernel<<<blocks, 256, 0, as_stream(stream)>>>(d_planar, n, 1, planar_stride, *grid,
+                                                          0, d_cell_of, nullptr, d_cell_count,
+                                                          d_flag);
+  return check_launch("pc_bin_count_planar");
 }
 
 int pc_key_digits(const int64_t* d_keys, const int32_t* d_perm, int64_t n, int64_t kmin,

@@ -43,20 +43,23 @@ __global__ void pos_planar_kernel(const double* __restrict__ pos, int n,
 }
 
 // Rebuild permutation in one pass (ref md.py:169-188 sort + the planar copy):
-// dst row k <- src row order[k] for pos4 (x, y, z, id) and the planar
-// velocities, and the planar x | y | z staging copy of the new pos4.
+// dst row k <- src row order[k]: x, y, z from the current planar positions,
+// the id from pos4 .w, the planar velocities; writes the new pos4 rows and
+// the new planar positions (a different buffer than the source).
 __global__ void md_permute_kernel(const int* __restrict__ order, int n,
+                                  const double* __restrict__ pl, int64_t ps,
                                   const double* __restrict__ pos4, double* __restrict__ pos4_out,
                                   const double* __restrict__ v, double* __restrict__ v_out,
-                                  int64_t vs, double* __restrict__ pl, int64_t ps) {
+                                  int64_t vs, double* __restrict__ pl_out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int j = order[k];
-  const double4 p = ld_pos4(pos4 + 4 * (int64_t)j);
-  reinterpret_cast<double4*>(pos4_out)[k] = p;
-  pl[k] = p.x;
-  pl[ps + k] = p.y;
-  pl[2 * ps + k] = p.z;
+  const double x = pl[j], y = pl[ps + j], z = pl[2 * ps + j];
+  const double w = pos4[4 * (int64_t)j + 3];
+  reinterpret_cast<double4*>(pos4_out)[k] = make_double4(x, y, z, w);
+  pl_out[k] = x;
+  pl_out[ps + k] = y;
+  pl_out[2 * ps + k] = z;
   v_out[k] = v[j];
   v_out[vs + k] = v[vs + j];
   v_out[2 * vs + k] = v[2 * vs + j];
@@ -171,12 +174,18 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride, const doubl
   return check_launch("pc_kick_drift_wrap");
 }
 
-int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_pos4, double* d_pos4_out,
-                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar,
-                  int64_t planar_stride, void* stream) {
+int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_planar,
+                  int64_t planar_stride, const double* d_pos4, double* d_pos4_out,
+                  const double* d_v, double* d_v_out, int64_t v_stride, double* d_planar_out,
+                  void* stream) {
   if (n <= 0) return PC_OK;
+  if (d_planar == d_planar_out) {
+    set_error("pc_md_permute: the planar source and destination must differ");
+    return PC_ERR_VALUE;
+  }
   md_permute_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0, as_stream(stream)>>>(
-      d_order, n, d_pos4, d_pos4_out, d_v, d_v_out, v_stride, d_planar, planar_stride);
+      d_order, n, d_planar, planar_stride, d_pos4, d_pos4_out, d_v, d_v_out, v_stride,
+      d_planar_out);
   return check_launch("pc_md_permute");
 }
 

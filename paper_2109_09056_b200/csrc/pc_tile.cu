@@ -807,8 +807,8 @@ __global__ void pos_from_planar_kernel(const double* __restrict__ pl, int64_t ps
 // out = the same particles ranked by (z, position in the cell).  Warp per
 // cell; z read from the unsorted pos4 rows.
 __global__ void __launch_bounds__(256)
-cell_zsort_kernel(const double* __restrict__ pos4, const int* __restrict__ cs, int ncells,
-                  const int* __restrict__ order, int* __restrict__ out) {
+cell_zsort_kernel(const double* __restrict__ zp, int64_t zs, const int* __restrict__ cs,
+                  int ncells, const int* __restrict__ order, int* __restrict__ out) {
   const int cell = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (cell >= ncells) return;
@@ -816,14 +816,14 @@ cell_zsort_kernel(const double* __restrict__ pos4, const int* __restrict__ cs, i
   for (int t0 = 0; t0 < m; t0 += 32) {
     const int t = t0 + lane;
     const int src = t < m ? order[s0 + t] : 0;
-    const double z = t < m ? pos4[4 * (int64_t)src + 2] : 0.0;
+    const double z = t < m ? zp[zs * src] : 0.0;
     // rank by (z, particle index): independent of the input order inside
     // the cell, so the placement before it need not be stable
     int rk = 0;
     for (int u0 = 0; u0 < m; u0 += 32) {
       const int uu = u0 + lane;
       const int su_l = uu < m ? order[s0 + uu] : 0;
-      const double zu_l = uu < m ? pos4[4 * (int64_t)su_l + 2] : 0.0;
+      const double zu_l = uu < m ? zp[zs * su_l] : 0.0;
       const int lim = min(32, m - u0);
       for (int v = 0; v < lim; ++v) {
         const double zu = __shfl_sync(0xffffffffu, zu_l, v);
@@ -1341,11 +1341,11 @@ int pc_pos_from_planar(const double* d_planar, int64_t planar_stride, int32_t n,
   return check_launch("pc_pos_from_planar");
 }
 
-int pc_cell_zsort(const double* d_pos4, const int32_t* d_cell_start, int32_t ncells,
-                  const int32_t* d_order, int32_t* d_out, void* stream) {
+int pc_cell_zsort(const double* d_z, int64_t z_stride, const int32_t* d_cell_start,
+                  int32_t ncells, const int32_t* d_order, int32_t* d_out, void* stream) {
   if (ncells <= 0) return PC_OK;
-  cell_zsort_kernel<<<(ncells + 7) / 8, 256, 0, as_stream(stream)>>>(d_pos4, d_cell_start, ncells,
-                                                                     d_order, d_out);
+  cell_zsort_kernel<<<(ncells + 7) / 8, 256, 0, as_stream(stream)>>>(d_z, z_stride, d_cell_start,
+                                                                     ncells, d_order, d_out);
   return check_launch("pc_cell_zsort");
 }
 

@@ -452,8 +452,8 @@ class DomainEngine:
             # z-sorted cells (local frame): the tile path's staged columns and
             # home rows are z-sorted slot runs (pc_tile.cu)
             order = torch.empty_like(srt.order)
-            call("pc_cell_zsort", ptr(self.binpos), ptr(srt.cell_start), self._grid.ncells,
-                 ptr(srt.order), ptr(order), s)
+            call("pc_cell_zsort", ptr(self.binpos[:, 2]), 4, ptr(srt.cell_start),
+                 self._grid.ncells, ptr(srt.order), ptr(order), s)
         new_pos = torch.empty_like(self.pos)
         new_pos[self.cap] = self.pos[self.cap]
         _kernels.gather_rows(self.pos, order, n, out=new_pos)

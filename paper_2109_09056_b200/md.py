@@ -300,6 +300,8 @@ class MDDriver:
         self.rebuilds = 0
         # the lattice lies in [0, L): the reference's initial migrate wrap
         # (decomp.py:90-91) is the identity on it
+        # the rebuild bins from the planar copy: fill it from the initial pos4
+        call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, stream())
         self._rebuild()
         self._force_step(kick_dtm=0.0)
         self._timer.reset()
@@ -332,22 +334,28 @@ class MDDriver:
         """Cell sort of all particle fields + SELL Verlet build (md.py:169-188)."""
         n, s = self.n, stream()
         e0 = self._t0()
-        self._sync_pos4()
         zsort = self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3
-        # (the z-sort re-ranks every cell: the placement need not be stable)
-        srt = _kernels.CellSort(self.pos[:n], 4, self._grid, stable=not zsort)
+        # binning, the z-sort and the permute read the planar positions (always
+        # current; pos4 x, y, z may lag behind after fused integrate steps).
+        # The z-sort re-ranks every cell: the placement need not be stable.
+        srt = _kernels.CellSort(self.pos[:n], 4, self._grid, stable=not zsort,
+                                planar=(self.pl, self._ps, n))
         order = srt.order
         if zsort:
             # z-sorted cells: staged columns / home rows of the tile path are
             # z-sorted slot runs (pc_tile.cu)
             order = torch.empty_like(srt.order)
-            call("pc_cell_zsort", ptr(self.pos), ptr(srt.cell_start), self._grid.ncells,
+            call("pc_cell_zsort", ptr(self.pl[2]), 1, ptr(srt.cell_start), self._grid.ncells,
                  ptr(srt.order), ptr(order), s)
-        # pos4, velocities and the planar staging copy in one pass
-        call("pc_md_permute", ptr(order), n, ptr(self.pos), ptr(self._pos_alt), ptr(self.vel),
-             ptr(self._vel_alt), self.vel.stride(0), ptr(self.pl), self._ps, s)
+        # pos4 (all fields current again), velocities and the planar staging
+        # copy in one pass; the new planar rows go to the spare planar buffer
+        call("pc_md_permute", ptr(order), n, ptr(self.pl), self._ps, ptr(self.pos),
+             ptr(self._pos_alt), ptr(self.vel), ptr(self._vel_alt), self.vel.stride(0),
+             ptr(self._pl_n), s)
         self.pos, self._pos_alt = self._pos_alt, self.pos
         self.vel, self._vel_alt = self._vel_alt, self.vel
+        self.pl, self._pl_n = self._pl_n, self.pl
+        self._pos_stale = False
         self._t1("sort", e0)
         e0 = self._t0()
         self._cell_start = srt.cell_start
