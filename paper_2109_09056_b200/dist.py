@@ -472,6 +472,21 @@ class DomainEngine:
                             for dst, ix in getattr(self, "_exports", {}).items()}
         self.ghost_blocks = [(src, inv32[at:at + m].contiguous())
                              for src, at, m in getattr(self, "_ghost_src", [])]
+        # the per-step refresh as one pack, one all-to-all, one unpack:
+        # exported rows concatenated by destination rank, ghost rows by source
+        world = self.fabric.n_ranks
+        self.send_split = [0] * world
+        self.recv_split = [0] * world
+        for dst, rows in self.export_rows.items():
+            self.send_split[dst] = int(rows.numel())
+        for src, rows in self.ghost_blocks:
+            self.recv_split[src] = int(rows.numel())
+        ex = [self.export_rows[d] for d in sorted(self.export_rows)]
+        gh = [rows for _, rows in self.ghost_blocks]
+        self.export_all = torch.cat(ex) if ex else torch.empty(0, dtype=torch.int32,
+                                                               device=self.device)
+        self.ghost_all = torch.cat(gh) if gh else torch.empty(0, dtype=torch.int32,
+                                                              device=self.device)
         if self.pl is not None:
             call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
@@ -568,6 +583,27 @@ class DomainEngine:
             out[dst] = buf
         self._t1("halo", e0)
         return out
+
+    def refresh_pack(self):
+        """The per-step refresh payload of all destinations in one buffer
+        (raw x, y, z of the exported rows, destination-rank order)."""
+        e0 = self._t0()
+        m = int(self.export_all.numel())
+        buf = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+        if m:
+            call("pc_halo_pack_planar", ptr(self.pl), self._ps, ptr(self.export_all), m,
+                 ptr(buf), stream())
+        self._t1("halo", e0)
+        return buf
+
+    def refresh_unpack(self, buf):
+        """Ghost rows of all sources from one received buffer (source order)."""
+        e0 = self._t0()
+        m = int(self.ghost_all.numel())
+        if m:
+            call("pc_halo_unpack", ptr(buf), ptr(self.ghost_all), m, ptr(self.pos),
+                 ptr(self.pl), self._ps, stream())
+        self._t1("halo", e0)
 
     def refresh_in(self, inbox):
         e0 = self._t0()
@@ -835,6 +871,16 @@ class NCCLTransport:
             inbox = {k: v.to(device) for k, v in inbox.items()}
         return inbox
 
+    def alltoall(self, send, send_split, recv_split, device):
+        """One all_to_all_single of (rows, 3) float64 blocks: rows for rank r
+        are send[sum(send_split[:r]) : +send_split[r]]; the received blocks
+        come back in source-rank order."""
+        out = torch.empty((sum(recv_split), send.shape[1] if send.dim() == 2 else 3),
+                          dtype=send.dtype, device="cpu" if self.host_staged else device)
+        self.dist.all_to_all_single(out, self._wire(send.contiguous()), list(recv_split),
+                                    list(send_split), group=self.group)
+        return out.to(device) if self.host_staged else out
+
     def allreduce(self, t):
         w = self._wire(t)
         self.dist.all_reduce(w, group=self.group)
@@ -905,12 +951,18 @@ class DistMD(_StepLogic):
         return [self.engine]
 
     def _exchange(self, out_name, in_name, width):
-        out = getattr(self.engine, out_name)()
-        recv = None
-        if out_name == "refresh_out":   # sizes fixed by the halo plan until the next rebuild
-            recv = {src: int(rows.numel()) for src, rows in self.engine.ghost_blocks}
-        inbox = self.transport.exchange(out, width, self.device, recv_counts=recv)
-        getattr(self.engine, in_name)(inbox)
+        e = self.engine
+        if out_name == "refresh_out":
+            # per step: one pack, one all-to-all (sizes fixed by the halo plan
+            # until the next rebuild), one unpack -- a few host calls per step
+            # whatever the number of neighbour ranks
+            buf = e.refresh_pack()
+            e.refresh_unpack(self.transport.alltoall(buf, e.send_split, e.recv_split,
+                                                      self.device))
+            return
+        out = getattr(e, out_name)()
+        inbox = self.transport.exchange(out, width, self.device)
+        getattr(e, in_name)(inbox)
 
     def diagnostics(self):
         if self.deterministic:

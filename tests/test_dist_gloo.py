@@ -38,6 +38,7 @@ def _worker(rank, world, port, q):
             rows[:, 1] = d
             rows[:, 2] = torch.arange(m, dtype=torch.float64)
             out[d] = rows
+        out_full = dict(out)
         if rank == world - 1:
             out.pop(0, None)          # a rank that sends nothing to rank 0
         inbox = t.exchange(out, 3, torch.device("cpu"))
@@ -48,6 +49,17 @@ def _worker(rank, world, port, q):
         assert sorted(again) == sorted(inbox)
         for s_ in again:
             assert torch.equal(again[s_], inbox[s_])
+        # the per-step refresh path: one all-to-all with per-rank split sizes
+        send_split = [0 if d == rank else (rank + 1) * (d + 1) for d in range(world)]
+        recv_split = [0 if s_ == rank else (s_ + 1) * (rank + 1) for s_ in range(world)]
+        send = torch.cat([out_full[d] for d in range(world) if d != rank])
+        got_a2a = t.alltoall(send, send_split, recv_split, torch.device("cpu"))
+        expect = torch.cat([torch.stack([torch.full(((s_ + 1) * (rank + 1),), float(s_)),
+                                         torch.full(((s_ + 1) * (rank + 1),), float(rank)),
+                                         torch.arange((s_ + 1) * (rank + 1),
+                                                      dtype=torch.float64)], 1)
+                            for s_ in range(world) if s_ != rank])
+        assert torch.equal(got_a2a, expect)
         red = t.allreduce(torch.tensor([float(rank), 1.0], dtype=torch.float64))
         q.put((rank, got, red.numpy().copy()))
     finally:
