@@ -186,6 +186,10 @@ class DomainEngine:
         # binning ghosts in the local frame needs every image within the
         # width.  Duplicate images never pair twice: the build's binpos
         # prefilter only accepts the image adjacent to the row particle.
+        # offsets grouped by destination rank (stable: product order within a
+        # destination), so one compaction over all offsets yields contiguous
+        # per-destination export blocks in the same order as per-offset passes
+        out = sorted(out, key=lambda ds: ds[0])
         dests = [dst for dst, _ in out]
         h_slot = np.arange(len(out), dtype=np.int32)
         h_shift = np.ascontiguousarray(np.stack([s for _, s in out])) if out else np.zeros((0, 3))
@@ -387,31 +391,30 @@ class DomainEngine:
              o["lo"].ctypes.data_as(ctypes.c_void_p), o["hi"].ctypes.data_as(ctypes.c_void_p),
              ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
         table = torch.as_tensor(o["shift"]).to(self.device)
-        per_dest = {}
-        # all offsets' scans first, then one device->host read of the totals
-        scans = [_kernels.scan_i32(flags[k]) for k in range(ns)]
-        totals = torch.stack([sc[n] for sc in scans]).cpu().tolist()
-        for k, dst in enumerate(o["dests"]):           # offsets in product order
-            pos = scans[k]
-            m = int(totals[k])
-            if m == 0:
-                continue
-            ix = torch.empty(m, dtype=torch.int32, device=self.device)
-            oc = torch.empty(m, dtype=torch.int8, device=self.device)
-            call("pc_compact", ptr(flags[k]), ptr(pos), n, ptr(ix), ptr(best[k]), ptr(oc),
-                 stream())
-            per_dest.setdefault(dst, []).append((ix, table[k].expand(m, 3)))
-        for dst in sorted(per_dest):
-            ix = torch.cat([a for a, _ in per_dest[dst]]).contiguous()
-            sh = torch.cat([b for _, b in per_dest[dst]])
-            m = ix.numel()
-            self._exports[dst] = ix
-            buf = torch.empty((m, HALO_W), dtype=torch.float64, device=self.device)
-            p = torch.empty((m, 4), dtype=torch.float64, device=self.device)
-            _kernels.gather_rows(self.pos, ix, m, out=p)
-            buf[:, 0:4] = p
-            buf[:, 4:7] = sh
-            out[dst] = buf
+        # one scan + one compaction over all offsets (flat index t = k * n + i)
+        pos = _kernels.scan_i32(flags.view(-1))
+        starts = pos[0: ns * n + 1: n].cpu().numpy()          # ns + 1 per-offset bounds
+        total = int(starts[ns])
+        if total:
+            t_idx = torch.empty(total, dtype=torch.int32, device=self.device)
+            oc = torch.empty(total, dtype=torch.int8, device=self.device)
+            call("pc_compact", ptr(flags.view(-1)), ptr(pos), ns * n, ptr(t_idx),
+                 ptr(best.view(-1)), ptr(oc), stream())
+            ix_all = (t_idx % n).to(torch.int32).contiguous()
+            k_all = (t_idx // n).to(torch.int64)
+            p = torch.empty((total, 4), dtype=torch.float64, device=self.device)
+            _kernels.gather_rows(self.pos, ix_all, total, out=p)
+            buf_all = torch.cat([p, table[k_all]], dim=1)        # (total, HALO_W)
+            k = 0
+            while k < ns:                                       # contiguous per destination
+                dst, k1 = o["dests"][k], k
+                while k1 < ns and o["dests"][k1] == dst:
+                    k1 += 1
+                a_, b_ = int(starts[k]), int(starts[k1])
+                if b_ > a_:
+                    self._exports[dst] = ix_all[a_:b_]
+                    out[dst] = buf_all[a_:b_]
+                k = k1
         self._t1("halo", e0)
         return out
 
