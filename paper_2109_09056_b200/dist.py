@@ -429,13 +429,14 @@ class DomainEngine:
         at = n
         self._ghost_src = []
         for src, b in blocks:
-            m = b.shape[0]
-            self.pos[at:at + m] = b[:, 0:4]
-            self.binpos[at:at + m, :3] = b[:, 0:3] + b[:, 4:7]
-            self.binpos[at:at + m, 3] = b[:, 3]
-            self.vel[:, at:at + m] = 0.0
-            self._ghost_src.append((src, at, m))
-            at += m
+            self._ghost_src.append((src, at, int(b.shape[0])))
+            at += int(b.shape[0])
+        if g:                                  # all sources' blocks at once
+            b = torch.cat([blk for _, blk in blocks]) if len(blocks) > 1 else blocks[0][1]
+            self.pos[n:at] = b[:, 0:4]
+            self.binpos[n:at, :3] = b[:, 0:3] + b[:, 4:7]
+            self.binpos[n:at, 3] = b[:, 3]
+            self.vel[:, n:at] = 0.0
         self.is_ghost[: self.cap].zero_()
         self.is_ghost[n:at] = 1
         self.n_total = at
