@@ -314,11 +314,20 @@ class DomainEngine:
         starts = host[: nr + 1].astype(np.int64)
         self._mig_order, self._mig_starts = order, starts
         out = {}
-        for dst in range(self.fabric.n_ranks):
-            a, b = int(starts[dst]), int(starts[dst + 1])
-            if dst == self.rank or b == a:
-                continue
-            out[dst] = self._pack_mig(order[a:b])
+        # every mover in one pack (owner order, the rank's own stayers cut out),
+        # then per-destination views
+        r0, r1 = int(starts[self.rank]), int(starts[self.rank + 1])
+        movers = [order[: r0], order[r1: int(starts[nr])]]
+        movers = [m for m in movers if m.numel()]
+        if movers:
+            idx = torch.cat(movers) if len(movers) > 1 else movers[0]
+            buf = self._pack_mig(idx)
+            for dst in range(nr):
+                a, b = int(starts[dst]), int(starts[dst + 1])
+                if dst == self.rank or b == a:
+                    continue
+                off = a if dst < self.rank else a - (r1 - r0)
+                out[dst] = buf[off: off + (b - a)]
         self._t1("migrate", e0)
         return out
 
@@ -390,7 +399,9 @@ class DomainEngine:
              o["slot"].ctypes.data_as(ctypes.c_void_p), o["shift"].ctypes.data_as(ctypes.c_void_p),
              o["lo"].ctypes.data_as(ctypes.c_void_p), o["hi"].ctypes.data_as(ctypes.c_void_p),
              ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
-        table = torch.as_tensor(o["shift"]).to(self.device)
+        if getattr(self, "_shift_dev", None) is None:       # per-offset shifts, once
+            self._shift_dev = torch.as_tensor(o["shift"]).to(self.device)
+        table = self._shift_dev
         # one scan + one compaction over all offsets (flat index t = k * n + i)
         pos = _kernels.scan_i32(flags.view(-1))
         starts = pos[0: ns * n + 1: n].cpu().numpy()          # ns + 1 per-offset bounds
