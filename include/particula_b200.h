@@ -419,6 +419,15 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride,
                        double dtm, double dt, const pc_box* box,
                        double* d_planar /* optional x|y|z planar copy, or NULL */,
                        int64_t planar_stride, void* stream);
+/* The decomposed engine's rebuild permutation: rows k of d_pos4_out,
+ * d_bin4_out (local-frame positions), d_v_out (planar, v_stride) and
+ * d_ghost_out <- rows d_order[k]; and the planar x | y | z copies of the new
+ * pos4 / bin4 rows into d_planar / d_bplanar (planar_stride). */
+int pc_domain_permute(const int32_t* d_order, int32_t n, const double* d_pos4,
+                      double* d_pos4_out, const double* d_bin4, double* d_bin4_out,
+                      const double* d_v, double* d_v_out, int64_t v_stride,
+                      const int32_t* d_ghost, int32_t* d_ghost_out, double* d_planar,
+                      double* d_bplanar, int64_t planar_stride, void* stream);
 /* Rebuild permutation in one pass: row k of d_pos4_out (x, y, z from the
  * planar d_planar, the id from d_pos4 .w), of d_v_out (planar velocities,
  * stride v_stride) and of the planar d_planar_out <- row d_order[k]. */

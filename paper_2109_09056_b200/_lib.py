@@ -97,6 +97,8 @@ SIGNATURES = {
     "pc_lj_force_sell_half": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32,
                                              ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl,
                                              c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "pc_domain_permute": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                         c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pc_md_permute": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                      c_vp, c_vp]),
     "pc_bin_count_planar": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(PcGrid), c_vp,

@@ -46,6 +46,37 @@ __global__ void pos_planar_kernel(const double* __restrict__ pos, int n,
 // dst row k <- src row order[k]: x, y, z from the current planar positions,
 // the id from pos4 .w, the planar velocities; writes the new pos4 rows and
 // the new planar positions (a different buffer than the source).
+// The decomposed engine's rebuild permutation in one pass: pos4, the
+// local-frame binpos4, planar velocities and ghost flags by order[k], plus
+// the planar x | y | z copies of both position arrays.
+__global__ void domain_permute_kernel(const int* __restrict__ order, int n,
+                                      const double* __restrict__ pos4,
+                                      double* __restrict__ pos4_out,
+                                      const double* __restrict__ bin4,
+                                      double* __restrict__ bin4_out,
+                                      const double* __restrict__ v, double* __restrict__ v_out,
+                                      int64_t vs, const int* __restrict__ ghost,
+                                      int* __restrict__ ghost_out, double* __restrict__ pl,
+                                      double* __restrict__ bpl, int64_t ps) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int j = order[k];
+  const double4 p = ld_pos4(pos4 + 4 * (int64_t)j);
+  const double4 q = ld_pos4(bin4 + 4 * (int64_t)j);
+  reinterpret_cast<double4*>(pos4_out)[k] = p;
+  reinterpret_cast<double4*>(bin4_out)[k] = q;
+  pl[k] = p.x;
+  pl[ps + k] = p.y;
+  pl[2 * ps + k] = p.z;
+  bpl[k] = q.x;
+  bpl[ps + k] = q.y;
+  bpl[2 * ps + k] = q.z;
+  v_out[k] = v[j];
+  v_out[vs + k] = v[vs + j];
+  v_out[2 * vs + k] = v[2 * vs + j];
+  ghost_out[k] = ghost[j];
+}
+
 __global__ void md_permute_kernel(const int* __restrict__ order, int n,
                                   const double* __restrict__ pl, int64_t ps,
                                   const double* __restrict__ pos4, double* __restrict__ pos4_out,
@@ -172,6 +203,19 @@ int pc_kick_drift_wrap(double* d_pos, double* d_v, int64_t v_stride, const doubl
                            as_stream(stream)>>>(d_pos, d_v, v_stride, d_f3, f_stride, n, dtm, dt,
                                                 *box, d_planar, planar_stride);
   return check_launch("pc_kick_drift_wrap");
+}
+
+int pc_domain_permute(const int32_t* d_order, int32_t n, const double* d_pos4,
+                      double* d_pos4_out, const double* d_bin4, double* d_bin4_out,
+                      const double* d_v, double* d_v_out, int64_t v_stride,
+                      const int32_t* d_ghost, int32_t* d_ghost_out, double* d_planar,
+                      double* d_bplanar, int64_t planar_stride, void* stream) {
+  if (n <= 0) return PC_OK;
+  domain_permute_kernel<<<(n + kIntThreads - 1) / kIntThreads, kIntThreads, 0,
+                          as_stream(stream)>>>(d_order, n, d_pos4, d_pos4_out, d_bin4,
+                                               d_bin4_out, d_v, d_v_out, v_stride, d_ghost,
+                                               d_ghost_out, d_planar, d_bplanar, planar_stride);
+  return check_launch("pc_domain_permute");
 }
 
 int pc_md_permute(const int32_t* d_order, int32_t n, const double* d_planar,

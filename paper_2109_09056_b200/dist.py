@@ -471,14 +471,22 @@ class DomainEngine:
                  self._grid.ncells, ptr(srt.order), ptr(order), s)
         new_pos = torch.empty_like(self.pos)
         new_pos[self.cap] = self.pos[self.cap]
-        _kernels.gather_rows(self.pos, order, n, out=new_pos)
         new_bin = torch.empty_like(self.binpos)
-        _kernels.gather_rows(self.binpos, order, n, out=new_bin)
         new_vel = torch.zeros_like(self.vel)
-        for a in range(3):
-            _kernels.gather_rows(self.vel[a], order, n, out=new_vel[a])
         new_g = torch.zeros_like(self.is_ghost)
-        _kernels.gather_rows(self.is_ghost, order, n, out=new_g)
+        self._planar_done = self.pl is not None and getattr(self, "bpl", None) is not None
+        if self._planar_done:
+            # one pass: pos4, binpos4, velocities, ghost flags + both planar copies
+            call("pc_domain_permute", ptr(order), n, ptr(self.pos), ptr(new_pos),
+                 ptr(self.binpos), ptr(new_bin), ptr(self.vel), ptr(new_vel),
+                 self.vel.stride(0), ptr(self.is_ghost), ptr(new_g), ptr(self.pl),
+                 ptr(self.bpl), self._ps, s)
+        else:
+            _kernels.gather_rows(self.pos, order, n, out=new_pos)
+            _kernels.gather_rows(self.binpos, order, n, out=new_bin)
+            for a in range(3):
+                _kernels.gather_rows(self.vel[a], order, n, out=new_vel[a])
+            _kernels.gather_rows(self.is_ghost, order, n, out=new_g)
         self.pos, self.binpos, self.vel, self.is_ghost = new_pos, new_bin, new_vel, new_g
         inv = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
         call("pc_invert_order", ptr(order), n, ptr(inv), s)
@@ -502,7 +510,7 @@ class DomainEngine:
                                                                device=self.device)
         self.ghost_all = torch.cat(gh) if gh else torch.empty(0, dtype=torch.int32,
                                                               device=self.device)
-        if self.pl is not None:
+        if self.pl is not None and not self._planar_done:
             call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
         e0 = self._t0()
@@ -551,7 +559,8 @@ class DomainEngine:
         capacities."""
         n, s, dev = self.n_total, stream(), self.device
         lib, g = _lib.load(), self._grid
-        call("pc_pos_planar", ptr(self.binpos), n, ptr(self.bpl), self._ps, s)
+        if not getattr(self, "_planar_done", False):
+            call("pc_pos_planar", ptr(self.binpos), n, ptr(self.bpl), self._ps, s)
         nt = int(lib.pc_tile_count(g))
         rw = torch.empty(nt, dtype=torch.int32, device=dev)
         call("pc_tile_rows", ptr(cell_start), g, ptr(rw), s)
