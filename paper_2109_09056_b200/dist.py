@@ -267,43 +267,25 @@ class DomainEngine:
              self._ps, stream())
         self._t1("integrate", e0)
 
-    def _owned_rows(self):
-        """Rows of owned particles in current order (drop ghosts, decomp.py:86-88)."""
-        n = self.n_total
-        if self.n_total == self.n_owned:
-            return None
-        own = (1 - self.is_ghost[:n]).contiguous()
-        pos = _kernels.scan_i32(own)
-        m = int(pos[n].item())
-        rows = torch.empty(max(m, 1), dtype=torch.int32, device=self.device)
-        dummy = torch.zeros(max(n, 1), dtype=torch.int8, device=self.device)
-        dummy_o = torch.empty(max(m, 1), dtype=torch.int8, device=self.device)
-        call("pc_compact", ptr(own), ptr(pos), n, ptr(rows), ptr(dummy), ptr(dummy_o), stream())
-        return rows[:m]
-
     def migrate_out(self):
         """Drop ghosts, wrap (done in integrate), owners, stable grouping by
         owner; returns {dest: (m, 7) rows} for dest != self (decomp.py:77-99)."""
         e0 = self._t0()
         self._sync_pos4()
-        rows = self._owned_rows()
-        if rows is not None:
-            n = rows.numel()
-            p = torch.empty((n + 1, 4), dtype=torch.float64, device=self.device)
-            _kernels.gather_rows(self.pos, rows, n, out=p)
-            vv = torch.empty((3, max(n, 1)), dtype=torch.float64, device=self.device)
-            for a in range(3):
-                _kernels.gather_rows(self.vel[a], rows, n, out=vv[a])
-            self.pos[:n] = p[:n]
-            self.vel[:, :n] = vv[:, :n]
-            self.n_owned = self.n_total = n
-        n = self.n_owned
+        # owners of every row; ghost rows get the out-of-range key n_ranks, which
+        # the partition drops (decomp.py:86-88 drops ghosts before migrating),
+        # so stayers and migrants are gathered straight from the current arrays
+        n = self.n_total
         x = self.pos[:n, :3].contiguous()
         owner = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         if n:
             call("pc_owner_of", ptr(x), n, 3, self.fabric.pc_grid(), ptr(owner), ptr(flag),
                  stream())
+            if self.n_total != self.n_owned:
+                owner[:n] = torch.where(self.is_ghost[:n] != 0,
+                                        torch.full_like(owner[:n], self.fabric.n_ranks),
+                                        owner[:n])
         # stable grouping by owner (decomp.py:97-99); the group starts and the
         # outside-box flag come back in one device->host read
         nr = self.fabric.n_ranks
