@@ -93,3 +93,35 @@ def test_distmd_deterministic_bitwise():
         assert p.exitcode == 0
     for _, es, _ in out:
         assert np.array_equal(es, np.array(ref))
+
+
+@pytest.mark.parametrize("det", [True, False])
+def test_distmd_four_processes(det):
+    """Four processes (rank grid 2x2x1: three neighbour ranks each, several
+    halo images per neighbour) through the same all-to-all refresh and
+    vectorised halo plan as the 8-GPU run: bitwise equal to the single-domain
+    run in deterministic mode, within the tile path's 1e-6 otherwise."""
+    import paper_2109_09056_b200 as pc
+    steps = 12
+    drv = pc.md.MDDriver(pc.md.MDConfig(**KW), deterministic=det)
+    ref = [drv.diagnostics()["E_total"]]
+    for s in range(1, steps + 1):
+        drv.step(s)
+        ref.append(drv.diagnostics()["E_total"])
+    ref = np.array(ref)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, q, steps, det)) for r in range(4)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sum(o[2] for o in out) == drv.n
+    for _, es, _ in out:
+        if det:
+            assert np.array_equal(es, ref)
+        else:
+            assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-6
