@@ -187,9 +187,11 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
-        dist.init_process_group("nccl")
+        # NCCL over NVLink; PC_BENCH_BACKEND=gloo runs the same N-rank path with
+        # several ranks on one GPU (tests/test_bench_contract.py)
+        dist.init_process_group(os.environ.get("PC_BENCH_BACKEND", "nccl"))
     import paper_2109_09056_b200 as pc
     from paper_2109_09056_b200 import _lib
 

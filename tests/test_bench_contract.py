@@ -43,3 +43,32 @@ def test_device_line():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["value"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "sm_mhz" in d["clocks"]
+
+
+def _torchrun(args, env_extra, timeout=600):
+    env = dict(os.environ, **env_extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + os.getpid() % 300),
+           os.path.join(ROOT, "bench.py")] + args
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]           # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_two_rank_line():
+    """The N-GPU path (torchrun, DistMD, max-over-ranks timing) with two ranks
+    sharing one GPU over gloo (PC_BENCH_BACKEND; the driver runs NCCL)."""
+    d = _torchrun(["--gpus", "2", "--cells", "16", "--steps", "10", "--warmup", "3"],
+                  {"PC_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["global_atoms"] == 2 * d["config"]["atoms_per_gpu"]
+    assert d["config"]["parallelism"] == "domain x2"
+
+
+def test_reference_arm_under_torchrun():
+    d = _torchrun(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                   "--cells", "6"], {})
+    assert d["impl"] == "reference" and d["value"] > 0

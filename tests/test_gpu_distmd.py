@@ -95,12 +95,13 @@ def test_distmd_deterministic_bitwise():
         assert np.array_equal(es, np.array(ref))
 
 
-@pytest.mark.parametrize("det", [True, False])
-def test_distmd_four_processes(det):
-    """Four processes (rank grid 2x2x1: three neighbour ranks each, several
-    halo images per neighbour) through the same all-to-all refresh and
-    vectorised halo plan as the 8-GPU run: bitwise equal to the single-domain
-    run in deterministic mode, within the tile path's 1e-6 otherwise."""
+@pytest.mark.parametrize("world,det", [(4, True), (4, False), (8, True)])
+def test_distmd_four_processes(world, det):
+    """Four / eight processes (rank grids 2x2x1 and 2x2x2, the 8-GPU bench's:
+    up to seven neighbour ranks, several halo images per neighbour) through
+    the same all-to-all refresh and vectorised halo plan as the 8-GPU run:
+    bitwise equal to the single-domain run in deterministic mode, within the
+    tile path's 1e-6 otherwise."""
     import paper_2109_09056_b200 as pc
     steps = 12
     drv = pc.md.MDDriver(pc.md.MDConfig(**KW), deterministic=det)
@@ -112,10 +113,11 @@ def test_distmd_four_processes(det):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 4, port, q, steps, det)) for r in range(4)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, steps, det))
+             for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=600) for _ in range(4)]
+    out = [q.get(timeout=600) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
