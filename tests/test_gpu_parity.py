@@ -559,3 +559,21 @@ def test_md_engine_tile_overflow_falls_back(pc, oracle):
                                [True] * 3, 1.0, 1.0, 2.5)
     assert force_err_ratio(f, fref) < 1.0
     assert abs(drv.diagnostics()["E_total"] - e0) < 1e-2 * abs(e0)
+
+
+def test_md_engine_overlap_raises(pc):
+    """Two coincident particles (r = 0) on the tile path: the exact per-pair
+    r^2 < (1e-10 sigma)^2 test flags it (ref md.py:117-119 FloatingPointError);
+    a finiteness check of the FP32 force would miss it (r^2 = 0 narrows to a
+    finite value)."""
+    cells = 12
+    a = (4.0 / 0.8442) ** (1.0 / 3.0)
+    x = pc.md.fcc_lattice(cells, a)
+    x[1] = x[0]
+    v = pc.md.initial_velocities(x.shape[0], 1.0, 1.0, 1)
+    cfg = pc.md.MDConfig(lattice_cells=cells, density=0.8442, temperature=1.0, cutoff=2.5,
+                         skin=0.3, rebuild_stride=10, seed=1, steps=0)
+    drv = pc.md.MDDriver(cfg, state=(x, v))
+    assert drv.mode == "tile"
+    with pytest.raises(FloatingPointError):
+        drv.check_errors()
