@@ -36,7 +36,7 @@ from . import _kernels, _lib
 from ._lib import call, ptr, stream
 from .decomp import DomainFabric, decompose
 from .geometry import Box
-from .md import PHASES, MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, _tile_order_kind, \
+from .md import MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, _tile_order_kind, \
     fcc_lattice, initial_velocities
 
 MIG_W = 7     # migrate row: x, y, z, vx, vy, vz, gid (int64 bits)
