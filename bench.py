@@ -1,26 +1,33 @@
 #!/usr/bin/env python
 """Benchmark of the LJ short-range MD hot path (BASELINE.json metric:
-atom-timesteps/sec, LJ rc = 2.5 sigma, plus % of the HBM roofline).
+atom-timesteps/sec, LJ rc = 2.5 sigma, at 1/2/4/8 B200, plus % of the HBM
+roofline).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--scaling strong|weak] [--cells C]
 
-Workload at N = 1 is BASELINE configs[1]: fcc 64^3 cells = 1,048,576 atoms,
-rho = 0.8442, T = 1.44, rc = 2.5, skin 0.3, neighbor rebuild every 20 steps,
-full neighbor list (``--list half`` for the Newton-3 variant).  A "step" is
-one velocity-Verlet MD step (integrate, rebuild on schedule, force + final
-kick).  Timing: W untimed warm-up steps, then exactly K steps between CUDA
-events on the launching stream, barrier + synchronize on both sides, max over
-ranks.  The working set (Verlet list ~330 MB at 1M atoms) exceeds the 126 MB
-L2, so no explicit L2 flush is done between steps.
+Workload (BASELINE configs[2], the configuration the metric is quoted on):
+fcc 128^3 cells = 8,388,608 atoms, rho = 0.8442, T = 1.44, rc = 2.5,
+skin 0.3, neighbor rebuild every 20 steps, full neighbor list.  At N = 1 the
+whole system runs on one B200.  Under torchrun (N > 1):
 
-Under torchrun (N > 1) the global system is N 64^3-cell blocks decomposed
-over rank_dims 2x1x1 / 2x2x1 / 2x2x2 (weak scaling): one rank per GPU, tile
-path on every rank's local grid, ghost refresh every step and migrate + halo
-rebuild every 20 steps over NCCL (paper_2109_09056_b200.dist).
+* ``--scaling strong`` (default, configs[2]): the same 8.4M-atom system
+  decomposed over rank_dims 2x1x1 / 2x2x1 / 2x2x2;
+* ``--scaling weak`` (configs[4]): a 128^3-cell block (8.4M atoms) per GPU,
+  67M atoms at N = 8.
+
+One rank per GPU, tile path on every rank's local grid, ghost refresh every
+step and migrate + halo rebuild every 20 steps over NCCL
+(paper_2109_09056_b200.dist).  A "step" is one velocity-Verlet
+MD step (integrate, rebuild on schedule, force + final kick).  Timing: W
+untimed warm-up steps, then exactly K steps between CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.  The
+working set (Verlet list ~1.4 GB at 8.4M atoms) exceeds the 126 MB L2, so no
+explicit L2 flush is done between steps.
 
 ``--impl reference`` times the CPU oracle port of the reference
 (oracle/particula_oracle.py: numpy, single-threaded like the reference) on a
-bounded sample of the same workload.
+bounded sample of the same workload (rank 0 only).
 """
 
 from __future__ import annotations
@@ -38,6 +45,24 @@ sys.path.insert(0, ROOT)
 METRIC = "atom-timesteps/sec (LJ, rc=2.5σ)"
 UNIT = "atom-steps/s"
 
+# SURVEY §8(d) algorithmic bytes per atom (FP64 x/v, 4-B index per list
+# entry, FP64 force): K6 full-list force 4k + 8 + 24 + 12, K8 integrate 168,
+# rebuild (K1 28 + K3 112 + K4/5 24 + 4k + 8) per rebuild
+def k6_bytes(k):
+    return 4.0 * k + 8 + 24 + 12
+
+
+def build_bytes(k):
+    return 24.0 + 4.0 * k + 8
+
+
+def rebuild_bytes(k):
+    return 28.0 + 112.0 + build_bytes(k)
+
+
+def step_bytes(k, rebuild):
+    return k6_bytes(k) + 168.0 + rebuild_bytes(k) / rebuild
+
 
 def parse_args():
     ap = argparse.ArgumentParser()
@@ -45,19 +70,21 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cells", type=int, default=64, help="fcc cells per axis per GPU")
+    ap.add_argument("--cells", type=int, default=128,
+                    help="fcc cells per axis: of the global system (strong) or per GPU (weak)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--temperature", type=float, default=1.44)
     ap.add_argument("--rebuild", type=int, default=20)
     ap.add_argument("--list", choices=["full", "half"], default="full")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0,
-                    help="steps of the end-to-end leg (0: the same K as the device leg)")
+                    help="steps of the end-to-end leg (0: max(K, 200))")
     ap.add_argument("--path", choices=["tile", "sell"], default="tile",
                     help="MD force/list path: TMA-staged tile rounds (default) or the "
                          "per-particle SELL list")
     ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
-                    help="force-kernel neighbor gather layout")
+                    help="SELL force-kernel neighbor gather layout")
     return ap.parse_args()
 
 
@@ -73,13 +100,34 @@ def md_kwargs(args, cells):
                 cutoff=2.5, skin=0.3, rebuild_stride=args.rebuild, seed=1)
 
 
+def global_cells(args, world):
+    """fcc cells per axis of the global system (strong: fixed; weak: grows
+    with the rank grid)."""
+    if world == 1 or args.scaling == "strong":
+        return [args.cells] * 3
+    from paper_2109_09056_b200.dist import rank_dims_for
+    return [args.cells * d for d in rank_dims_for(world)]
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def static_traffic():
+    """ncu DRAM read+write per launch per atom of the force kernel, from the
+    committed capture (an ncu replay cannot run inside the timed region)."""
+    p = os.path.join(ROOT, "profiles", "force_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["bytes_per_launch_per_atom"]), d.get("source", p)
+    except Exception:
+        return None, None
 
 
 class ClockSampler:
@@ -116,7 +164,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self._nv is not None:
@@ -152,10 +200,11 @@ def run_reference(args):
     if rank != 0:
         return
     kw = md_kwargs(args, args.cells)
+    gc = global_cells(args, world)
     # size the sample so warmup+steps finish in ~2 minutes of CPU time
     probe_rate, _, _ = cpu_oracle_rate(kw, 8, 2)
     budget_atoms = probe_rate * 120.0 / max(1, args.steps + args.warmup)
-    cells = max(6, min(args.cells, int((budget_atoms / 4) ** (1 / 3))))
+    cells = max(6, min(gc[0], int((budget_atoms / 4) ** (1 / 3))))
     from oracle import particula_oracle as orc
     cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=args.steps))
     drv = orc.MDOracle(cfg)
@@ -166,19 +215,29 @@ def run_reference(args):
         drv.step(s)
     dt = time.perf_counter() - t0
     value = drv.n * args.steps / dt
-    sample = (f"oracle port (numpy, 1 thread, like the reference) MD on fcc {cells}^3 = "
-              f"{drv.n} atoms, same rho/T/rc/skin/rebuild as the {args.cells}^3 workload")
+    ncpu = os.cpu_count()
+    sample = (f"oracle port of the reference MD (numpy, 1 thread: the reference is "
+              f"single-threaded; 1 of {ncpu} host cores) on fcc {cells}^3 = {drv.n} atoms, "
+              f"same rho/T/rc/skin/rebuild as the fcc {'x'.join(map(str, gc))} workload")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"LJ fcc {args.cells}^3 x{world}", "sample_atoms": drv.n,
-                       "rebuild_stride": args.rebuild, "list": "full"},
+            "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"LJ fcc {'x'.join(map(str, gc))} "
+                                   f"({4 * gc[0] * gc[1] * gc[2]} atoms)",
+                       "sample_atoms": drv.n, "rebuild_stride": args.rebuild, "list": "full",
+                       "host_cores": ncpu},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": sample},
+                             "host_cores": ncpu, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def _avg_ms(pairs):
+    import numpy as np
+    return float(np.mean([a.elapsed_time(b) for a, b in pairs])) if pairs else None
 
 
 def run_ours(args):
@@ -195,21 +254,21 @@ def run_ours(args):
     import paper_2109_09056_b200 as pc
     from paper_2109_09056_b200 import _lib
 
-    kw = md_kwargs(args, args.cells)
+    gc = global_cells(args, world)
+    kw = md_kwargs(args, gc[0])
     cfg = pc.md.MDConfig(**kw, steps=args.steps)
     if world > 1:
-        # weak scaling: a 64^3-cell block per GPU, spatial decomposition with
-        # ghost halo over NCCL (paper_2109_09056_b200.dist)
+        # spatial decomposition, ghost halo over NCCL (paper_2109_09056_b200.dist)
         from paper_2109_09056_b200.dist import DistMD, rank_dims_for
         dims = rank_dims_for(world)
         cfg.rank_dims = dims
-        drv = DistMD(cfg, cells=[args.cells * d for d in dims], local_init=True)
+        drv = DistMD(cfg, cells=gc, local_init=True)
         eng = drv.engine
     else:
         drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar",
                              tile=args.path == "tile", half_list=args.list == "half")
         eng = drv
-    n = drv.n                      # global atoms
+    n_global = int(drv.n)
     W, K = args.warmup, args.steps
     for s in range(1, W + 1):
         drv.step(s)
@@ -218,6 +277,7 @@ def run_ours(args):
         dist.barrier()
     lib = _lib.load()
     eng.force_events = []
+    eng.rebuild_events = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = lib.pc_launch_count()
     with ClockSampler(local) as clk:
@@ -234,44 +294,69 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         ms = float(t.item())
-    value = n * K / (ms * 1e-3)
+    value = n_global * K / (ms * 1e-3)
     diag = drv.diagnostics()
-    force_ms = [a.elapsed_time(b) for a, b in eng.force_events]
+    force_ms = _avg_ms(eng.force_events)
+    rb = eng.rebuild_events
+    build_ms = _avg_ms([(e[1], e[2]) for e in rb])
+    rebuild_ms = _avg_ms([(e[0], e[2]) for e in rb])
     eng.force_events = None
-    n_local = eng.n_owned if world > 1 else n
+    eng.rebuild_events = None
+    n_local = int(eng.n_owned) if world > 1 else n_global
     kmean = eng.mean_neighbors()
-    # algorithmic bytes per force launch per atom (SURVEY §8d
-    # K6 + the fused final kick): a 4-B neighbour index per list entry (k)
-    # + row length 4 + position read once 24 + FP64 force write 24 + final
-    # kick v read+write 48 -- the same figure for every list layout
     mode = getattr(eng, "mode", "sell")
+    peak, peak_kind = measured_peak()
+    # dominant kernel: the force pass.  Algorithmic bytes per launch = the
+    # §8(d) K6 figure x the atoms the launch processes (this rank's owned
+    # atoms); the fused final kick / next integrate are NOT counted
+    b_force = k6_bytes(kmean)
     if mode == "half":
-        # half list: 4k_half + count + pos once + f read-modify-write (atomics)
-        bytes_per_atom = 4 * kmean + 4 + 24 + 48
         kname = "lj_force_sell_half_kernel (Newton-3, FP64 atomics; kick separate)"
     elif mode == "tile":
-        bytes_per_atom = 4 * kmean + 4 + 24 + 24 + 48
-        kname = "tile_force_kernel (TMA-staged smem neighbourhood, 16-bit slot rounds, +fused final kick)"
+        kname = ("tile_force_kernel (TMA-staged smem neighbourhood, 16-bit slot rounds, "
+                 "fused final kick + next integrate)")
     else:
-        bytes_per_atom = 4 * kmean + 4 + 24 + 24 + 48
         kname = "lj_force_sell_kernel (+fused final kick)"
-    force_avg_s = float(np.mean(force_ms)) * 1e-3
-    achieved = n_local * bytes_per_atom / force_avg_s / 1e9
-    peak, peak_kind = measured_peak()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "force_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get("bytes_per_launch_per_atom")
-            traffic = None if traffic is None else traffic * n
+    achieved = n_local * b_force / (force_ms * 1e-3) / 1e9
+    tr_atom, tr_src = static_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": None if tr_atom is None else tr_atom * n_local,
+                "traffic_source": None if tr_src is None else
+                f"static: ncu DRAM read+write per launch per atom from {tr_src}, x {n_local} "
+                f"atoms (an ncu replay cannot run inside the timed region)",
+                "kernel": kname, "bytes_per_atom": b_force,
+                "bytes_model": "SURVEY §8(d) K6: 4k + 8 + 24 + 12, k = mean list length",
+                "peak_kind": peak_kind, "avg_launch_us": force_ms * 1e3,
+                "launches": K,
+                "limiter": "not HBM: instruction issue and shared-memory wavefronts of the "
+                           "exact FP64 pair test (ncu, profiles/, DESIGN.md §5)"}
+    per_gpu_rate = value / world
+    b_step = step_bytes(kmean, args.rebuild)
+    roofline_step = {"bound": "hbm", "achieved": per_gpu_rate * b_step / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": per_gpu_rate * b_step / 1e9 / peak,
+                     "bytes_per_atom_step": b_step,
+                     "bytes_model": "SURVEY §8(d): K6 + K8 168 + rebuild/R"}
+    roofline_build = None
+    if build_ms:
+        bb = build_bytes(kmean)
+        roofline_build = {"bound": "hbm", "kernel": "tile_build_kernel + tile_order_kernel"
+                          if mode == "tile" else "nbr build (SELL)",
+                          "achieved": n_local * bb / (build_ms * 1e-3) / 1e9, "peak": peak,
+                          "unit": "GB/s",
+                          "frac": n_local * bb / (build_ms * 1e-3) / 1e9 / peak,
+                          "bytes_per_atom": bb, "bytes_model": "SURVEY §8(d) K4/5: 24 + 4k + 8",
+                          "avg_launch_us": build_ms * 1e3,
+                          "rebuild_us": rebuild_ms * 1e3, "rebuilds": len(rb)}
 
     # the device leg's engine goes back to PyTorch's caching allocator, so the
     # end-to-end leg (a fresh engine through the public API) allocates from a
     # warm pool, as a process calling run_md repeatedly does
     del drv, eng
+    torch.cuda.empty_cache()
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(pc, kw, args.e2e_steps or K, world,
+        e2e = run_e2e(pc, kw, args.e2e_steps or max(K, 200),
                       dict(tile=args.path == "tile", half_list=args.list == "half",
                            planar_gather=args.gather == "planar"))
 
@@ -279,28 +364,33 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, natoms, secs = cpu_oracle_rate(kw, 16, 20)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"oracle port (numpy, 1 thread) 20 MD steps on fcc 16^3 = {natoms} "
-                         f"atoms, same rho/T/rc/skin/rebuild ({secs:.1f} s)"}
+               "host_cores": os.cpu_count(),
+               "sample": f"oracle port (numpy, 1 thread, as the single-threaded reference; "
+                         f"1 of {os.cpu_count()} host cores) 20 MD steps on fcc 16^3 = "
+                         f"{natoms} atoms, same rho/T/rc/skin/rebuild ({secs:.1f} s)"}
     if rank == 0:
+        shape = "x".join(map(str, gc))
+        if world == 1:
+            workload = (f"LJ fcc {shape} ({n_global} atoms) on one GPU, rho=0.8442 "
+                        f"T={args.temperature} rc=2.5 skin=0.3 rebuild={args.rebuild} "
+                        f"{args.list} list")
+        else:
+            workload = (f"LJ fcc {shape} ({n_global} atoms) over {world} GPUs "
+                        f"({args.scaling} scaling, ~{n_global // world} atoms per GPU), "
+                        f"rho=0.8442 T={args.temperature} rc=2.5 skin=0.3 "
+                        f"rebuild={args.rebuild} {args.list} list")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32(LJ magnitude)",
+                "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None,
+                "dtype": "f64+f32(LJ magnitude)",
                 "data": "synthetic fcc lattice, seeded Gaussian velocities",
-                "config": {"workload": f"LJ fcc {args.cells}^3 ({n} atoms) per GPU, "
-                                       f"rho=0.8442 T={args.temperature} rc=2.5 skin=0.3 "
-                                       f"rebuild={args.rebuild} {args.list} list",
-                           "atoms_per_gpu": n, "global_atoms": n * world,
+                "config": {"workload": workload, "global_atoms": n_global,
+                           "atoms_per_gpu": n_global / world, "rank0_owned_atoms": n_local,
                            "parallelism": f"domain x{world}" if world > 1 else "single domain",
-                           "l2": "working set > L2 (Verlet list ~4k B/atom), no flush",
+                           "l2": "working set > L2 (Verlet list ~170 B/atom), no flush",
                            "mean_neighbors": kmean},
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                             "kernel": kname,
-                             "bytes_per_atom": bytes_per_atom, "peak_kind": peak_kind,
-                             "avg_launch_us": force_avg_s * 1e6,
-                             "limiter": "not HBM: instruction issue (~64 % active) and "
-                                        "shared-memory wavefronts (~55 %) of the exact "
-                                        "FP64 pair test (ncu, profiles/, DESIGN.md §5)"},
+                "roofline": roofline, "roofline_step": roofline_step,
+                "roofline_build": roofline_build,
                 "gpu_launches": int(launches),
                 "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu,
@@ -310,7 +400,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(pc, kw, steps, world, driver_options=None):
+def run_e2e(pc, kw, steps, driver_options=None):
     """Same metric through the public API with host buffers: pinned host x, v
     uploaded inside the timed region, then `pc.md.run_md` (the reference's
     run_md contract: every step's KE/PE/E_total/temperature row, returned to
@@ -330,15 +420,11 @@ def run_e2e(pc, kw, steps, world, driver_options=None):
     e1.synchronize()
     assert len(rows) == steps + 1
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"value": n * world * steps / (ms * 1e-3), "unit": UNIT,
+    return {"value": n * steps / (ms * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": n * 48 / steps, "d2h_bytes_per_step": 40,
-            "steps": steps, "includes": "H2D of x, v + initial rebuild/force + run_md's "
-                                        "per-step diagnostics rows (D2H at the end)"}
+            "steps": steps, "includes": "H2D of x, v + engine setup (sort, list build, first "
+                                        "force) + the steps + run_md's per-step diagnostics "
+                                        "rows (D2H at the end)"}
 
 
 def main():

@@ -168,13 +168,15 @@ def _axis_stencil(nc_a: int, periodic_a: bool):
     return keep
 
 
-def neighbor_pairs(x, low, high, periodic, cutoff, cell_ratio=1.0, chunk=16384):
+def neighbor_pairs(x, low, high, periodic, cutoff, cell_ratio=1.0, chunk=16384, rows=None):
     """All ordered (i, j), i != j, with min-image r^2 < cutoff^2, as arrays
     sorted by (i, j) -- the full-convention sets of ref neighbors.py:49-97.
 
     Same cell grid as the reference (``nc = max(1, floor(L/(rc*ratio)))``,
     width ``L/nc``, clipped floor) and the same FP64 predicate, evaluated
     vectorised over candidate pairs instead of a Python loop over cells.
+    ``rows``: only the rows i in this index array (sampled parity checks of
+    multi-million-atom systems; the row sets are the full-list rows).
     """
     x = np.ascontiguousarray(x, np.float64)
     n, d = x.shape
@@ -195,8 +197,10 @@ def neighbor_pairs(x, low, high, periodic, cutoff, cell_ratio=1.0, chunk=16384):
     offs = list(itertools.product(*[_axis_stencil(int(nc[a]), bool(per[a]))
                                     for a in range(d)]))
     out_i, out_j = [], []
-    for b in range(0, n, chunk):
-        ids = np.arange(b, min(n, b + chunk), dtype=np.int64)
+    sel = (np.arange(n, dtype=np.int64) if rows is None
+           else np.unique(np.asarray(rows, np.int64)))
+    for b in range(0, sel.size, chunk):
+        ids = sel[b:b + chunk]
         ci = idx[ids]
         cand_i, cand_j = [], []
         for off in offs:

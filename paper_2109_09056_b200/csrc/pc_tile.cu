@@ -589,15 +589,23 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   tile_setup<true>(blockIdx.x, g, b, cs, T);
   if (T.S > p.max_stage) {
     // flag it; leave an empty plan so that a speculatively launched force
-    // pass stays in bounds (the caller discards it and falls back)
+    // pass stays in bounds (the caller discards it and falls back).  The
+    // tile keeps ONE empty row-warp (no rows, zero rounds): the force
+    // kernel's warp that takes it releases the staging buffer the tile was
+    // loaded into -- a tile without items would hold its buffer forever and
+    // stall every later tile of the CTA (tile_rows_kernel reserves >= 1
+    // row-warp per tile, so rw0[tile] is this tile's own)
+    const int r0 = rw0[blockIdx.x];
+    if (threadIdx.x < 32) rowidx[(int64_t)r0 * 32 + threadIdx.x] = -1;
     if (threadIdx.x == 0) {
       atomicOr(flag, kFlagStage);
       atomicMax(flag + 1, T.S);
       int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
       pg[0] = 0;
       pg[1] = 0;
-      pg[2] = 0;
-      pg[3] = rw0[blockIdx.x];
+      pg[2] = 1;
+      pg[3] = r0;
+      rounds[r0] = 0;
     }
     return;
   }

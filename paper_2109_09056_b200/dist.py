@@ -127,6 +127,7 @@ class DomainEngine:
         self.ghost_blocks = []    # [(src, int32 sorted rows)] ascending src
         self.rebuilds = 0
         self.force_events = None  # optional [(start, end)] CUDA events per force launch
+        self.rebuild_events = None  # optional [(sort start, build start, end)] per rebuild
 
     # ---- geometry -----------------------------------------------------------
     def _local_grid(self):
@@ -437,7 +438,25 @@ class DomainEngine:
 
     def sort_and_build(self):
         """Stable cell sort of owned + ghost rows on the local grid, then the
-        SELL Verlet build of all rows (ghost rows emptied)."""
+        tile (else SELL) Verlet build of all rows (ghost rows emptied)."""
+        rev = self.rebuild_events
+        if rev is None:
+            self._sort_and_build()
+            return
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        self._build_mark = ev[1]
+        self._sort_and_build()
+        ev[2].record()
+        rev.append(tuple(ev))
+
+    def _mark_build(self):
+        m = getattr(self, "_build_mark", None)
+        if m is not None:
+            m.record()
+            self._build_mark = None
+
+    def _sort_and_build(self):
         n = self.n_total
         s = stream()
         e0 = self._t0()
@@ -496,6 +515,7 @@ class DomainEngine:
             call("pc_pos_planar", ptr(self.pos), n, ptr(self.pl), self._ps, s)
         self._t1("sort", e0)
         e0 = self._t0()
+        self._mark_build()
         if tile and self._tile_build(srt.cell_start):
             self.rebuilds += 1
             self._t1("neighbor", e0)
@@ -906,6 +926,9 @@ class DistMD(_StepLogic):
         self.cfg = cfg
         self.transport = transport if transport is not None else NCCLTransport()
         world, rank = self.transport.world, self.transport.rank
+        if tuple(cfg.rank_dims) != (1, 1, 1) and int(np.prod(cfg.rank_dims)) != world:
+            raise ValueError(f"rank_dims {tuple(cfg.rank_dims)} do not match the world "
+                             f"size {world}")
         dims = tuple(cfg.rank_dims) if int(np.prod(cfg.rank_dims)) == world \
             else rank_dims_for(world)
         cells = np.array(cells if cells is not None else [cfg.lattice_cells] * 3, np.int64)

@@ -247,11 +247,20 @@ class MDDriver:
         ids = torch.arange(n, dtype=torch.int64, device=dev)
         # pos has one extra row: the SELL padding target (NaN position, tag -1)
         self.pos = self._new_pos()
-        self.pos[:n] = _kernels.pack_pos4(x.to(dev, non_blocking=True), ids)
+        xd = x.to(dev, torch.float64, non_blocking=True)
+        if state is not None:
+            # caller positions: the reference's initial migrate wraps them into
+            # the box (decomp.py:90-91); the lattice path is already in [0, L)
+            if xd.data_ptr() == x.data_ptr():
+                xd = xd.clone()
+            xd = xd.contiguous()
+            call("pc_box_wrap", ptr(xd), n, 3, self._pbox, stream())
+        self.pos[:n] = _kernels.pack_pos4(xd, ids)
         self._pos_alt = self._new_pos()
         self.vel = v.to(dev, non_blocking=True).t().contiguous()           # (3, n)
         self._vel_alt = torch.empty_like(self.vel)
         self.force_events = None      # optional list collecting (start, end) per force launch
+        self.rebuild_events = None    # optional list: (sort start, build start, end) per rebuild
         self.frc = torch.zeros((3, n), dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(n, dtype=torch.int32, device=dev)
         self.ell_width = -(-self.ell_width // 4) * 4
@@ -334,6 +343,10 @@ class MDDriver:
         """Cell sort of all particle fields + SELL Verlet build (md.py:169-188)."""
         n, s = self.n, stream()
         e0 = self._t0()
+        rev = self.rebuild_events
+        if rev is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
         zsort = self.tile and min(self._grid.nc[0], self._grid.nc[1], self._grid.nc[2]) >= 3
         # binning, the z-sort and the permute read the planar positions (always
         # current; pos4 x, y, z may lag behind after fused integrate steps).
@@ -358,9 +371,14 @@ class MDDriver:
         self._pos_stale = False
         self._t1("sort", e0)
         e0 = self._t0()
+        if rev is not None:
+            ev[1].record()
         self._cell_start = srt.cell_start
         if not (self.tile and self._tile_build(srt.cell_start)):
             self._sell_build(srt.cell_start)
+        if rev is not None:
+            ev[2].record()
+            rev.append(tuple(ev))
         self._t1("neighbor", e0)
         self.rebuilds += 1
 

@@ -31,7 +31,8 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_device_line():
-    d = _run(["--steps", "20", "--warmup", "3", "--cells", "16", "--no-cpu-baseline"])
+    d = _run(["--steps", "20", "--warmup", "3", "--cells", "16", "--no-cpu-baseline",
+              "--e2e-steps", "20"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "gpu_launches", "clocks", "e2e"):
@@ -43,6 +44,10 @@ def test_device_line():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["value"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "sm_mhz" in d["clocks"]
+    assert d["config"]["global_atoms"] == 4 * 16 ** 3 == d["config"]["atoms_per_gpu"]
+    for key in ("roofline_step", "roofline_build"):
+        q = d[key]
+        assert 0 < q["frac"] < 1 and abs(q["frac"] - q["achieved"] / q["peak"]) < 1e-9
 
 
 def _torchrun(args, env_extra, timeout=600):
@@ -58,14 +63,21 @@ def _torchrun(args, env_extra, timeout=600):
 
 
 @pytest.mark.gpu
-def test_two_rank_line():
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_two_rank_line(scaling):
     """The N-GPU path (torchrun, DistMD, max-over-ranks timing) with two ranks
-    sharing one GPU over gloo (PC_BENCH_BACKEND; the driver runs NCCL)."""
-    d = _torchrun(["--gpus", "2", "--cells", "16", "--steps", "10", "--warmup", "3"],
-                  {"PC_BENCH_BACKEND": "gloo"})
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
-    assert d["config"]["global_atoms"] == 2 * d["config"]["atoms_per_gpu"]
-    assert d["config"]["parallelism"] == "domain x2"
+    sharing one GPU over gloo (PC_BENCH_BACKEND; the driver runs NCCL).
+    strong: the 16^3-cell system split over 2x1x1; weak: a 16^3-cell block per
+    rank (32x16x16 global)."""
+    d = _torchrun(["--gpus", "2", "--cells", "16", "--steps", "10", "--warmup", "3",
+                   "--scaling", scaling], {"PC_BENCH_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0
+    n = 4 * 16 ** 3 * (2 if scaling == "weak" else 1)
+    c = d["config"]
+    assert c["global_atoms"] == n and c["atoms_per_gpu"] == n / 2
+    assert 0.4 * n < c["rank0_owned_atoms"] < 0.6 * n
+    assert c["parallelism"] == "domain x2"
+    assert abs(d["value"] - n * 10 / (d["ms_per_step"] * 10e-3)) < 1e-6 * d["value"]
 
 
 def test_reference_arm_under_torchrun():
