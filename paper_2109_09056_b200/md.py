@@ -244,9 +244,11 @@ class MDDriver:
             v = torch.as_tensor(initial_velocities(n, cfg.temperature, cfg.mass, cfg.seed))
         else:       # host (ideally pinned) x, v in global-id order
             x, v = (t if isinstance(t, torch.Tensor) else torch.as_tensor(t) for t in state)
-        ids = torch.arange(n, dtype=torch.int64, device=dev)
-        # pos has one extra row: the SELL padding target (NaN position, tag -1)
-        self.pos = self._new_pos()
+        # ingest through the reference's particle store: an AoSoA set of
+        # MD_SCHEMA with the configured vector length V (ref md.py:147-153,
+        # aosoa.py:63-142) in HBM, then the engine's SoA working arrays are
+        # extracted from it (pc_aosoa_field).  V shapes the store, never the
+        # physics: the step loop runs on the SoA copies (ref test_md.py:86-91)
         xd = x.to(dev, torch.float64, non_blocking=True)
         if state is not None:
             # caller positions: the reference's initial migrate wraps them into
@@ -255,9 +257,20 @@ class MDDriver:
                 xd = xd.clone()
             xd = xd.contiguous()
             call("pc_box_wrap", ptr(xd), n, 3, self._pbox, stream())
+        store = aosoa.create(MD_SCHEMA, cfg.vector_length, n, device=dev)
+        store.slice("x").device_assign(xd)
+        store.slice("x0").device_assign(xd)
+        store.slice("v").device_assign(v.to(dev, torch.float64, non_blocking=True))
+        store.slice("id").device_assign(torch.arange(n, dtype=torch.int64, device=dev))
+        xd = store.slice("x").device_values()
+        vd = store.slice("v").device_values()
+        ids = store.slice("id").device_values()
+        del store
+        # pos has one extra row: the SELL padding target (NaN position, tag -1)
+        self.pos = self._new_pos()
         self.pos[:n] = _kernels.pack_pos4(xd, ids)
         self._pos_alt = self._new_pos()
-        self.vel = v.to(dev, non_blocking=True).t().contiguous()           # (3, n)
+        self.vel = vd.t().contiguous()                                   # (3, n)
         self._vel_alt = torch.empty_like(self.vel)
         self.force_events = None      # optional list collecting (start, end) per force launch
         self.rebuild_events = None    # optional list: (sort start, build start, end) per rebuild

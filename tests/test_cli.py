@@ -59,7 +59,10 @@ def test_seeded_runs_byte_identical_and_format(tmp_path):
 
 @pytest.mark.gpu
 def test_layout_transparency(tmp_path):
-    """Criterion 2 (md part): physics rows bitwise identical for V in {1,4,8,16,SoA}."""
+    """Criterion 2 (md part): physics rows bitwise identical for V in {1,4,8,16,SoA}.
+    V is the vector length of the AoSoA particle store the engine ingests its
+    initial state through (MDDriver, pc_aosoa_field); the step loop then runs
+    on SoA working arrays, so the rows must not depend on V."""
     n_md = 4 * 4 ** 3
     outs = []
     for v in (1, 4, 8, 16, n_md):
@@ -103,3 +106,41 @@ def test_ranks_byte_identical_deterministic(tmp_path):
     assert cli.main(["md", "--steps", "12", "--lattice-cells", "6", "--parallel", "--output",
                      str(q)]) == 0
     assert len(q.read_text().splitlines()) == 2 + 13
+
+
+def _golden_args():
+    import importlib.util
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    spec = importlib.util.spec_from_file_location("make_cli_golden",
+                                                  os.path.join(here, "make_cli_golden.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return here, mod.CASES
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["md_4", "md_6_ranks"])
+def test_md_csv_matches_reference_cli(tmp_path, case):
+    """f1 vs the reference CLI itself (tests/golden/make_cli_golden.py ran
+    ``particula md`` unchanged, ref cli.py:173-206): the ``#`` echo line and
+    the header byte for byte, every diagnostics value within 1e-8 relative
+    (deterministic mode: FP64 LJ, id-ordered sums), the phases sidecar with
+    the reference's six buckets."""
+    import numpy as np
+    here, cases = _golden_args()
+    p = tmp_path / f"{case}.csv"
+    assert cli.main(["md", *cases[case], "--output", str(p)]) == 0
+    mine = p.read_text().splitlines()
+    with open(f"{here}/cli_{case}.csv") as fh:
+        ref = fh.read().splitlines()
+    assert mine[0] == ref[0] and mine[1] == ref[1]
+    assert len(mine) == len(ref)
+    a = np.array([[float(t) for t in ln.split(",")] for ln in mine[2:]])
+    b = np.array([[float(t) for t in ln.split(",")] for ln in ref[2:]])
+    assert np.array_equal(a[:, 0], b[:, 0])
+    assert np.max(np.abs(a[:, 1:] - b[:, 1:]) / np.abs(b[:, 1:])) < 1e-8
+    side = (tmp_path / f"{case}.csv.phases.csv").read_text().splitlines()
+    assert side[0] == ref[0] and side[1] == "phase,seconds"
+    assert [ln.split(",")[0] for ln in side[2:]] == sorted(
+        ["force", "halo", "integrate", "migrate", "neighbor", "sort"])

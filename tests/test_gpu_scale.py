@@ -3,10 +3,11 @@
 The MD engine's tile path -- the configuration bench.py measures -- against
 the CPU oracle on identical positions:
 
-* C2 (fcc 64^3 = 1,048,576 atoms, the configs[1] workload): after 25 steps
-  (one rebuild at step 20) the whole Verlet list equals the oracle's
-  ``build_verlet`` as sorted per-particle sets, bit for bit; every atom's
-  force is within 1e-5 * max(|F_ref,i|_inf, F_rms); PE within 1e-6.
+* C2 (fcc 64^3 = 1,048,576 atoms, the configs[1] workload): the whole
+  Verlet list of the step-20 rebuild equals the oracle's ``build_verlet`` on
+  the step-20 positions as sorted per-particle sets, bit for bit; five steps
+  later every atom's force is within 1e-5 * max(|F_ref,i|_inf, F_rms) and PE
+  within 1e-6.
 * C3 (fcc 128^3 = 8,388,608 atoms, the BASELINE metric's configuration):
   the same checks on a random 100k-row sample (the oracle restricted to those
   rows), plus the tile path's FP32-per-pair / FP64-per-row energies against
@@ -43,10 +44,14 @@ def _engine(pc, cells, temp, rebuild, steps, seed=5):
     cfg = pc.md.MDConfig(lattice_cells=cells, density=0.8442, temperature=temp, cutoff=2.5,
                          skin=0.3, rebuild_stride=rebuild, seed=seed, steps=0)
     drv = pc.md.MDDriver(cfg, time_phases=False)
-    for s in range(1, steps + 1):
-        drv.step(s)
+    _advance(drv, 0, steps)
     assert drv.mode == "tile" and drv.tile_failures == 0
     return drv
+
+
+def _advance(drv, s0, s1):
+    for s in range(s0 + 1, s1 + 1):
+        drv.step(s)
 
 
 def _gid(drv):
@@ -99,11 +104,14 @@ def _check_forces(oracle, drv, x, f, rows=None):
 
 
 def test_c2_full_lists_forces_energy(pc, oracle):
-    """C2, the driver-benched size: whole list bit-exact, all forces, PE."""
-    drv = _engine(pc, 64, 1.44, 20, 25)
+    """C2 (configs[1]): whole list bit-exact at the step-20 rebuild; all
+    forces and PE five steps later."""
+    drv = _engine(pc, 64, 1.44, 20, 20)       # the list of the step-20 rebuild
+    x, _ = drv.gather_state()
+    _check_sets(oracle, drv, x, _gid(drv))
+    _advance(drv, 20, 25)                     # forces 5 steps into the list's life
     x, _ = drv.gather_state()
     gid = _gid(drv)
-    _check_sets(oracle, drv, x, gid)
     f = _forces_by_gid(drv, gid)
     peref = _check_forces(oracle, drv, x, f)
     d = drv.diagnostics()
@@ -114,11 +122,13 @@ def test_c2_full_lists_forces_energy(pc, oracle):
 def test_c3_sampled_rows(pc, oracle):
     """C3, the metric's size (8.4M atoms): 100k sampled rows -- lists
     bit-exact and forces within tolerance; tile vs SELL-path energies."""
-    drv = _engine(pc, 128, 1.44, 20, 25)
+    drv = _engine(pc, 128, 1.44, 20, 20)
+    x, _ = drv.gather_state()
+    rows = np.sort(np.random.default_rng(11).choice(drv.n, 100_000, replace=False))
+    _check_sets(oracle, drv, x, _gid(drv), rows)
+    _advance(drv, 20, 25)
     x, _ = drv.gather_state()
     gid = _gid(drv)
-    rows = np.sort(np.random.default_rng(11).choice(drv.n, 100_000, replace=False))
-    _check_sets(oracle, drv, x, gid, rows)
     f = _forces_by_gid(drv, gid)
     _check_forces(oracle, drv, x, f, rows)
     d_tile = drv.diagnostics()
@@ -136,11 +146,14 @@ def test_c3_sampled_rows(pc, oracle):
 
 def test_hot_c4_32cubed(pc, oracle):
     """Hot liquid (T = 3.0, rebuild every 5 steps) at 32^3 = 131k atoms,
-    17 steps (3 rebuilds): whole list bit-exact, forces, PE."""
-    drv = _engine(pc, 32, 3.0, 5, 17)
+    whole list bit-exact at the step-15 rebuild (the third), forces and PE
+    two steps later."""
+    drv = _engine(pc, 32, 3.0, 5, 15)
+    x, _ = drv.gather_state()
+    _check_sets(oracle, drv, x, _gid(drv))
+    _advance(drv, 15, 17)
     x, _ = drv.gather_state()
     gid = _gid(drv)
-    _check_sets(oracle, drv, x, gid)
     f = _forces_by_gid(drv, gid)
     peref = _check_forces(oracle, drv, x, f)
     d = drv.diagnostics()
