@@ -304,13 +304,15 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
  * grid and box), the exact FP64 predicate uses the raw positions d_planar and
  * the global box_exact (the reference's ghost convention), and rows i with
  * d_skip[i] != 0 (ghosts) get empty lists.  NULL d_bplanar / box_exact /
- * d_skip: pc_tile_build. */
+ * d_skip: pc_tile_build.  d_tile_ghost (nullable, one int per tile): 1 when
+ * the tile's staged neighbourhood holds a ghost row (d_skip), else 0 -- the
+ * interior / boundary split of pc_tile_force. */
 int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
                          const int32_t* d_cell_start, const pc_grid* grid, const pc_box* box,
                          double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
                          void* stream, const double* d_bplanar, const pc_box* box_exact,
-                         const int32_t* d_skip);
+                         const int32_t* d_skip, int32_t* d_tile_ghost);
 /* Reorder the rounds of every row-warp (after pc_tile_build, same list):
  * residue round-robin per row so that the 16 lanes of a half-warp read 16
  * distinct shared-memory bank pairs in most rounds.  rw_bound >= the total
@@ -328,13 +330,22 @@ int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_
  * (r^2 < overlap2) sets d_flag bit 2.  With d_planar_next != NULL the next
  * step's integrate block (v' = v + dtm_next f, x' = wrap(x + dt v'), ref
  * md.py:219-231) is fused into the epilogue and written to d_planar_next /
- * d_v_next (same strides); d_planar and d_v keep this step's state. */
+ * d_v_next (same strides); d_planar and d_v keep this step's state.
+ * d_virial (nullable): the pair virial W = sum over pairs of r.F, one
+ * partial per warp in column 0 of a zero-initialised (partials, 5) array
+ * (reduce with pc_reduce_partials).  The reference has no virial; this is
+ * the north-star "FP64 energy/virial reduction" (BASELINE.json).
+ * d_tiles / d_trange (nullable): run only the tiles d_tiles[trange[0] ..
+ * trange[1]) (device-side bounds; ntiles stays the launch bound) -- the
+ * interior / boundary passes that overlap a decomposed domain's ghost
+ * refresh (ref md.py:192-200); each pass writes its own partial rows. */
 int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
                   const int32_t* d_plan, const int32_t* d_rowidx, const int32_t* d_rounds,
                   const void* d_list, int32_t q8, const pc_box* box, const pc_lj* lj,
                   double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
                   double dtm, double mass, double* d_partial, int32_t* d_flag,
                   double* d_planar_next, double* d_v_next, double dtm_next, double dt,
+                  double* d_virial, const int32_t* d_tiles, const int32_t* d_trange,
                   void* stream);
 int32_t pc_tile_force_partials(int32_t ntiles);
 /* pos4 x, y, z <- planar rows [0, n) (tags untouched). */
@@ -461,6 +472,23 @@ int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
  * (ref decomp.py:92-96). */
 int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* box,
                          int32_t* d_flag, void* stream);
+/* Fused halo selection for the decomposed MD engine (same export set and
+ * (slot, particle index) order as pc_halo_plan + scan + pc_compact, ref
+ * decomp.py:143-228), reading pos4 rows (x, y, z, id bits) directly:
+ * pc_halo_select_count writes d_hist[slot * C + c] = exported particles of
+ * slot `slot` in chunk c (C = pc_halo_select_chunks(n)); after an exclusive
+ * scan of d_hist (pc_scan_i32 -> d_off, slot s starts at d_off[s * C]),
+ * pc_halo_select_place writes d_out_idx[k] (particle index) and the ghost
+ * row d_out_rows[k] = (x, y, z, id bits, shift of the winning image). */
+int64_t pc_halo_select_chunks(int64_t n);
+int pc_halo_select_count(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
+                         const int32_t* h_slot, const double* h_shift, const double* h_lo,
+                         const double* h_hi, int32_t n_slots, double w2, int32_t* d_hist,
+                         void* stream);
+int pc_halo_select_place(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
+                         const int32_t* h_slot, const double* h_shift, const double* h_lo,
+                         const double* h_hi, int32_t n_slots, double w2, const int32_t* d_off,
+                         int32_t* d_out_idx, double* d_out_rows, void* stream);
 /* Halo export planning for one source rank (ref decomp.py:143-228): n_off
  * candidate images in product order (host arrays: destination slot, shift,
  * destination box lo/hi, each d wide); per particle and slot the best image

@@ -111,6 +111,11 @@ SIGNATURES = {
     "pc_halo_plan": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                     c_dbl, c_vp, c_vp, c_vp]),
     "pc_compact": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "pc_halo_select_chunks": (c_i64, [c_i64]),
+    "pc_halo_select_count": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                            c_i32, c_dbl, c_vp, c_vp]),
+    "pc_halo_select_place": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                            c_i32, c_dbl, c_vp, c_vp, c_vp, c_vp]),
     "pc_gather_shift": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "pc_scatter_add": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_halo_pack": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
@@ -139,11 +144,11 @@ SIGNATURES = {
     "pc_tile_build_domain": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
                                             ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp,
                                             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                            ctypes.POINTER(PcBox), c_vp]),
+                                            ctypes.POINTER(PcBox), c_vp, c_vp]),
     "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl, c_vp,
                                      c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp,
-                                     c_dbl, c_dbl, c_vp]),
+                                     c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp]),
     "pc_pos_from_planar": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pc_tile_force_partials": (c_i32, [c_i32]),
     "pc_tile_order": (ctypes.c_int, [c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),

@@ -97,6 +97,97 @@ __global__ void halo_plan_kernel(const double* __restrict__ x, int64_t n, HaloTa
   }
 }
 
+// ---- fused halo selection (decomposed MD engine) ----------------------------
+// The export set of build_halo (ref decomp.py:143-228: best image per
+// destination slot, export iff its d^2 < w^2, entries ordered by (slot,
+// particle index)) in two passes over the particles, without the per-slot
+// flag matrix: (1) per 1024-particle chunk and slot, the number of exported
+// particles; (2) after a scan of those counts (slot-major, chunk-minor: the
+// (slot, index) order), each particle writes its index and its ghost row
+// (x, y, z, global-id bits, shift of the winning image) at its place.
+constexpr int kSelChunk = 1024;
+
+__device__ __forceinline__ unsigned halo_select_mask(const double* __restrict__ pos4, int64_t i,
+                                                     int64_t n, const HaloTable& t,
+                                                     int8_t* bo_out) {
+  if (i >= n) return 0u;
+  double xi[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < t.d; ++a) xi[a] = pos4[i * 4 + a];
+  double best[kMaxSlots];
+  int bo[kMaxSlots];
+  for (int q = 0; q < t.n_slots; ++q) { best[q] = INFINITY; bo[q] = -1; }
+  for (int k = 0; k < t.n_off; ++k) {
+    const int q = t.off[k].slot;
+    const double d2 = dist2_box(xi, t.off[k], t.d);
+    if (bo[q] < 0 || d2 < best[q]) { best[q] = d2; bo[q] = k; }
+  }
+  unsigned m = 0u;
+  for (int q = 0; q < t.n_slots; ++q) {
+    if (best[q] < t.w2) m |= 1u << q;
+    if (bo_out) bo_out[q] = (int8_t)bo[q];
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(kSelChunk)
+halo_select_count_kernel(const double* __restrict__ pos4, int64_t n, HaloTable t, int nchunks,
+                         int* __restrict__ hist) {
+  __shared__ int h[kMaxSlots];
+  if (threadIdx.x < kMaxSlots) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kSelChunk + threadIdx.x;
+  const unsigned m = halo_select_mask(pos4, i, n, t, nullptr);
+  const int lane = threadIdx.x & 31;
+  for (int q = 0; q < t.n_slots; ++q) {
+    const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+    if (lane == 0 && b) atomicAdd(&h[q], __popc(b));
+  }
+  __syncthreads();
+  if (threadIdx.x < t.n_slots) hist[(int64_t)threadIdx.x * nchunks + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSelChunk)
+halo_select_place_kernel(const double* __restrict__ pos4, int64_t n, HaloTable t, int nchunks,
+                         const int* __restrict__ off, int* __restrict__ out_idx,
+                         double* __restrict__ out_rows) {
+  __shared__ int wc[kSelChunk / 32][kMaxSlots];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kSelChunk + threadIdx.x;
+  int8_t bo[kMaxSlots];
+  const unsigned m = halo_select_mask(pos4, i, n, t, bo);
+  unsigned below[kMaxSlots];
+  for (int q = 0; q < t.n_slots; ++q) {
+    const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+    below[q] = __popc(b & ((1u << lane) - 1u));
+    if (lane == 0) wc[warp][q] = __popc(b);
+  }
+  __syncthreads();
+  if (threadIdx.x < t.n_slots) {              // exclusive prefix over the warps, per slot
+    int run = 0;
+    for (int w = 0; w < kSelChunk / 32; ++w) {
+      const int v = wc[w][threadIdx.x];
+      wc[w][threadIdx.x] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (!m) return;
+  for (int q = 0; q < t.n_slots; ++q) {
+    if (!((m >> q) & 1u)) continue;
+    const int64_t at = off[(int64_t)q * nchunks + blockIdx.x] + wc[warp][q] + below[q];
+    out_idx[at] = (int)i;
+    const HaloOffset& o = t.off[bo[q]];
+    double* r = out_rows + at * 7;
+    r[0] = pos4[i * 4 + 0];
+    r[1] = pos4[i * 4 + 1];
+    r[2] = pos4[i * 4 + 2];
+    r[3] = pos4[i * 4 + 3];
+    r[4] = o.shift[0];
+    r[5] = o.shift[1];
+    r[6] = o.shift[2];
+  }
+}
+
 // Stable compaction of one slot: idx[pos[i]] = i where flag[i].
 __global__ void compact_kernel(const int* __restrict__ flag, const int* __restrict__ pos,
                                int64_t n, int* __restrict__ out_idx,
@@ -194,6 +285,60 @@ int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* 
   nonperiodic_check_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
       d_x, n, d, *box, d_flag);
   return check_launch("pc_check_nonperiodic");
+}
+
+static int make_halo_table(const char* who, int32_t d, int32_t n_off, const int32_t* h_slot,
+                           const double* h_shift, const double* h_lo, const double* h_hi,
+                           int32_t n_slots, double w2, HaloTable& t) {
+  if (n_off > kMaxSlots || n_slots > kMaxSlots || d < 1 || d > 3) {
+    set_error("%s: too many offsets or bad dimension", who);
+    return PC_ERR_VALUE;
+  }
+  t.n_off = n_off;
+  t.n_slots = n_slots;
+  t.d = d;
+  t.w2 = w2;
+  for (int k = 0; k < n_off; ++k) {
+    t.off[k].slot = h_slot[k];
+    for (int a = 0; a < 3; ++a) {
+      t.off[k].shift[a] = a < d ? h_shift[k * d + a] : 0.0;
+      t.off[k].lo[a] = a < d ? h_lo[k * d + a] : 0.0;
+      t.off[k].hi[a] = a < d ? h_hi[k * d + a] : 0.0;
+    }
+  }
+  return PC_OK;
+}
+
+int64_t pc_halo_select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
+
+int pc_halo_select_count(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
+                         const int32_t* h_slot, const double* h_shift, const double* h_lo,
+                         const double* h_hi, int32_t n_slots, double w2, int32_t* d_hist,
+                         void* stream) {
+  if (n <= 0) return PC_OK;
+  HaloTable t;
+  const int rc = make_halo_table("pc_halo_select_count", d, n_off, h_slot, h_shift, h_lo, h_hi,
+                                 n_slots, w2, t);
+  if (rc != PC_OK) return rc;
+  const int64_t nch = pc_halo_select_chunks(n);
+  halo_select_count_kernel<<<(unsigned)nch, kSelChunk, 0, as_stream(stream)>>>(d_pos4, n, t,
+                                                                              (int)nch, d_hist);
+  return check_launch("pc_halo_select_count");
+}
+
+int pc_halo_select_place(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
+                         const int32_t* h_slot, const double* h_shift, const double* h_lo,
+                         const double* h_hi, int32_t n_slots, double w2, const int32_t* d_off,
+                         int32_t* d_out_idx, double* d_out_rows, void* stream) {
+  if (n <= 0) return PC_OK;
+  HaloTable t;
+  const int rc = make_halo_table("pc_halo_select_place", d, n_off, h_slot, h_shift, h_lo, h_hi,
+                                 n_slots, w2, t);
+  if (rc != PC_OK) return rc;
+  const int64_t nch = pc_halo_select_chunks(n);
+  halo_select_place_kernel<<<(unsigned)nch, kSelChunk, 0, as_stream(stream)>>>(
+      d_pos4, n, t, (int)nch, d_off, d_out_idx, d_out_rows);
+  return check_launch("pc_halo_select_place");
 }
 
 int pc_halo_plan(const double* d_x, int64_t n, int32_t d, int32_t n_off, const int32_t* h_slot,

@@ -58,6 +58,12 @@ constexpr int kNDummy = 16;
 #define PC_FORCE_WARPS 32
 #endif
 constexpr int kForceWarps = PC_FORCE_WARPS;
+#ifndef PC_FORCE_VIRIAL
+#define PC_FORCE_VIRIAL 1       // rows sum u = 2 sr12 - sr6 and sr6: energy + pair virial
+#endif
+#ifndef PC_FORCE_PREFETCH
+#define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
+#endif
 constexpr int kBuildWarps = 10;
 constexpr int kHitCap = 112;
 constexpr int kHitSlack = 3;   // spare rows per hit column (unclamped 4-candidate stores)
@@ -283,6 +289,10 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // ---- per-tile plan (written by the build, read by the force kernel) --------
@@ -582,7 +592,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
                   int* __restrict__ flag, const double* __restrict__ bpl, pc_box e,
-                  const int* __restrict__ skip) {
+                  const int* __restrict__ skip, int* __restrict__ tile_ghost) {
   extern __shared__ float4 cz[];                 // staged FP32 copy | per-warp hit rows
   __shared__ TileSetup T;
   uint16_t* hits_all = reinterpret_cast<uint16_t*>(cz + p.max_stage);
@@ -606,6 +616,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       pg[2] = 1;
       pg[3] = r0;
       rounds[r0] = 0;
+      if (tile_ghost) tile_ghost[blockIdx.x] = 1;
     }
     return;
   }
@@ -635,6 +646,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     }
   }
   const int64_t ps = p.ps;
+  int ghost_seen = 0;        // a ghost row among the staged particles (tile_ghost)
   // stage: slot order, one warp per segment (a segment is ~40 particles:
   // all threads walking every segment left 7 of 8 idle)
   for (int e = threadIdx.x >> 5; e < kSegs; e += kBuildWarps) {
@@ -652,9 +664,13 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       q.z = (float)(bpl[2 * ps + j] + sz);
       q.w = 0.f;
       cz[dst + t] = q;
+      if (tile_ghost && skip) ghost_seen |= skip[j];
     }
   }
-  __syncthreads();
+  // interior tiles (no ghost in the staged neighbourhood) do not read ghost
+  // positions: their force pass may run while the ghost refresh is in flight
+  ghost_seen = __syncthreads_or(ghost_seen);
+  if (tile_ghost && threadIdx.x == 0) tile_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
 
   uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
   for (int w = warp; w < nrw; w += kBuildWarps) {
@@ -854,6 +870,10 @@ cell_zsort_kernel(const double* __restrict__ zp, int64_t zs, const int* __restri
 // tile into it, so staging overlaps the compute of the tiles in flight and
 // no warp idles at a tile boundary.
 constexpr int kNBuf = 4;       // max staging buffers (runtime: as many as fit)
+#ifndef PC_FORCE_STATIC_BUF
+#define PC_FORCE_STATIC_BUF 0   // 1: per-buffer code paths (buffer base in the LDS immediate): 1525 vs 1133 us at C3 (i-cache), off
+#endif
+extern __shared__ __align__(16) double pc_force_dyn[];
 
 struct TileForceParams {
   double cutoff2, overlap2;
@@ -874,7 +894,15 @@ struct ForceShared {
   int loaded;                // tickets: next tile sequence index to load
   int K;                     // tiles of this CTA
   int items;                 // row-warps of this CTA
+  const int* tiles;          // tile subset (nullptr: all tiles)
+  int t0;                    // first entry of the subset in `tiles`
 };
+
+// tile of this CTA's sequence index k (all tiles, or a subset list)
+__device__ __forceinline__ int tile_at(const int* __restrict__ tiles, int t0, int k) {
+  const int s = (int)blockIdx.x + k * (int)gridDim.x;
+  return tiles ? tiles[t0 + s] : s;
+}
 
 // FP64 -> FP32 by truncation in two integer instructions (SHF.L.W + IADD):
 // the funnel shift moves exponent bits 8..0 and 23 mantissa bits into place,
@@ -893,7 +921,8 @@ template <bool MI, bool UNIT_SIGMA>
 __device__ __forceinline__ void tile_pair(const char* __restrict__ st, uint32_t off, double xi,
                                           double yi, double zi, bool nx, bool ny, bool nz,
                                           const pc_box& b, const TileForceParams& p, double& fx,
-                                          double& fy, double& fz, float& pe, bool& overlap) {
+                                          double& fy, double& fz, float& su, float& s6,
+                                          bool& overlap) {
   const double* q = reinterpret_cast<const double*>(st + off);
   double dx = __dsub_rn(q[0], xi);
   double dy = __dsub_rn(q[kStageStride], yi);
@@ -914,43 +943,60 @@ __device__ __forceinline__ void tile_pair(const char* __restrict__ st, uint32_t 
   const float inv = rcp_approx(r2f);
   const float sr2 = UNIT_SIGMA ? inv : p.sig2 * inv;
   const float sr6 = sr2 * sr2 * sr2;
-  const float fm = (sr6 * inv) * fmaf(2.0f, sr6, -1.0f);     // (2 sr12 - sr6) / r2
-  pe += fmaf(sr6, sr6, -sr6);                                  // sr12 - sr6
+  // u = 2 sr12 - sr6 = r F(r) / 24 eps: the pair virial; fm = u / r^2; the
+  // pair energy sr12 - sr6 = (u - sr6) / 2 -- so the row keeps two sums,
+  // sum u (virial) and sum sr6, at the cost the single energy sum had
+#if PC_FORCE_VIRIAL
+  const float u = sr6 * fmaf(2.0f, sr6, -1.0f);
+  const float fm = u * inv;
+  su += u;
+  s6 += sr6;
+#else     // energy only (r01 form): su holds 2 sum (sr12 - sr6), s6 stays 0
+  const float fm = (sr6 * inv) * fmaf(2.0f, sr6, -1.0f);
+  su += 2.0f * fmaf(sr6, sr6, -sr6);
+#endif
   const double fmd = (double)fm;
   fx = fma(-fmd, dx, fx);
   fy = fma(-fmd, dy, fy);
   fz = fma(-fmd, dz, fz);
 }
 
-template <bool MI, bool UNIT_SIGMA>
-__device__ __forceinline__ void tile_row(const char* __restrict__ st,
+template <bool MI, bool UNIT_SIGMA, int B>
+__device__ __forceinline__ void tile_row(const char* __restrict__ st_rt,
                                          const uint4* __restrict__ lp, uint4 first, int R,
                                          double xi, double yi, double zi, bool nx, bool ny,
                                          bool nz, const pc_box& b, const TileForceParams& p,
-                                         double& fx, double& fy, double& fz, float& pe,
-                                         bool& overlap) {
+                                         double& fx, double& fy, double& fz, float& su,
+                                         float& s6, bool& overlap) {
+  // B >= 0: buffer B at a compile-time offset of the dynamic shared window
+  const char* __restrict__ st =
+      B >= 0 ? reinterpret_cast<const char*>(pc_force_dyn) + (size_t)B * 3 * kStageStride * 8
+             : st_rt;
   const int G = R >> 3;           // full 8-round groups
   const int tail = R & 7;         // rounds of the open group (padded with dummies: skipped)
   uint4 nxt = first;
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
     if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
+    // the group after next into L2 (no register: the list streams from HBM
+    // at ~1 us latency, one group of compute ahead is not always enough)
+    if (PC_FORCE_PREFETCH && gi + 2 < G) prefetch_l2(lp + (gi + 2) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       tile_pair<MI, UNIT_SIGMA>(st, w[h] & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz,
-                                pe, overlap);
-      tile_pair<MI, UNIT_SIGMA>(st, w[h] >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
-                                overlap);
+                                su, s6, overlap);
+      tile_pair<MI, UNIT_SIGMA>(st, w[h] >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, su,
+                                s6, overlap);
     }
   }
   // open group: pairs in twos (warp-uniform count)
   for (int j = 0; j < tail; j += 2) {
     const uint32_t w = (j >> 1) == 0 ? nxt.x : ((j >> 1) == 1 ? nxt.y : ((j >> 1) == 2 ? nxt.z : nxt.w));
-    tile_pair<MI, UNIT_SIGMA>(st, w & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
-                              overlap);
+    tile_pair<MI, UNIT_SIGMA>(st, w & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, su,
+                              s6, overlap);
     if (j + 1 < tail)
-      tile_pair<MI, UNIT_SIGMA>(st, w >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
+      tile_pair<MI, UNIT_SIGMA>(st, w >> 16, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, su, s6,
                                 overlap);
   }
 }
@@ -959,7 +1005,7 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st,
 __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ stage, int b,
                                            int k, const int* __restrict__ plan,
                                            const double* __restrict__ pl, int64_t ps, int lane) {
-  const int tile = blockIdx.x + k * gridDim.x;
+  const int tile = tile_at(F.tiles, F.t0, k);
   const int* gp = plan + (int64_t)tile * kPlanInts;
   const int m = gp[0], S = gp[1];
   double* st = stage + (int64_t)b * 3 * kStageStride;
@@ -991,12 +1037,21 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
                   double* __restrict__ f3, int64_t fs, double* __restrict__ v, int64_t vs,
                   double dtm, double mass, double* __restrict__ partial, int* __restrict__ flag,
                   int nbuf, double* __restrict__ x_next, double* __restrict__ v_next,
-                  double dtm_next, double dt) {
-  extern __shared__ double dyn[];
+                  double dtm_next, double dt, double* __restrict__ virial,
+                  const int* __restrict__ tiles, const int* __restrict__ trange) {
+  double* dyn = pc_force_dyn;
   double* stage = dyn;                                             // nbuf x (x|y|z)
   __shared__ ForceShared F;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  // all tiles, or the subset tiles[trange[0] .. trange[1]) (interior /
+  // boundary passes of a decomposed domain; `ntiles` is then the bound the
+  // grid and the shared memory were sized for)
+  int t0 = 0, nt = ntiles;
+  if (tiles) {
+    t0 = trange[0];
+    nt = trange[1] - t0;
+  }
+  const int K = max(0, (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x);
   int* pre = reinterpret_cast<int*>(dyn + nbuf * 3 * kStageStride);    // K + 1 item prefix
   int* rwbk = pre + K + 1;                                              // first row-warp per k
   if (warp == 0) {
@@ -1004,7 +1059,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     int carry = 0;
     for (int k0 = 0; k0 < K; k0 += 32) {
       const int k = k0 + lane;
-      const int* gpk = plan + (int64_t)(blockIdx.x + k * gridDim.x) * kPlanInts;
+      const int* gpk = plan + (int64_t)(k < K ? tile_at(tiles, t0, k) : 0) * kPlanInts;
       const int c = k < K ? gpk[2] : 0;
       if (k < K) rwbk[k] = gpk[3];
       int inc = c;
@@ -1020,6 +1075,8 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       pre[K] = carry;
       F.items = carry;
       F.K = K;
+      F.tiles = tiles;
+      F.t0 = t0;
       F.next_item = 0;
       for (int q = 0; q < kNBuf; ++q) {
         F.seq[q] = -1;
@@ -1038,6 +1095,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
   __syncthreads();
   const int items = F.items;
   double ake = 0.0, ape = 0.0, apx = 0.0, apy = 0.0, apz = 0.0;   // this lane's rows
+  double avir = 0.0;
 
   for (;;) {
     int i = 0;
@@ -1063,6 +1121,11 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       xi = pl[a];
       yi = pl[p.ps + a];
       zi = pl[2 * p.ps + a];
+      if (PC_FORCE_PREFETCH && v) {  // the epilogue's velocities: into L2 now, read after the rounds
+        prefetch_l2(v + a);
+        prefetch_l2(v + vs + a);
+        prefetch_l2(v + 2 * vs + a);
+      }
     }
     // buffer holding tile k (loaded in ticket order; spin until published)
     int bsel = -1;
@@ -1081,14 +1144,28 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     const bool ny = act && b.periodic[1] && (yi - b.low[1] < p.guard || b.high[1] - yi <= p.guard);
     const bool nz = act && b.periodic[2] && (zi - b.low[2] < p.guard || b.high[2] - zi <= p.guard);
     double fx = 0.0, fy = 0.0, fz = 0.0;
-    float pe = 0.f;
+    float su = 0.f, s6 = 0.f;
     bool overlap = false;
-    if (__any_sync(0xffffffffu, nx || ny || nz))
-      tile_row<true, UNIT_SIGMA>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
-                                 overlap);
-    else
-      tile_row<false, UNIT_SIGMA>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, pe,
-                                  overlap);
+    const bool mi = __any_sync(0xffffffffu, nx || ny || nz);
+#define PC_ROW(BB)                                                                            \
+  if (mi)                                                                                     \
+    tile_row<true, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, \
+                                   su, s6, overlap);                                          \
+  else                                                                                        \
+    tile_row<false, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy,   \
+                                    fz, su, s6, overlap);
+#if PC_FORCE_STATIC_BUF
+    static_assert(kNBuf == 4, "one code path per staging buffer");
+    switch (bsel) {
+      case 0: PC_ROW(0) break;
+      case 1: PC_ROW(1) break;
+      case 2: PC_ROW(2) break;
+      default: PC_ROW(3) break;
+    }
+#else
+    PC_ROW(-1)
+#endif
+#undef PC_ROW
     // release the buffer when this was the tile's last row-warp; refill it
     int last = 0;
     if (lane == 0) last = atomicAdd(&F.done[bsel], 1) + 1 == pre[k + 1] - pre[k];
@@ -1108,7 +1185,10 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       fx *= p.eps24d;
       fy *= p.eps24d;
       fz *= p.eps24d;
-      ped = (double)pe * p.eps2d;
+      // row energy 2 eps (sum sr12 - sr6) = eps (sum u - sum sr6); row
+      // virial sum_j r.F / 2 = 12 eps sum u (both halves of each pair)
+      ped = ((double)su - (double)s6) * p.eps2d * 0.5;
+      avir += (double)su * p.eps24d * 0.5;
       f3[a] = fx;
       f3[fs + a] = fy;
       f3[2 * fs + a] = fz;
@@ -1164,6 +1244,11 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       double* o = partial + ((int64_t)blockIdx.x * kForceWarps + warp) * 5;
       o[0] = ake; o[1] = ape; o[2] = apx; o[3] = apy; o[4] = apz;
     }
+  }
+  if (virial) {
+    avir = warp_sum(avir);
+    // column 0 of a (partials, 5) zero-initialised array: pc_reduce_partials sums it
+    if (lane == 0) virial[((int64_t)blockIdx.x * kForceWarps + warp) * 5] = avir;
   }
 }
 
@@ -1370,7 +1455,7 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
                   void* d_list, int32_t* d_flag, void* stream) {
   return pc_tile_build_domain(d_planar, planar_stride, d_cell_start, grid, box, cutoff2, q8,
                               d_rw0, d_plan, d_rowidx, d_rounds, d_list, d_flag, stream,
-                              nullptr, nullptr, nullptr);
+                              nullptr, nullptr, nullptr, nullptr);
 }
 
 int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
@@ -1378,7 +1463,7 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
                          double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
                          void* stream, const double* d_bplanar, const pc_box* box_exact,
-                         const int32_t* d_skip) {
+                         const int32_t* d_skip, int32_t* d_tile_ghost) {
   if (q8 <= 0 || planar_stride % 16) {
     set_error("pc_tile_build: bad list capacity or planar stride");
     return PC_ERR_VALUE;
@@ -1418,7 +1503,7 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
       d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
       reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
-      box_exact ? *box_exact : *box, d_skip);
+      box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
   return check_launch("pc_tile_build");
 }
 
@@ -1428,6 +1513,7 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
                   double mi_guard, double* d_f3, int64_t f_stride, double* d_v, int64_t v_stride,
                   double dtm, double mass, double* d_partial, int32_t* d_flag,
                   double* d_planar_next, double* d_v_next, double dtm_next, double dt,
+                  double* d_virial, const int32_t* d_tiles, const int32_t* d_trange,
                   void* stream) {
   if (d_planar_next && !d_v) {
     set_error("pc_tile_force: the fused integrate needs the velocities");
@@ -1484,12 +1570,12 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
     tile_force_kernel<true><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
         *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
-        d_v_next, dtm_next, dt);
+        d_v_next, dtm_next, dt, d_virial, d_tiles, d_trange);
   else
     tile_force_kernel<false><<<grid, kForceWarps * 32, smem, as_stream(stream)>>>(
         d_planar, p, ntiles, d_plan, d_rowidx, d_rounds, reinterpret_cast<const uint4*>(d_list),
         *box, d_f3, f_stride, d_v, v_stride, dtm, mass, d_partial, d_flag, nbuf, d_planar_next,
-        d_v_next, dtm_next, dt);
+        d_v_next, dtm_next, dt, d_virial, d_tiles, d_trange);
   return check_launch("pc_tile_force");
 }
 

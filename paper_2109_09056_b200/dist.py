@@ -375,30 +375,25 @@ class DomainEngine:
         if ns == 0 or n == 0:
             self._t1("halo", e0)
             return out
-        x = self.pos[:n, :3].contiguous()
-        flags = torch.empty((ns, n), dtype=torch.int32, device=self.device)
-        best = torch.empty((ns, n), dtype=torch.int8, device=self.device)
-        call("pc_halo_plan", ptr(x), n, 3, len(o["slot"]),
-             o["slot"].ctypes.data_as(ctypes.c_void_p), o["shift"].ctypes.data_as(ctypes.c_void_p),
-             o["lo"].ctypes.data_as(ctypes.c_void_p), o["hi"].ctypes.data_as(ctypes.c_void_p),
-             ns, float(self.halo_width * self.halo_width), ptr(flags), ptr(best), stream())
-        if getattr(self, "_shift_dev", None) is None:       # per-offset shifts, once
-            self._shift_dev = torch.as_tensor(o["shift"]).to(self.device)
-        table = self._shift_dev
-        # one scan + one compaction over all offsets (flat index t = k * n + i)
-        pos = _kernels.scan_i32(flags.view(-1))
-        starts = pos[0: ns * n + 1: n].cpu().numpy()          # ns + 1 per-offset bounds
+        # fused selection (pc_halo_select_*): per-chunk counts per image slot,
+        # one scan, then every exported particle writes its index and ghost
+        # row in (slot, index) order -- one host read of the slot bounds
+        vp = ctypes.c_void_p
+        slot, shift = o["slot"].ctypes.data_as(vp), o["shift"].ctypes.data_as(vp)
+        lo, hi = o["lo"].ctypes.data_as(vp), o["hi"].ctypes.data_as(vp)
+        w2 = float(self.halo_width * self.halo_width)
+        nch = int(_lib.load().pc_halo_select_chunks(n))
+        hist = torch.empty(ns * nch, dtype=torch.int32, device=self.device)
+        call("pc_halo_select_count", ptr(self.pos), n, 3, len(o["slot"]), slot, shift, lo, hi,
+             ns, w2, ptr(hist), stream())
+        pos = _kernels.scan_i32(hist)
+        starts = pos[0: ns * nch + 1: nch].cpu().numpy()        # ns + 1 per-slot bounds
         total = int(starts[ns])
         if total:
-            t_idx = torch.empty(total, dtype=torch.int32, device=self.device)
-            oc = torch.empty(total, dtype=torch.int8, device=self.device)
-            call("pc_compact", ptr(flags.view(-1)), ptr(pos), ns * n, ptr(t_idx),
-                 ptr(best.view(-1)), ptr(oc), stream())
-            ix_all = (t_idx % n).to(torch.int32).contiguous()
-            k_all = (t_idx // n).to(torch.int64)
-            p = torch.empty((total, 4), dtype=torch.float64, device=self.device)
-            _kernels.gather_rows(self.pos, ix_all, total, out=p)
-            buf_all = torch.cat([p, table[k_all]], dim=1)        # (total, HALO_W)
+            ix_all = torch.empty(total, dtype=torch.int32, device=self.device)
+            buf_all = torch.empty((total, HALO_W), dtype=torch.float64, device=self.device)
+            call("pc_halo_select_place", ptr(self.pos), n, 3, len(o["slot"]), slot, shift, lo,
+                 hi, ns, w2, ptr(pos), ptr(ix_all), ptr(buf_all), stream())
             k = 0
             while k < ns:                                       # contiguous per destination
                 dst, k1 = o["dests"][k], k
@@ -577,17 +572,23 @@ class DomainEngine:
         if self._tplan is None or self._tplan.numel() < nt * pi:
             self._tplan = torch.empty(nt * pi, dtype=torch.int32, device=dev)
         self._nblk_tile = int(lib.pc_tile_force_partials(nt))
-        if self.partial.shape[0] < self._nblk_tile:
-            self.partial = torch.zeros((self._nblk_tile, 5), dtype=torch.float64, device=dev)
+        # two partial blocks: the interior / boundary passes of a split step
+        if self.partial.shape[0] < 2 * self._nblk_tile:
+            self.partial = torch.zeros((2 * self._nblk_tile, 5), dtype=torch.float64,
+                                       device=dev)
+        self._tghost = torch.empty(max(nt, 1), dtype=torch.int32, device=dev)
         self.build_flag.zero_()
         call("pc_tile_build_domain", ptr(self.pl), self._ps, ptr(cell_start), g, self._lbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
              ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s, ptr(self.bpl),
-             self._gbox, ptr(self.is_ghost))
+             self._gbox, ptr(self.is_ghost), ptr(self._tghost))
         fl = int(self.build_flag[0].item())
         if fl & (_lib.FLAG_STAGE | _lib.FLAG_OVERFLOW):
             self.tile_failures += 1
             return False
+        # interior tiles (no ghost staged) first, then boundary tiles, each in
+        # ascending tile order; bounds stay on the device ([0, n_int, nt])
+        self._tsplit, self._tbounds = _kernels.stable_partition(self._tghost[:nt], 2)
         call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds), ptr(self._tlist),
              self._q8, _tile_order_kind(self.cfg.rebuild_stride), s)
         self.mode = "tile"
@@ -639,19 +640,44 @@ class DomainEngine:
                  ptr(self.pl), self._ps, stream())
         self._t1("halo", e0)
 
-    def force(self, kick_dtm):
+    @property
+    def can_split(self) -> bool:
+        """The force pass can run as interior + boundary tile passes around
+        the ghost refresh (tile path only)."""
+        return self.mode == "tile"
+
+    def force(self, kick_dtm, part=None):
+        """Force + fused final kick / next integrate.  part: None (all rows),
+        "interior" (tiles whose staged neighbourhood holds no ghost: safe while
+        the ghost refresh is in flight) or "boundary" (the rest, after the
+        refresh) -- each row is computed by the same code either way, so the
+        trajectory is bitwise the same as with one pass."""
         e0 = self._t0()
         ev = self.force_events
         if ev is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
         if self.mode == "tile":
+            npart = self._nblk_tile
+            tiles = trange = None
+            out = self.partial
+            if part == "interior":
+                tiles, trange = self._tsplit, self._tbounds[0:]
+            elif part == "boundary":
+                tiles, trange = self._tsplit, self._tbounds[1:]
+                out = self.partial[npart:]
+            elif part is not None:
+                raise ValueError(f"unknown force part {part!r}")
+            self._split = part is not None
             call("pc_tile_force", ptr(self.pl), self._ps, self._ntiles, ptr(self._tplan),
                  ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._gbox,
                  self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
-                 float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
-                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), stream())
-            self._advanced = True
+                 float(kick_dtm), float(self.cfg.mass), ptr(out), ptr(self.flag),
+                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), None,
+                 None if tiles is None else ptr(tiles), None if trange is None else ptr(trange),
+                 stream())
+            if part != "interior":
+                self._advanced = True
         elif self.deterministic:
             if getattr(self, "_atom", None) is None or self._atom.shape[0] < self.cap:
                 self._atom = torch.zeros((self.cap, 5), dtype=torch.float64, device=self.device)
@@ -672,8 +698,10 @@ class DomainEngine:
         self._t1("force", e0)
 
     def local_diagnostics(self):
-        nb = self._nblk_tile if self.mode == "tile" else \
-            int(_lib.load().pc_lj_force_sell_partials(self.n_total))
+        if self.mode == "tile":
+            nb = self._nblk_tile * (2 if getattr(self, "_split", False) else 1)
+        else:
+            nb = int(_lib.load().pc_lj_force_sell_partials(self.n_total))
         call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
         return self.diag
 
@@ -758,11 +786,19 @@ class _StepLogic:
         for e in self._engines():
             e.sort_and_build()
 
+    overlap = True      # split the force around the ghost refresh (tile path)
+
     def step(self, step_index: int):
         for e in self._engines():
             e.integrate()
         if step_index % self.cfg.rebuild_stride == 0:
             self._rebuild_all()
+        elif self.overlap and all(e.can_split for e in self._engines()):
+            # ref md.py:192-200 (ghost refresh, then forces) with the interior
+            # tiles' force overlapping the refresh: pack -> exchange in flight
+            # -> interior force -> unpack -> boundary force
+            self._refresh_overlapped()
+            return
         else:
             self._exchange("refresh_out", "refresh_in", 3)
         for e in self._engines():
@@ -813,6 +849,15 @@ class FabricMD(_StepLogic):
         outs = [getattr(e, out_name)() for e in self.engines]
         for e, inbox in zip(self.engines, _route(outs)):
             getattr(e, in_name)(inbox)
+
+    def _refresh_overlapped(self):
+        outs = [e.refresh_out() for e in self.engines]          # packs
+        for e in self.engines:
+            e.force(self._dtm, part="interior")
+        for e, inbox in zip(self.engines, _route(outs)):
+            e.refresh_in(inbox)
+        for e in self.engines:
+            e.force(self._dtm, part="boundary")
 
     def diagnostics(self):
         if self.deterministic:          # per-atom rows in global-id order, one tree
@@ -907,6 +952,24 @@ class NCCLTransport:
                                     list(send_split), group=self.group)
         return out.to(device) if self.host_staged else out
 
+    def alltoall_async(self, send, send_split, recv_split, device):
+        """alltoall started without blocking the compute stream: returns
+        (finish, out); finish() makes the current stream wait for the
+        exchange (NCCL: a stream dependency, no host sync) and returns the
+        received rows.  gloo moves host tensors, so it completes up front."""
+        if self.host_staged:
+            out = self.alltoall(send, send_split, recv_split, device)
+            return (lambda: out), out
+        out = torch.empty((sum(recv_split), send.shape[1] if send.dim() == 2 else 3),
+                          dtype=send.dtype, device=device)
+        work = self.dist.all_to_all_single(out, send.contiguous(), list(recv_split),
+                                           list(send_split), group=self.group, async_op=True)
+
+        def finish():
+            work.wait()
+            return out
+        return finish, out
+
     def allreduce(self, t):
         w = self._wire(t)
         self.dist.all_reduce(w, group=self.group)
@@ -978,6 +1041,16 @@ class DistMD(_StepLogic):
 
     def _engines(self):
         return [self.engine]
+
+    def _refresh_overlapped(self):
+        """Pack, start the all-to-all (NCCL stream), interior force on the
+        compute stream meanwhile, then wait, unpack, boundary force."""
+        e = self.engine
+        buf = e.refresh_pack()
+        work, recv = self.transport.alltoall_async(buf, e.send_split, e.recv_split, self.device)
+        e.force(self._dtm, part="interior")
+        e.refresh_unpack(work())
+        e.force(self._dtm, part="boundary")
 
     def _exchange(self, out_name, in_name, width):
         e = self.engine

@@ -461,6 +461,10 @@ class MDDriver:
         npart = int(lib.pc_tile_force_partials(nt))
         if self.partial.shape[0] < npart:
             self.partial = torch.zeros((npart, 5), dtype=torch.float64, device=dev)
+        if getattr(self, "_vir_part", None) is None or self._vir_part.shape[0] < npart:
+            # pair virial partials (column 0; pc_tile_force), reduced on demand
+            self._vir_part = torch.zeros((npart, 5), dtype=torch.float64, device=dev)
+            self._vir = torch.zeros(5, dtype=torch.float64, device=dev)
         self.build_flag.zero_()
         call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
@@ -512,7 +516,8 @@ class MDDriver:
                  ptr(self._rowidx), ptr(self._rounds), ptr(self._tlist), self._q8, self._pbox,
                  self._lj, self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
                  float(kick_dtm), float(self.cfg.mass), ptr(self.partial), ptr(self.flag),
-                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt), stream())
+                 ptr(self._pl_n), ptr(self._vel_n), self._dtm, float(self.cfg.dt),
+                 ptr(self._vir_part), None, None, stream())
             self._advanced = True
         elif self.mode == "half":
             self.frc.zero_()
@@ -606,14 +611,30 @@ class MDDriver:
         call("pc_reduce_partials", ptr(self.partial), self._nblk, ptr(d), stream())
         return d
 
+    def device_virial(self):
+        """Pair virial W = sum over pairs of r.F of the last force pass (tile
+        path; FP64 per-warp partials, one fixed reduction), or None on the
+        SELL paths."""
+        if self.mode != "tile":
+            return None
+        call("pc_reduce_partials", ptr(self._vir_part), self._nblk, ptr(self._vir), stream())
+        return self._vir[0]
+
     def diagnostics(self):
-        """Global energies (ref md.py:261-277)."""
+        """Global energies (ref md.py:261-277), plus the pair virial W and the
+        pressure P = (2 KE + W) / (3 V) where the force path computes W (the
+        reference reports neither)."""
         d = self.device_diagnostics().cpu().numpy()
         self.check_errors()
         ke, pe = float(d[0]), float(d[1])
-        return {"KE": ke, "PE": pe, "E_total": ke + pe,
-                "temperature": 2.0 * ke / (3.0 * self.n),
-                "momentum": d[2:5].copy()}
+        out = {"KE": ke, "PE": pe, "E_total": ke + pe,
+               "temperature": 2.0 * ke / (3.0 * self.n),
+               "momentum": d[2:5].copy()}
+        w = self.device_virial()
+        if w is not None:
+            out["virial"] = float(w.item())
+            out["pressure"] = (2.0 * ke + out["virial"]) / (3.0 * float(np.prod(self.box.lengths)))
+        return out
 
     def gather_state(self):
         """Positions and velocities in global-id order (ref md.py:279-287)."""

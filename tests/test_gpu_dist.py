@@ -142,3 +142,29 @@ def test_strides_transparent(pc):
         assert np.max(np.abs(got - base) / np.abs(base)) <= 1e-9
     tile = _run(pc.md.MDDriver(pc.md.MDConfig(**dict(kw, skin=0.3, rebuild_stride=5))), 40)
     assert np.max(np.abs(tile - base) / np.abs(base)) <= 1e-6
+
+
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 2)])
+def test_fabric_overlap_split_bitwise(pc, dims):
+    """The force pass split into interior tiles (staged neighbourhood free of
+    ghosts: run while the ghost refresh is in flight) and boundary tiles
+    reproduces the one-pass step bitwise in positions and velocities (every
+    row is computed by the same code); energies differ only in the grouping
+    of the per-warp partial sums (1e-12).  VERDICT r1 next #4."""
+    import torch
+    kw = dict(lattice_cells=12, density=0.8442, temperature=1.44, cutoff=2.5, skin=0.3,
+              rebuild_stride=5, seed=1, steps=0, rank_dims=dims)
+    runs = []
+    for overlap in (False, True):
+        fab = pc.dist.FabricMD(pc.md.MDConfig(**kw))
+        fab.overlap = overlap
+        assert all(e.mode == "tile" for e in fab.engines)
+        es = _run(fab, 12)
+        x, v = fab.gather_state()
+        n_int = [int(e._tbounds[1].item()) for e in fab.engines]
+        runs.append((es, x, v, n_int, [e._ntiles for e in fab.engines]))
+    (ea, xa, va, _, _), (eb, xb, vb, n_int, nt) = runs
+    assert all(0 < a < b for a, b in zip(n_int, nt))       # both passes non-empty
+    assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+    assert np.max(np.abs(ea - eb) / np.abs(ea)) < 1e-12
+    del torch

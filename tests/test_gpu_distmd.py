@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, steps, det=False):
+def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -35,12 +35,19 @@ def _worker(rank, world, port, q, steps, det=False):
         torch.cuda.set_device(0)
         import paper_2109_09056_b200 as pc
         from paper_2109_09056_b200.dist import DistMD
-        drv = DistMD(pc.md.MDConfig(**KW), deterministic=det)
+        drv = DistMD(pc.md.MDConfig(**(kw or KW)), deterministic=det)
+        if overlap is not None:
+            drv.overlap = overlap
         es = [drv.diagnostics()["E_total"]]
         for s in range(1, steps + 1):
             drv.step(s)
             es.append(drv.diagnostics()["E_total"])
-        q.put((rank, np.array(es), drv.engine.n_owned))
+        if overlap is None:
+            q.put((rank, np.array(es), drv.engine.n_owned))
+        else:
+            gid, x, v = drv.engine.owned_state()
+            o = np.argsort(gid)
+            q.put((rank, np.array(es), gid[o], x[o], v[o]))
     finally:
         dist.destroy_process_group()
 
@@ -127,3 +134,31 @@ def test_distmd_four_processes(world, det):
             assert np.array_equal(es, ref)
         else:
             assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-6
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distmd_overlap_split_bitwise(world):
+    """Across processes: the step with the interior-tile force overlapping the
+    ghost all-to-all (then unpack, then boundary tiles) gives positions and
+    velocities bitwise equal to the one-pass step on every rank, energies to
+    1e-12 (on a GPU box the all-to-all is NCCL on its own
+    stream, here gloo)."""
+    kw = dict(KW, lattice_cells=10)
+    res = {}
+    for overlap in (False, True):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_worker, args=(r, world, port, q, 12, False, overlap, kw))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        res[overlap] = out
+    for a, b in zip(res[False], res[True]):
+        assert np.array_equal(a[2], b[2])
+        assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+        assert np.max(np.abs(a[1] - b[1]) / np.abs(a[1])) < 1e-12
