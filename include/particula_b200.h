@@ -472,6 +472,16 @@ int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
  * (ref decomp.py:92-96). */
 int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* box,
                          int32_t* d_flag, void* stream);
+/* Reverse halo of the half-list (Newton-3) decomposed engine (ref
+ * decomp.py:263-300, halo_scatter): pc_halo_force_pack copies the planar
+ * forces of rows d_rows[k] (ghosts, source-rank order) into d_buf (m x 3)
+ * and clears them; pc_halo_force_add adds d_buf (m x 3) onto rows d_rows[k]
+ * (owners, in export order) with FP64 atomics -- a particle exported as
+ * several images appears several times. */
+int pc_halo_force_pack(double* d_f3, int64_t f_stride, const int32_t* d_rows, int64_t m,
+                       double* d_buf, void* stream);
+int pc_halo_force_add(double* d_f3, int64_t f_stride, const int32_t* d_rows, int64_t m,
+                      const double* d_buf, void* stream);
 /* Fused halo selection for the decomposed MD engine (same export set and
  * (slot, particle index) order as pc_halo_plan + scan + pc_compact, ref
  * decomp.py:143-228), reading pos4 rows (x, y, z, id bits) directly:
@@ -519,6 +529,16 @@ int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double
 int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,
                    const double* d_src, void* stream);
 
+/* Exact, order-independent column sums of (n x w) FP64 rows (w <= 8; rows
+ * with d_skip[i] != 0 left out; |values| < 2^50, bits below 2^-90
+ * truncated): pc_exact_sum ADDS each column's integer part and three 30-bit
+ * fraction limbs into d_limbs (w x 4 int64, zeroed by the caller; integer
+ * sums, so limbs of disjoint row sets -- threads, ranks, devices -- simply
+ * add); pc_exact_finish converts the limbs into w doubles.  The
+ * deterministic mode's energies (ref md.py:261-277). */
+int pc_exact_sum(const double* d_rows, int64_t n, int32_t w, const int32_t* d_skip,
+                 int64_t* d_limbs, void* stream);
+int pc_exact_finish(const int64_t* d_limbs, int32_t w, double* d_out, void* stream);
 /* Sum per-block partials (nblocks x 5) into out[5] in a fixed order. */
 int pc_reduce_partials(const double* d_partial, int32_t nblocks, double* d_out,
                        void* stream);

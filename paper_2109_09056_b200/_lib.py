@@ -111,6 +111,10 @@ SIGNATURES = {
     "pc_halo_plan": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                     c_dbl, c_vp, c_vp, c_vp]),
     "pc_compact": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "pc_exact_sum": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "pc_exact_finish": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
+    "pc_halo_force_pack": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "pc_halo_force_add": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "pc_halo_select_chunks": (c_i64, [c_i64]),
     "pc_halo_select_count": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                             c_i32, c_dbl, c_vp, c_vp]),

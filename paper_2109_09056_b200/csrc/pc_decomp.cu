@@ -107,26 +107,41 @@ __global__ void halo_plan_kernel(const double* __restrict__ x, int64_t n, HaloTa
 // (x, y, z, global-id bits, shift of the winning image) at its place.
 constexpr int kSelChunk = 1024;
 
-__device__ __forceinline__ unsigned halo_select_mask(const double* __restrict__ pos4, int64_t i,
-                                                     int64_t n, const HaloTable& t,
-                                                     int8_t* bo_out) {
-  if (i >= n) return 0u;
-  double xi[3] = {0.0, 0.0, 0.0};
-  for (int a = 0; a < t.d; ++a) xi[a] = pos4[i * 4 + a];
-  double best[kMaxSlots];
-  int bo[kMaxSlots];
-  for (int q = 0; q < t.n_slots; ++q) { best[q] = INFINITY; bo[q] = -1; }
+// winning image of slot q (strict <, first offset in product order wins)
+__device__ __forceinline__ int halo_best_offset(const double* xi, const HaloTable& t, int q,
+                                                double& best) {
+  best = INFINITY;
+  int bo = -1;
   for (int k = 0; k < t.n_off; ++k) {
-    const int q = t.off[k].slot;
+    if (t.off[k].slot != q) continue;
     const double d2 = dist2_box(xi, t.off[k], t.d);
-    if (bo[q] < 0 || d2 < best[q]) { best[q] = d2; bo[q] = k; }
+    if (bo < 0 || d2 < best) { best = d2; bo = k; }
   }
+  return bo;
+}
+
+// export mask over slots; `ident`: slots 1:1 with offsets (one slot per image,
+// the decomposed engine's layout) -- no per-slot minimum, no local arrays
+__device__ __forceinline__ unsigned halo_select_mask(const double* xi, const HaloTable& t,
+                                                     bool ident) {
   unsigned m = 0u;
-  for (int q = 0; q < t.n_slots; ++q) {
-    if (best[q] < t.w2) m |= 1u << q;
-    if (bo_out) bo_out[q] = (int8_t)bo[q];
+  if (ident) {
+    for (int k = 0; k < t.n_off; ++k)
+      if (dist2_box(xi, t.off[k], t.d) < t.w2) m |= 1u << k;
+  } else {
+    for (int q = 0; q < t.n_slots; ++q) {
+      double best;
+      halo_best_offset(xi, t, q, best);
+      if (best < t.w2) m |= 1u << q;
+    }
   }
   return m;
+}
+
+__device__ __forceinline__ bool halo_ident(const HaloTable& t) {
+  bool id = t.n_slots == t.n_off;
+  for (int k = 0; k < t.n_off; ++k) id &= t.off[k].slot == k;
+  return id;
 }
 
 __global__ void __launch_bounds__(kSelChunk)
@@ -136,11 +151,17 @@ halo_select_count_kernel(const double* __restrict__ pos4, int64_t n, HaloTable t
   if (threadIdx.x < kMaxSlots) h[threadIdx.x] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kSelChunk + threadIdx.x;
-  const unsigned m = halo_select_mask(pos4, i, n, t, nullptr);
+  unsigned m = 0u;
+  if (i < n) {
+    const double xi[3] = {pos4[i * 4], pos4[i * 4 + 1], pos4[i * 4 + 2]};
+    m = halo_select_mask(xi, t, halo_ident(t));
+  }
   const int lane = threadIdx.x & 31;
+  const unsigned any = __reduce_or_sync(0xffffffffu, m);
   for (int q = 0; q < t.n_slots; ++q) {
+    if (!((any >> q) & 1u)) continue;               // warp-uniform
     const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
-    if (lane == 0 && b) atomicAdd(&h[q], __popc(b));
+    if (lane == 0) atomicAdd(&h[q], __popc(b));
   }
   __syncthreads();
   if (threadIdx.x < t.n_slots) hist[(int64_t)threadIdx.x * nchunks + blockIdx.x] = h[threadIdx.x];
@@ -153,12 +174,21 @@ halo_select_place_kernel(const double* __restrict__ pos4, int64_t n, HaloTable t
   __shared__ int wc[kSelChunk / 32][kMaxSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kSelChunk + threadIdx.x;
-  int8_t bo[kMaxSlots];
-  const unsigned m = halo_select_mask(pos4, i, n, t, bo);
-  unsigned below[kMaxSlots];
+  const bool ident = halo_ident(t);
+  double xi[3] = {0.0, 0.0, 0.0};
+  unsigned m = 0u;
+  if (i < n) {
+    xi[0] = pos4[i * 4];
+    xi[1] = pos4[i * 4 + 1];
+    xi[2] = pos4[i * 4 + 2];
+    m = halo_select_mask(xi, t, ident);
+  }
+  const unsigned any = __reduce_or_sync(0xffffffffu, m);
+  for (int q = lane; q < t.n_slots; q += 32) wc[warp][q] = 0;
+  __syncwarp();
   for (int q = 0; q < t.n_slots; ++q) {
+    if (!((any >> q) & 1u)) continue;
     const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
-    below[q] = __popc(b & ((1u << lane) - 1u));
     if (lane == 0) wc[warp][q] = __popc(b);
   }
   __syncthreads();
@@ -171,21 +201,52 @@ halo_select_place_kernel(const double* __restrict__ pos4, int64_t n, HaloTable t
     }
   }
   __syncthreads();
-  if (!m) return;
   for (int q = 0; q < t.n_slots; ++q) {
+    if (!((any >> q) & 1u)) continue;
+    const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
     if (!((m >> q) & 1u)) continue;
-    const int64_t at = off[(int64_t)q * nchunks + blockIdx.x] + wc[warp][q] + below[q];
+    const int64_t at = off[(int64_t)q * nchunks + blockIdx.x] + wc[warp][q] +
+                       __popc(b & ((1u << lane) - 1u));
+    double best;
+    const int k = ident ? q : halo_best_offset(xi, t, q, best);
     out_idx[at] = (int)i;
-    const HaloOffset& o = t.off[bo[q]];
+    const HaloOffset& o = t.off[k];
     double* r = out_rows + at * 7;
-    r[0] = pos4[i * 4 + 0];
-    r[1] = pos4[i * 4 + 1];
-    r[2] = pos4[i * 4 + 2];
+    r[0] = xi[0];
+    r[1] = xi[1];
+    r[2] = xi[2];
     r[3] = pos4[i * 4 + 3];
     r[4] = o.shift[0];
     r[5] = o.shift[1];
     r[6] = o.shift[2];
   }
+}
+
+// ---- reverse halo of the half-list (Newton-3) MD engine --------------------
+// ref decomp.py:263-300 (halo_scatter): ghost rows' accumulated forces go
+// back to their owners.  Pack: buf[k] = f[:, rows[k]] (planar force, stride
+// fs) and the ghost row's force is cleared (so the kick leaves ghost
+// velocities at zero); add: f[:, rows[k]] += buf[k] with FP64 atomics (a
+// particle exported as several images appears several times in `rows`).
+__global__ void halo_force_pack_kernel(double* __restrict__ f, int64_t fs,
+                                       const int* __restrict__ rows, int64_t m,
+                                       double* __restrict__ buf) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t r = rows[k];
+  for (int a = 0; a < 3; ++a) {
+    buf[k * 3 + a] = f[a * fs + r];
+    f[a * fs + r] = 0.0;
+  }
+}
+
+__global__ void halo_force_add_kernel(double* __restrict__ f, int64_t fs,
+                                      const int* __restrict__ rows, int64_t m,
+                                      const double* __restrict__ buf) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t r = rows[k];
+  for (int a = 0; a < 3; ++a) atomicAdd(f + a * fs + r, buf[k * 3 + a]);
 }
 
 // Stable compaction of one slot: idx[pos[i]] = i where flag[i].
@@ -365,6 +426,22 @@ int pc_halo_plan(const double* d_x, int64_t n, int32_t d, int32_t n_off, const i
   halo_plan_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(d_x, n, t, d_flags,
                                                                                d_best_off);
   return check_launch("pc_halo_plan");
+}
+
+int pc_halo_force_pack(double* d_f3, int64_t f_stride, const int32_t* d_rows, int64_t m,
+                       double* d_buf, void* stream) {
+  if (m <= 0) return PC_OK;
+  halo_force_pack_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_f3, f_stride, d_rows, m, d_buf);
+  return check_launch("pc_halo_force_pack");
+}
+
+int pc_halo_force_add(double* d_f3, int64_t f_stride, const int32_t* d_rows, int64_t m,
+                      const double* d_buf, void* stream) {
+  if (m <= 0) return PC_OK;
+  halo_force_add_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_f3, f_stride, d_rows, m, d_buf);
+  return check_launch("pc_halo_force_add");
 }
 
 int pc_compact(const int32_t* d_flag, const int32_t* d_pos, int64_t n, int32_t* d_out_idx,

@@ -153,6 +153,80 @@ reduce_partials_kernel(const double* __restrict__ partial, int nblocks, double* 
   }
 }
 
+// ---- exact, order-independent sums (deterministic mode) --------------------
+// Each FP64 value v (|v| < 2^50) is split exactly into an integer part and
+// three 30-bit fraction limbs: v = i + (f1 2^60 + f2 2^30 + f3) 2^-90 - r,
+// 0 <= r < 2^-90 (the bits below 2^-90 are truncated).  Limb sums are
+// integer additions, so any partition of the atoms over threads, blocks,
+// ranks or devices gives the same limb totals: the energies of a
+// decomposed run equal the single-domain ones bit for bit (ref md.py:7-11,
+// 261-277: "sums in global-id order" -- here the order does not matter at
+// all), and ranks combine 4 x width int64 instead of one row per atom.
+constexpr int kExactLimbs = 4;
+constexpr int kExactMaxW = 8;
+
+__device__ __forceinline__ void exact_split(double v, long long* l) {
+  const double hi = floor(v);
+  double f = (v - hi) * 1073741824.0;            // exact: v - floor(v), * 2^30
+  const double f1 = floor(f);
+  f = (f - f1) * 1073741824.0;
+  const double f2 = floor(f);
+  f = (f - f2) * 1073741824.0;
+  const double f3 = floor(f);
+  l[0] = (long long)hi;
+  l[1] = (long long)f1;
+  l[2] = (long long)f2;
+  l[3] = (long long)f3;
+}
+
+__global__ void exact_sum_kernel(const double* __restrict__ rows, int64_t n, int w,
+                                 const int* __restrict__ skip, long long* __restrict__ limbs) {
+  long long acc[kExactMaxW][kExactLimbs];
+#pragma unroll
+  for (int c = 0; c < kExactMaxW; ++c)
+#pragma unroll
+    for (int q = 0; q < kExactLimbs; ++q) acc[c][q] = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (skip && skip[i]) continue;
+#pragma unroll
+    for (int c = 0; c < kExactMaxW; ++c) {
+      if (c >= w) break;
+      long long l[kExactLimbs];
+      exact_split(rows[i * w + c], l);
+#pragma unroll
+      for (int q = 0; q < kExactLimbs; ++q) acc[c][q] += l[q];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kExactMaxW; ++c) {
+    if (c >= w) break;
+#pragma unroll
+    for (int q = 0; q < kExactLimbs; ++q) {
+      long long v = acc[c][q];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0 && v)
+        atomicAdd(reinterpret_cast<unsigned long long*>(limbs + c * kExactLimbs + q),
+                  (unsigned long long)v);
+    }
+  }
+}
+
+// limbs -> doubles: carry-normalise the fraction limbs into [0, 2^30), then
+// i + F 2^-90 with F = (f1 2^60 + f2 2^30 + f3) (deterministic rounding)
+__global__ void exact_finish_kernel(const long long* __restrict__ limbs, int w,
+                                    double* __restrict__ out) {
+  const int c = threadIdx.x;
+  if (c >= w) return;
+  const long long M = 1LL << 30;
+  long long i = limbs[c * 4], f1 = limbs[c * 4 + 1], f2 = limbs[c * 4 + 2], f3 = limbs[c * 4 + 3];
+  long long k = f3 >> 30; f3 -= k * M; f2 += k;        // arithmetic shifts: floor division
+  k = f2 >> 30; f2 -= k * M; f1 += k;
+  k = f1 >> 30; f1 -= k * M; i += k;
+  const double frac = ((double)f1 * 1073741824.0 + (double)f2) * 1073741824.0 + (double)f3;
+  out[c] = (double)i + frac * 8.077935669463161e-28;     // 2^-90
+}
+
 // Box.wrap / Box.min_image on (rows, d) arrays (ref geometry.py:40-58).
 __global__ void box_wrap_kernel(double* __restrict__ x, int64_t rows, int d, pc_box b) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -271,6 +345,30 @@ int pc_lj_pair(const double* d_dx, const double* d_r2, int64_t n, double eps, do
   lj_pair_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_dx, d_r2, n, eps,
                                                                              sigma, d_e, d_f);
   return check_launch("pc_lj_pair");
+}
+
+int pc_exact_sum(const double* d_rows, int64_t n, int32_t w, const int32_t* d_skip,
+                 int64_t* d_limbs, void* stream) {
+  if (w < 1 || w > kExactMaxW) {
+    set_error("pc_exact_sum: width must be in [1, %d]", kExactMaxW);
+    return PC_ERR_VALUE;
+  }
+  if (n <= 0) return PC_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  exact_sum_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      d_rows, n, w, d_skip, reinterpret_cast<long long*>(d_limbs));
+  return check_launch("pc_exact_sum");
+}
+
+int pc_exact_finish(const int64_t* d_limbs, int32_t w, double* d_out, void* stream) {
+  if (w < 1 || w > kExactMaxW) {
+    set_error("pc_exact_finish: width must be in [1, %d]", kExactMaxW);
+    return PC_ERR_VALUE;
+  }
+  exact_finish_kernel<<<1, 32, 0, as_stream(stream)>>>(
+      reinterpret_cast<const long long*>(d_limbs), w, d_out);
+  return check_launch("pc_exact_finish");
 }
 
 int pc_reduce_partials(const double* d_partial, int32_t nblocks, double* d_out, void* stream) {

@@ -61,6 +61,9 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_VIRIAL
 #define PC_FORCE_VIRIAL 1       // rows sum u = 2 sr12 - sr6 and sr6: energy + pair virial
 #endif
+#ifndef PC_FORCE_NEXT
+#define PC_FORCE_NEXT 1         // claim items one ahead: next row's index loaded, its data L2-prefetched
+#endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
@@ -1097,21 +1100,53 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
   double ake = 0.0, ape = 0.0, apx = 0.0, apy = 0.0, apz = 0.0;   // this lane's rows
   double avir = 0.0;
 
-  for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(&F.next_item, 1);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= items) break;
-    // tile sequence index of item i (pre is ascending; K is small)
+  // tile sequence index and global row-warp of item i (pre is ascending; K is small)
+  auto locate = [&](int i, int& k) -> int {
     int lo = 0, hi = K - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (pre[mid] <= i) lo = mid; else hi = mid - 1;
     }
-    const int k = lo;
-    const int rw = rwbk[k] + (i - pre[k]);
-    // prefetch everything that does not depend on the staged tile
+    k = lo;
+    return rwbk[lo] + (i - pre[lo]);
+  };
+#if PC_FORCE_NEXT
+  // items are claimed one ahead: the next row-warp's row index is loaded
+  // (and its positions / velocities prefetched into L2) while this one runs
+  int i_next = 0;
+  if (lane == 0) i_next = atomicAdd(&F.next_item, 1);
+  i_next = __shfl_sync(0xffffffffu, i_next, 0);
+  int a_next = -1;
+  if (i_next < items) {
+    int kn;
+    a_next = rowidx[(int64_t)locate(i_next, kn) * 32 + lane];
+  }
+#endif
+  for (;;) {
+#if PC_FORCE_NEXT
+    const int i = i_next;
+    if (i >= items) break;
+    if (lane == 0) i_next = atomicAdd(&F.next_item, 1);
+    i_next = __shfl_sync(0xffffffffu, i_next, 0);
+    int k;
+    const int rw = locate(i, k);
+    const int a = a_next;
+    int rw_next = -1;
+    if (i_next < items) {
+      int kn;
+      rw_next = locate(i_next, kn);
+      a_next = rowidx[(int64_t)rw_next * 32 + lane];
+    }
+#else
+    int i = 0;
+    if (lane == 0) i = atomicAdd(&F.next_item, 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= items) break;
+    int k;
+    const int rw = locate(i, k);
     const int a = rowidx[(int64_t)rw * 32 + lane];
+#endif
+    // prefetch everything that does not depend on the staged tile
     const int R = rounds[rw];
     const uint4* lp = list + (int64_t)rw * p.Q8 * 32 + lane;
     const uint4 first = R > 0 ? ld_stream(lp) : make_uint4(0u, 0u, 0u, 0u);
@@ -1166,6 +1201,21 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     PC_ROW(-1)
 #endif
 #undef PC_ROW
+#if PC_FORCE_NEXT
+    if (rw_next >= 0) {      // next row-warp's positions, velocities, first list word -> L2
+      if (a_next >= 0) {
+        prefetch_l2(pl + a_next);
+        prefetch_l2(pl + p.ps + a_next);
+        prefetch_l2(pl + 2 * p.ps + a_next);
+        if (v) {
+          prefetch_l2(v + a_next);
+          prefetch_l2(v + vs + a_next);
+          prefetch_l2(v + 2 * vs + a_next);
+        }
+      }
+      prefetch_l2(list + (int64_t)rw_next * p.Q8 * 32 + lane);
+    }
+#endif
     // release the buffer when this was the tile's last row-warp; refill it
     int last = 0;
     if (lane == 0) last = atomicAdd(&F.done[bsel], 1) + 1 == pre[k + 1] - pre[k];

@@ -69,7 +69,7 @@ class DomainEngine:
 
     def __init__(self, cfg: MDConfig, fabric: DomainFabric, rank: int, x, v, gid, device,
                  ell_width: int = 128, planar_gather: bool = True, time_phases: bool = False,
-                 tile: bool = True, deterministic: bool = False):
+                 tile: bool = True, deterministic: bool = False, half_list: bool = False):
         self.cfg = cfg
         self.fabric = fabric
         self.rank = rank
@@ -92,6 +92,15 @@ class DomainEngine:
         self.deterministic = bool(deterministic)
         if self.deterministic:
             tile, planar_gather = False, True
+        # Newton-3 half list (K7 + K12): each pair once on exactly one rank
+        # (row i owned, neighbour j with gid_j > gid_i, ghost or owned), FP64
+        # atomics on both sides, ghost forces sent back to their owners
+        # (reverse halo, ref decomp.py:263-300), then the final kick
+        self.half = bool(half_list)
+        if self.half and self.deterministic:
+            raise ValueError("the half-list engine is not deterministic (FP64 atomics)")
+        if self.half:
+            tile = False
         self.planar_gather = planar_gather or tile
         # tile path (pc_tile.cu, as the single-domain engine): local grid,
         # binpos-staged FP32 prefilter, raw positions + global minimum image
@@ -515,9 +524,12 @@ class DomainEngine:
             self.rebuilds += 1
             self._t1("neighbor", e0)
             return
-        self.mode = "sell"
+        self.mode = "half" if self.half else "sell"
         used = ctypes.c_int32(0)
-        staged = True
+        # half list: the per-particle kernel, whose half test compares global
+        # ids (gid_j > gid_i) -- the rule that puts every cross-rank pair on
+        # exactly one rank; ghost rows are emptied below
+        staged = not self.half
         while True:
             self.build_flag.zero_()
             if staged:
@@ -527,9 +539,9 @@ class DomainEngine:
                      ptr(self.binpos), self._gbox, 0)
             else:
                 call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
-                     self._lbox, self._search2, 0, _lib.PC_NBR_SELL, 0, ptr(self.cnt), None,
-                     ptr(self.nbr), self.cap, self.ell_width, ptr(self.build_flag), s,
-                     ptr(self.binpos), self._gbox)
+                     self._lbox, self._search2, int(self.half), _lib.PC_NBR_SELL, 0,
+                     ptr(self.cnt), None, ptr(self.nbr), self.cap, self.ell_width,
+                     ptr(self.build_flag), s, ptr(self.binpos), self._gbox)
             fl = int(self.build_flag[0].item())
             if fl & _lib.FLAG_STAGE:
                 staged = False
@@ -588,7 +600,8 @@ class DomainEngine:
             return False
         # interior tiles (no ghost staged) first, then boundary tiles, each in
         # ascending tile order; bounds stay on the device ([0, n_int, nt])
-        self._tsplit, self._tbounds = _kernels.stable_partition(self._tghost[:nt], 2)
+        self._tsplit, bounds = _kernels.stable_partition(self._tghost[:nt], 2)
+        self._tbounds = bounds.contiguous()          # (a strided view of the scan)
         call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds), ptr(self._tlist),
              self._q8, _tile_order_kind(self.cfg.rebuild_stride), s)
         self.mode = "tile"
@@ -678,6 +691,13 @@ class DomainEngine:
                  stream())
             if part != "interior":
                 self._advanced = True
+        elif self.half:
+            # local pair forces only: owned and ghost rows accumulate (FP64
+            # atomics); reverse_pack / reverse_add and kick() complete the step
+            self.frc.zero_()
+            call("pc_lj_force_sell_half", ptr(self.pos), self.n_total, ptr(self.cnt),
+                 ptr(self.nbr), self.ell_width, self._gbox, self._lj, self._mi_guard,
+                 ptr(self.frc), self.cap, ptr(self.partial), ptr(self.flag), stream())
         elif self.deterministic:
             if getattr(self, "_atom", None) is None or self._atom.shape[0] < self.cap:
                 self._atom = torch.zeros((self.cap, 5), dtype=torch.float64, device=self.device)
@@ -697,7 +717,68 @@ class DomainEngine:
             ev.append((a, b))
         self._t1("force", e0)
 
+    # ---- half list: reverse halo + kick (K12) ---------------------------------
+    def reverse_out(self):
+        """Ghost forces per source rank (and cleared on the ghost rows)."""
+        e0 = self._t0()
+        out = {}
+        for src, rows in self.ghost_blocks:
+            m = rows.numel()
+            buf = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+            call("pc_halo_force_pack", ptr(self.frc), self.cap, ptr(rows), m, ptr(buf), stream())
+            out[src] = buf
+        self._t1("halo", e0)
+        return out
+
+    def reverse_in(self, inbox):
+        """Add the forces our ghosts received on other ranks onto the owned
+        rows they were exported from (halo_scatter, ref decomp.py:281-293)."""
+        e0 = self._t0()
+        for dst, rows in self.export_rows.items():
+            if dst in inbox:
+                call("pc_halo_force_add", ptr(self.frc), self.cap, ptr(rows), rows.numel(),
+                     ptr(inbox[dst]), stream())
+        self._t1("halo", e0)
+
+    def reverse_pack(self):
+        """All ghost forces in one buffer (ghost_all: source-rank order)."""
+        m = int(self.ghost_all.numel())
+        buf = torch.empty((m, 3), dtype=torch.float64, device=self.device)
+        if m:
+            call("pc_halo_force_pack", ptr(self.frc), self.cap, ptr(self.ghost_all), m,
+                 ptr(buf), stream())
+        return buf
+
+    def reverse_add(self, buf):
+        """Received ghost forces (export_all: destination-rank order) onto owners."""
+        m = int(self.export_all.numel())
+        if m:
+            call("pc_halo_force_add", ptr(self.frc), self.cap, ptr(self.export_all), m,
+                 ptr(buf), stream())
+
+    def kick(self, kick_dtm):
+        """Final half kick v += dtm f of the half-list step (ghost rows: f = 0
+        after reverse_out, so their zero velocities stay) + KE partials."""
+        e0 = self._t0()
+        nk = int(_lib.load().pc_lj_force_blocks(self.n_total))
+        if getattr(self, "partial_k", None) is None or self.partial_k.shape[0] < nk:
+            self.partial_k = torch.zeros((max(nk, 1), 5), dtype=torch.float64,
+                                         device=self.device)
+        call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n_total,
+             float(kick_dtm), float(self.cfg.mass), ptr(self.partial_k), stream())
+        self._t1("integrate", e0)
+
     def local_diagnostics(self):
+        if self.half:
+            # KE / momentum from the kick partials, PE from the force partials
+            nb = int(_lib.load().pc_lj_force_sell_partials(self.n_total))
+            call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
+            nk = int(_lib.load().pc_lj_force_blocks(self.n_total))
+            d = torch.empty(5, dtype=torch.float64, device=self.device)
+            call("pc_reduce_partials", ptr(self.partial_k), nk, ptr(d), stream())
+            d[1] = self.diag[1]
+            self.diag.copy_(d)
+            return self.diag
         if self.mode == "tile":
             nb = self._nblk_tile * (2 if getattr(self, "_split", False) else 1)
         else:
@@ -705,15 +786,12 @@ class DomainEngine:
         call("pc_reduce_partials", ptr(self.partial), nb, ptr(self.diag), stream())
         return self.diag
 
-    def scatter_atom_rows(self, dst, n_global):
-        """Deterministic mode: this rank's per-atom (KE, PE, px, py, pz) rows
-        into dst (n_global + 1, 5) at their global ids (ghost rows -> the
-        dump row n_global)."""
-        n = self.n_total
-        gid = self.pos[:n, 3].contiguous().view(torch.int64)
-        tgt = torch.where(self.is_ghost[:n] != 0, torch.full_like(gid, n_global), gid)
-        tgt = tgt.to(torch.int32).contiguous()
-        call("pc_scatter_rows", ptr(self._atom), ptr(dst), ptr(tgt), n, 40, stream())
+    def exact_limbs(self, limbs):
+        """Deterministic mode: add this rank's owned per-atom (KE, PE, px, py,
+        pz) rows to the exact integer limbs (pc_exact_sum, ghost rows left
+        out) -- limbs of all ranks add up to the single-domain limbs."""
+        call("pc_exact_sum", ptr(self._atom), self.n_total, 5, ptr(self.is_ghost), ptr(limbs),
+             stream())
 
     def mean_neighbors(self) -> float:
         """Mean Verlet-list length over owned rows (ghost rows are empty)."""
@@ -801,13 +879,20 @@ class _StepLogic:
             return
         else:
             self._exchange("refresh_out", "refresh_in", 3)
-        for e in self._engines():
-            e.force(self._dtm)
+        self._forces(self._dtm)
+
+    def _forces(self, dtm):
+        engines = self._engines()
+        for e in engines:
+            e.force(dtm)
+        if engines and engines[0].half:
+            self._reverse()            # ghost forces -> owners (K12)
+            for e in engines:
+                e.kick(dtm)
 
     def _init_forces(self):
         self._rebuild_all()
-        for e in self._engines():
-            e.force(0.0)
+        self._forces(0.0)
 
 
 class FabricMD(_StepLogic):
@@ -816,7 +901,7 @@ class FabricMD(_StepLogic):
     kernels doing every data-sized step."""
 
     def __init__(self, cfg: MDConfig, device=None, tile: bool = True,
-                 deterministic: bool = False):
+                 deterministic: bool = False, half_list: bool = False):
         cfg.validate()
         self.deterministic = bool(deterministic)
         self.cfg = cfg
@@ -834,12 +919,14 @@ class FabricMD(_StepLogic):
         for r in range(self.fabric.n_ranks):
             if r == 0:
                 self.engines.append(DomainEngine(cfg, self.fabric, r, x, v, ids, dev, tile=tile,
-                                                 deterministic=deterministic))
+                                                 deterministic=deterministic,
+                                                 half_list=half_list))
             else:
                 z = torch.zeros((0, 3), dtype=torch.float64)
                 self.engines.append(DomainEngine(cfg, self.fabric, r, z, z,
                                                  torch.zeros(0, dtype=torch.int64), dev,
-                                                 tile=tile, deterministic=deterministic))
+                                                 tile=tile, deterministic=deterministic,
+                                                 half_list=half_list))
         self._init_forces()
 
     def _engines(self):
@@ -849,6 +936,11 @@ class FabricMD(_StepLogic):
         outs = [getattr(e, out_name)() for e in self.engines]
         for e, inbox in zip(self.engines, _route(outs)):
             getattr(e, in_name)(inbox)
+
+    def _reverse(self):
+        outs = [e.reverse_out() for e in self.engines]          # {src: ghost forces}
+        for e, inbox in zip(self.engines, _route(outs)):
+            e.reverse_in(inbox)
 
     def _refresh_overlapped(self):
         outs = [e.refresh_out() for e in self.engines]          # packs
@@ -860,13 +952,14 @@ class FabricMD(_StepLogic):
             e.force(self._dtm, part="boundary")
 
     def diagnostics(self):
-        if self.deterministic:          # per-atom rows in global-id order, one tree
-            g = torch.zeros((self.n + 1, 5), dtype=torch.float64, device=self.engines[0].device)
+        if self.deterministic:          # exact per-atom sums, order-independent
+            dev = self.engines[0].device
+            limbs = torch.zeros(20, dtype=torch.int64, device=dev)
             for e in self.engines:
                 if e.n_total:
-                    e.scatter_atom_rows(g, self.n)
-            d = torch.zeros(5, dtype=torch.float64, device=g.device)
-            call("pc_reduce_partials", ptr(g), self.n, ptr(d), stream())
+                    e.exact_limbs(limbs)
+            d = torch.zeros(5, dtype=torch.float64, device=dev)
+            call("pc_exact_finish", ptr(limbs), 5, ptr(d), stream())
             return _diag_dict(d.cpu().numpy(), self.n)
         tot = sum(e.local_diagnostics().cpu().numpy() for e in self.engines)
         ke, pe = float(tot[0]), float(tot[1])
@@ -983,7 +1076,7 @@ class DistMD(_StepLogic):
 
     def __init__(self, cfg: MDConfig, cells=None, transport=None, device=None,
                  local_init: bool = False, time_phases: bool = False,
-                 deterministic: bool = False):
+                 deterministic: bool = False, half_list: bool = False):
         import torch.distributed as dist
         cfg.validate()
         self.cfg = cfg
@@ -1005,7 +1098,8 @@ class DistMD(_StepLogic):
         x, v, ids = self._initial(cells, a, rank, local_init)
         self.deterministic = bool(deterministic)
         self.engine = DomainEngine(cfg, self.fabric, rank, x, v, ids, self.device,
-                                   time_phases=time_phases, deterministic=deterministic)
+                                   time_phases=time_phases, deterministic=deterministic,
+                                   half_list=half_list)
         self._init_forces()
         del dist
 
@@ -1042,6 +1136,13 @@ class DistMD(_StepLogic):
     def _engines(self):
         return [self.engine]
 
+    def _reverse(self):
+        """Ghost forces back to their owners: one all-to-all, the transpose of
+        the per-step refresh (split sizes swapped)."""
+        e = self.engine
+        buf = e.reverse_pack()
+        e.reverse_add(self.transport.alltoall(buf, e.recv_split, e.send_split, self.device))
+
     def _refresh_overlapped(self):
         """Pack, start the all-to-all (NCCL stream), interior force on the
         compute stream meanwhile, then wait, unpack, boundary force."""
@@ -1068,14 +1169,14 @@ class DistMD(_StepLogic):
 
     def diagnostics(self):
         if self.deterministic:
-            # every rank scatters its owned rows into the global id-ordered
-            # array; the sum over ranks is exact (one nonzero per entry)
-            g = torch.zeros((self.n + 1, 5), dtype=torch.float64, device=self.device)
+            # exact integer limbs per rank, summed over ranks (20 int64): the
+            # energies equal the single-domain ones bit for bit
+            limbs = torch.zeros(20, dtype=torch.int64, device=self.device)
             if self.engine.n_total:
-                self.engine.scatter_atom_rows(g, self.n)
-            self.transport.allreduce(g)
+                self.engine.exact_limbs(limbs)
+            self.transport.allreduce(limbs)
             d = torch.zeros(5, dtype=torch.float64, device=self.device)
-            call("pc_reduce_partials", ptr(g), self.n, ptr(d), stream())
+            call("pc_exact_finish", ptr(limbs), 5, ptr(d), stream())
             return _diag_dict(d.cpu().numpy(), self.n)
         d = self.engine.local_diagnostics().clone()
         self.transport.allreduce(d)

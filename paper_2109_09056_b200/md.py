@@ -431,7 +431,6 @@ class MDDriver:
                  self.ell_width, ptr(self.build_flag), s)
             if int(self.build_flag[0].item()) & _lib.FLAG_OVERFLOW:
                 raise RuntimeError("deterministic mode: a Verlet row exceeds 256 entries")
-            self._gid32 = self.pos[:n, 3].contiguous().view(torch.int64).to(torch.int32)
 
     def _tile_build(self, cell_start) -> bool:
         """Issue the tile round-list build (pc_tile.cu) without a host sync.
@@ -527,7 +526,6 @@ class MDDriver:
         elif self.deterministic:
             if getattr(self, "_atom", None) is None:
                 self._atom = torch.zeros((self.n, 5), dtype=torch.float64, device=self.device)
-                self._atom_g = torch.zeros_like(self._atom)
             call("pc_lj_force_sell_atoms", ptr(self.pos), ptr(self.pl), self._ps, self.n,
                  ptr(self.cnt), ptr(self.nbr), self.ell_width, self._pbox, self._lj,
                  self._mi_guard, ptr(self.frc), self.cap, ptr(self.vel), self.cap,
@@ -587,11 +585,12 @@ class MDDriver:
         if self.deterministic:
             if not self._ke_fresh:   # per-atom rows again (v unchanged: zero kick)
                 self._force(0.0)
-            # per-atom rows in global-id order, one fixed reduction tree
-            call("pc_scatter_rows", ptr(self._atom), ptr(self._atom_g), ptr(self._gid32),
-                 self.n, 40, stream())
+            # per-atom rows summed exactly (integer limbs, pc_exact_sum): the
+            # result does not depend on the order or the decomposition
+            limbs = torch.zeros(20, dtype=torch.int64, device=self.device)
+            call("pc_exact_sum", ptr(self._atom), self.n, 5, None, ptr(limbs), stream())
             d = self.diag if out is None else out
-            call("pc_reduce_partials", ptr(self._atom_g), self.n, ptr(d), stream())
+            call("pc_exact_finish", ptr(limbs), 5, ptr(d), stream())
             return d
         if not self._ke_fresh:       # velocities changed outside a force pass
             call("pc_kick", ptr(self.vel), self.cap, ptr(self.frc), self.cap, self.n, 0.0,

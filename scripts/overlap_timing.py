@@ -24,27 +24,23 @@ for e in fab.engines:
     print(f"rank {e.rank}: owned {e.n_owned} ghosts {e.n_total - e.n_owned} tiles {nt} "
           f"interior {ni} ({ni / nt:.2f})")
 s = 0
+R = cfg.rebuild_stride
 for overlap in (False, True, False, True):
     fab.overlap = overlap
-    for _ in range(5):
+    # advance to just after a rebuild, then time R - 1 refresh steps (the
+    # split applies to them; rebuild steps run the force in one pass)
+    while True:
         s += 1
         fab.step(s)
+        if s % R == 0:
+            break
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # steps between rebuilds only (the split applies to refresh steps)
-    while (s + 1) % cfg.rebuild_stride == 0:
-        s += 1
-        fab.step(s)
-    k = 0
     a.record()
-    while k < 15:
+    for _ in range(R - 1):
         s += 1
-        if s % cfg.rebuild_stride == 0:
-            fab.step(s)
-            continue
         fab.step(s)
-        k += 1
     b.record()
     b.synchronize()
-    print(f"overlap={overlap}: {a.elapsed_time(b) / 15:.3f} ms per step (8 ranks in sequence, "
-          f"incl. any rebuild in the window)")
+    print(f"overlap={overlap}: {a.elapsed_time(b) / (R - 1):.3f} ms per refresh step "
+          f"({len(fab.engines)} ranks in sequence on one GPU)")

@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None):
+def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None, half=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -35,7 +35,7 @@ def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None):
         torch.cuda.set_device(0)
         import paper_2109_09056_b200 as pc
         from paper_2109_09056_b200.dist import DistMD
-        drv = DistMD(pc.md.MDConfig(**(kw or KW)), deterministic=det)
+        drv = DistMD(pc.md.MDConfig(**(kw or KW)), deterministic=det, half_list=half)
         if overlap is not None:
             drv.overlap = overlap
         es = [drv.diagnostics()["E_total"]]
@@ -162,3 +162,30 @@ def test_distmd_overlap_split_bitwise(world):
         assert np.array_equal(a[2], b[2])
         assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
         assert np.max(np.abs(a[1] - b[1]) / np.abs(a[1])) < 1e-12
+
+
+def test_distmd_half_list_two_processes():
+    """Two processes, half list + reverse halo over the transport (the
+    transpose of the refresh all-to-all): the energy series matches the
+    single-domain half-list engine within 1e-9."""
+    import paper_2109_09056_b200 as pc
+    steps = 15
+    drv = pc.md.MDDriver(pc.md.MDConfig(**KW), half_list=True, tile=False)
+    ref = [drv.diagnostics()["E_total"]]
+    for s in range(1, steps + 1):
+        drv.step(s)
+        ref.append(drv.diagnostics()["E_total"])
+    ref = np.array(ref)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, steps, False, None, None, True))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for _, es, _ in out:
+        assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-9
