@@ -155,8 +155,8 @@ reduce_partials_kernel(const double* __restrict__ partial, int nblocks, double* 
 
 // ---- exact, order-independent sums (deterministic mode) --------------------
 // Each FP64 value v (|v| < 2^50) is split exactly into an integer part and
-// three 30-bit fraction limbs: v = i + (f1 2^60 + f2 2^30 + f3) 2^-90 - r,
-// 0 <= r < 2^-90 (the bits below 2^-90 are truncated).  Limb sums are
+// three 30-bit fraction limbs: |v| = i + (f1 2^60 + f2 2^30 + f3) 2^-90 - r,
+// 0 <= r < 2^-90 (the bits below 2^-90 are truncated), limbs signed as v.  Limb sums are
 // integer additions, so any partition of the atoms over threads, blocks,
 // ranks or devices gives the same limb totals: the energies of a
 // decomposed run equal the single-domain ones bit for bit (ref md.py:7-11,
@@ -166,17 +166,22 @@ constexpr int kExactLimbs = 4;
 constexpr int kExactMaxW = 8;
 
 __device__ __forceinline__ void exact_split(double v, long long* l) {
-  const double hi = floor(v);
-  double f = (v - hi) * 1073741824.0;            // exact: v - floor(v), * 2^30
+  // split |v| (a - floor(a) is exact for a >= 0; for a small negative v,
+  // v - floor(v) = v + 1 would round) and give the limbs v's sign: limbs may
+  // be negative, exact_finish_kernel's floor-division carries normalise them
+  const double a = fabs(v);
+  const double hi = floor(a);
+  double f = (a - hi) * 1073741824.0;            // exact: a - floor(a), * 2^30
   const double f1 = floor(f);
   f = (f - f1) * 1073741824.0;
   const double f2 = floor(f);
   f = (f - f2) * 1073741824.0;
   const double f3 = floor(f);
-  l[0] = (long long)hi;
-  l[1] = (long long)f1;
-  l[2] = (long long)f2;
-  l[3] = (long long)f3;
+  const long long s = v < 0.0 ? -1 : 1;
+  l[0] = s * (long long)hi;
+  l[1] = s * (long long)f1;
+  l[2] = s * (long long)f2;
+  l[3] = s * (long long)f3;
 }
 
 __global__ void exact_sum_kernel(const double* __restrict__ rows, int64_t n, int w,

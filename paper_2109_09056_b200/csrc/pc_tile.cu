@@ -62,7 +62,7 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #define PC_FORCE_VIRIAL 1       // rows sum u = 2 sr12 - sr6 and sr6: energy + pair virial
 #endif
 #ifndef PC_FORCE_NEXT
-#define PC_FORCE_NEXT 1         // claim items one ahead: next row's index loaded, its data L2-prefetched
+#define PC_FORCE_NEXT 0         // 1: claim items one ahead (next row index loaded, its data L2-prefetched): spills 24 B, C3 force 1252 vs 1138 us (profiles/r02d), off
 #endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
