@@ -17,7 +17,9 @@ bin_count_kernel(const double* __restrict__ x, int64_t n, int x_stride, int64_t 
     const double* p = x + i * x_stride;
     int c[3] = {0, 0, 0};
     bool outside = false;
-    for (int a = 0; a < g.ndim; ++a) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {     // unrolled: no local copy of g (was a 112-B stack frame)
+      if (a >= g.ndim) break;
       double v = p[a * a_stride];
       outside |= (v < g.low[a]) || (v > g.high[a]);
       c[a] = cell_coord(v, g.low[a], g.width[a], g.nc[a]);

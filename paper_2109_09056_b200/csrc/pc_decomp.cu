@@ -32,7 +32,9 @@ __global__ void owner_kernel(const double* __restrict__ x, int64_t n, int d, pc_
   if (i >= n) return;
   int c[3] = {0, 0, 0};
   bool outside = false;
-  for (int a = 0; a < d; ++a) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {       // unrolled: no local copy of g
+    if (a >= d) break;
     const double v = x[i * d + a];
     outside |= (v < g.low[a]) || (v > g.high[a]);
     double q = floor(__ddiv_rn(__dsub_rn(v, g.low[a]), g.width[a]));
@@ -51,7 +53,9 @@ __global__ void nonperiodic_check_kernel(const double* __restrict__ x, int64_t n
                                          pc_box b, int* __restrict__ flag) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  for (int a = 0; a < d; ++a) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a >= d) break;
     if (b.periodic[a]) continue;
     const double v = x[i * d + a];
     if (v < b.low[a] || v > b.high[a]) atomicOr(flag, kFlagNonPeriodic);
@@ -62,7 +66,11 @@ __global__ void nonperiodic_check_kernel(const double* __restrict__ x, int64_t n
 // for d = 3 (ref decomp.py:115-120).
 __device__ __forceinline__ double dist2_box(const double* x, const HaloOffset& o, int d) {
   double t[3] = {0.0, 0.0, 0.0};
-  for (int a = 0; a < d; ++a) {
+  // unrolled over the 3 axes (a runtime bound put t[] in local memory: a
+  // 48-B stack frame per thread in the halo selection kernels)
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a >= d) break;
     const double p = __dadd_rn(x[a], o.shift[a]);
     const double below = fmax(__dsub_rn(o.lo[a], p), 0.0);
     const double above = fmax(__dsub_rn(p, o.hi[a]), 0.0);

@@ -52,7 +52,7 @@ constexpr int kSCols = kSX * kSY;
 constexpr int kSegs = kSCols * 3;
 constexpr int kNDummy = 16;
 #ifndef PC_FORCE_SLEEP
-#define PC_FORCE_SLEEP 64
+#define PC_FORCE_SLEEP 256      // tile-wait poll interval (ns): 64 -> 256 frees ~0.5 % at C3 (profiles/r02g)
 #endif
 #ifndef PC_FORCE_WARPS
 #define PC_FORCE_WARPS 32
@@ -63,6 +63,9 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #endif
 #ifndef PC_FORCE_NEXT
 #define PC_FORCE_NEXT 0         // 1: claim items one ahead (next row index loaded, its data L2-prefetched): spills 24 B, C3 force 1252 vs 1138 us (profiles/r02d), off
+#endif
+#ifndef PC_FORCE_AHEAD
+#define PC_FORCE_AHEAD 0        // 1: L2 prefetch of the list head / row indices of item i + kForceWarps (2: two list groups); C3 force 1157 / 1154 vs 1134 us without (profiles/r02f), off
 #endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
@@ -1146,6 +1149,26 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     const int rw = locate(i, k);
     const int a = rowidx[(int64_t)rw * 32 + lane];
 #endif
+#if PC_FORCE_AHEAD
+    // the item this warp will most likely take next is ~one item per warp
+    // later (items are claimed in order by kForceWarps warps): its list
+    // head, row indices and round count into L2 now, a full row-warp time
+    // ahead (the first list group of a row-warp otherwise waits on HBM)
+    {
+      const int ia = i + kForceWarps;
+      if (ia < items) {
+        int ka;
+        const int rwa = locate(ia, ka);
+        const uint4* lpa = list + (int64_t)rwa * p.Q8 * 32 + lane;
+        prefetch_l2(lpa);
+        if (PC_FORCE_AHEAD > 1) prefetch_l2(lpa + 32);
+        if (lane == 0) {
+          prefetch_l2(rowidx + (int64_t)rwa * 32);
+          prefetch_l2(rounds + rwa);
+        }
+      }
+    }
+#endif
     // prefetch everything that does not depend on the staged tile
     const int R = rounds[rw];
     const uint4* lp = list + (int64_t)rw * p.Q8 * 32 + lane;
@@ -1311,6 +1334,9 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
 // prefer 16 distinct residues in every round: 1.6 LDS.64 passes per
 // half-warp instead of 2.5 (simulated), force pass -14 % (measured).
 constexpr int kOrdWarps = 8;
+#ifndef PC_ORDER_PREFETCH
+#define PC_ORDER_PREFETCH 1
+#endif
 constexpr int kOrdSmem = kOrdWarps * ((kHitCap + 1) * 32 * 2 + 16 * 32 * 4);
 
 // RR = false: class-major with the start rotated to the lane's residue (the
@@ -1335,8 +1361,12 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
 #pragma unroll
   for (int c = 0; c < 16; ++c) st[c * 32] = 0u;
   int cnt = 0;                                          // real entries precede padding
+  // list groups are loaded one ahead in both passes (the first use of each
+  // group stalled on its load: ~26 % of the kernel's stall samples, r02c)
+  uint4 qn = lp[0];
   for (int g = 0; g < G; ++g) {                         // per-class counts
-    const uint4 q = lp[g * 32];
+    const uint4 q = PC_ORDER_PREFETCH ? qn : lp[g * 32];
+    if (PC_ORDER_PREFETCH && g + 1 < G) qn = lp[(g + 1) * 32];
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -1360,8 +1390,10 @@ tile_order_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
     run += n;
   }
   unsigned ne = 0u;
+  qn = lp[0];
   for (int g = 0; g < G; ++g) {                         // class-major scatter -> smem
-    const uint4 q = lp[g * 32];
+    const uint4 q = PC_ORDER_PREFETCH ? qn : lp[g * 32];
+    if (PC_ORDER_PREFETCH && g + 1 < G) qn = lp[(g + 1) * 32];
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
