@@ -366,6 +366,8 @@ def run_ours(args):
         e2e = run_e2e(pc, kw, args.e2e_steps or max(K, 200),
                       dict(tile=args.path == "tile", half_list=args.list == "half",
                            planar_gather=args.gather == "planar"))
+    elif not args.no_e2e:
+        e2e = run_e2e_dist(pc, kw, args.e2e_steps or max(K, 100), gc, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -432,6 +434,50 @@ def run_e2e(pc, kw, steps, driver_options=None):
             "steps": steps, "includes": "H2D of x, v + engine setup (sort, list build, first "
                                         "force) + the steps + run_md's per-step diagnostics "
                                         "rows (D2H at the end)"}
+
+
+def run_e2e_dist(pc, kw, steps, cells, world):
+    """The N-GPU end-to-end leg through the public multi-GPU API: every rank
+    uploads its own block of the lattice from pinned host memory
+    (DistMD(state=...)) inside the timed region, runs the steps keeping each
+    step's (KE, PE, px, py, pz) partial row on the device, and the per-step
+    rows are summed over ranks and read back to the host at the end (40 B of
+    diagnostics per step, as run_md).  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2109_09056_b200.dist import DistMD, local_block, rank_dims_for
+    rank = dist.get_rank()
+    cfg = pc.md.MDConfig(**kw, steps=steps)
+    cfg.rank_dims = rank_dims_for(world)
+    x, v, ids = (torch.as_tensor(t).pin_memory()
+                 for t in local_block(cfg, cells, cfg.rank_dims, rank))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    hist = torch.zeros((steps + 1, 5), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    drv = DistMD(cfg, cells=cells, state=(x, v, ids))
+    hist[0] = drv.engine.local_diagnostics()
+    for s in range(1, steps + 1):
+        drv.step(s)
+        hist[s] = drv.engine.local_diagnostics()
+    dist.all_reduce(hist)
+    rows = hist.cpu()
+    e1.record()
+    e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    assert rows.shape[0] == steps + 1 and bool(torch.isfinite(rows).all())
+    n = int(drv.n)
+    h2d = int(x.numel() * 8 + v.numel() * 8 + ids.numel() * 8)
+    del drv
+    return {"value": n * steps / (float(ms.item()) * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": 40, "steps": steps,
+            "includes": "per rank: H2D of its block's x, v, ids (pinned) + DistMD setup "
+                        "(migrate, halo, sort, list build, first force) + the steps, each "
+                        "step's energy row kept on the device; rows summed over ranks and "
+                        "read back at the end; h2d bytes are rank 0's; max over ranks"}
 
 
 def main():

@@ -1071,12 +1071,37 @@ class NCCLTransport:
         return t
 
 
+def local_block(cfg: MDConfig, cells, rank_dims, rank: int):
+    """This rank's block of the fcc lattice (ids = the global lattice order)
+    with per-rank seeded velocities, as numpy (x, v, ids): the input of a run
+    too large for one global velocity stream (DistMD(local_init=True), or
+    `state=` from the host)."""
+    cells = np.asarray(cells, np.int64)
+    dims = np.asarray(rank_dims, np.int64)
+    a = (4.0 / cfg.density) ** (1.0 / 3.0)
+    c = np.array(np.unravel_index(rank, tuple(dims)), np.int64)
+    per = cells // dims
+    lo = c * per
+    hi = np.where(c == dims - 1, cells, lo + per)
+    gx, gy, gz = np.meshgrid(*[np.arange(lo[k], hi[k]) for k in range(3)], indexing="ij")
+    corner = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+    basis = np.array([[0, 0, 0], [0.5, 0.5, 0], [0.5, 0, 0.5], [0, 0.5, 0.5]])
+    x = (corner[:, None, :] + basis[None]).reshape(-1, 3) * a
+    flat = (corner[:, 0] * cells[1] + corner[:, 1]) * cells[2] + corner[:, 2]
+    ids = (flat[:, None] * 4 + np.arange(4)[None]).reshape(-1).astype(np.int64)
+    v = initial_velocities(x.shape[0], cfg.temperature, cfg.mass, cfg.seed * 1000003 + rank)
+    return x, v, ids
+
+
 class DistMD(_StepLogic):
     """One rank per GPU under torch.distributed (launch with torchrun)."""
 
     def __init__(self, cfg: MDConfig, cells=None, transport=None, device=None,
                  local_init: bool = False, time_phases: bool = False,
-                 deterministic: bool = False, half_list: bool = False):
+                 deterministic: bool = False, half_list: bool = False, state=None):
+        """`state`: this rank's own atoms as host (ideally pinned) tensors
+        (x, v, ids) -- e.g. `local_block(...)` -- instead of building them
+        here; rows owned by another rank move there at the first migrate."""
         import torch.distributed as dist
         cfg.validate()
         self.cfg = cfg
@@ -1095,7 +1120,10 @@ class DistMD(_StepLogic):
         self.n = int(4 * np.prod(cells))
         self._dtm = 0.5 * cfg.dt / cfg.mass
         self.device = torch.device(device) if device is not None else _lib.device()
-        x, v, ids = self._initial(cells, a, rank, local_init)
+        if state is not None:
+            x, v, ids = (t if isinstance(t, torch.Tensor) else torch.as_tensor(t) for t in state)
+        else:
+            x, v, ids = self._initial(cells, a, rank, local_init)
         self.deterministic = bool(deterministic)
         self.engine = DomainEngine(cfg, self.fabric, rank, x, v, ids, self.device,
                                    time_phases=time_phases, deterministic=deterministic,
@@ -1118,20 +1146,8 @@ class DistMD(_StepLogic):
             keep = owner == rank
             return (torch.as_tensor(x[keep]), torch.as_tensor(v[keep]),
                     torch.as_tensor(ids[keep]))
-        dims = self.fabric.rank_dims
-        c = self.fabric.coords_of(rank)
-        per = cells // dims
-        lo = c * per
-        hi = np.where(c == dims - 1, cells, lo + per)
-        gx, gy, gz = np.meshgrid(*[np.arange(lo[k], hi[k]) for k in range(3)], indexing="ij")
-        corner = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
-        basis = np.array([[0, 0, 0], [0.5, 0.5, 0], [0.5, 0, 0.5], [0, 0.5, 0.5]])
-        x = (corner[:, None, :] + basis[None]).reshape(-1, 3) * a
-        flat = (corner[:, 0] * cells[1] + corner[:, 1]) * cells[2] + corner[:, 2]
-        ids = (flat[:, None] * 4 + np.arange(4)[None]).reshape(-1).astype(np.int64)
-        v = initial_velocities(x.shape[0], cfg.temperature, cfg.mass,
-                               cfg.seed * 1000003 + rank)
-        return torch.as_tensor(x), torch.as_tensor(v), torch.as_tensor(ids)
+        return tuple(torch.as_tensor(t) for t in
+                     local_block(cfg, cells, self.fabric.rank_dims, rank))
 
     def _engines(self):
         return [self.engine]

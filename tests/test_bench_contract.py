@@ -78,6 +78,9 @@ def test_two_rank_line(scaling):
     assert 0.4 * n < c["rank0_owned_atoms"] < 0.6 * n
     assert c["parallelism"] == "domain x2"
     assert abs(d["value"] - n * 10 / (d["ms_per_step"] * 10e-3)) < 1e-6 * d["value"]
+    # end-to-end leg through DistMD(state=host block) at N ranks
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 40
 
 
 def test_reference_arm_under_torchrun():

@@ -84,6 +84,10 @@ def test_layout_bench_and_fabric(tmp_path):
     assert lines[1] == "vector_length,phase,seconds,checksum"
     sums = {ln.split(",")[3] for ln in lines[2:]}
     assert len(sums) == 1
+    # the V-dependent part: an AoSoA <-> SoA round trip of all fields per step
+    rt = {ln.split(",")[0]: float(ln.split(",")[2]) for ln in lines[2:]
+          if ln.split(",")[1] == "store_roundtrip"}
+    assert set(rt) == {"1", "16"} and all(t > 0 for t in rt.values())
     q = tmp_path / "fab.csv"
     assert cli.main(["md", "--steps", "5", "--lattice-cells", "4", "--density", "1.1",
                      "--cutoff", "2.3", "--ranks", "2,2,2", "--output", str(q)]) == 0

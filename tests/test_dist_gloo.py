@@ -101,3 +101,29 @@ def test_rank_dims_for():
     assert rank_dims_for(4) == (2, 2, 1)
     assert rank_dims_for(8) == (2, 2, 2)
     assert int(np.prod(rank_dims_for(6))) == 6
+
+
+@pytest.mark.parametrize("dims", [(2, 1, 1), (2, 2, 1), (2, 2, 2)])
+def test_local_blocks_tile_the_lattice(dims):
+    """dist.local_block (the per-rank host input of DistMD(local_init=True) and
+    of the bench's N-GPU end-to-end leg): the blocks of all ranks are the
+    reference's fcc lattice (md.py:67-74) split by owner, ids = lattice order."""
+    from paper_2109_09056_b200.dist import local_block
+    from paper_2109_09056_b200.md import MDConfig, fcc_lattice
+    cfg = MDConfig(lattice_cells=6, temperature=1.44, skin=0.3, rebuild_stride=5)
+    cells = np.array([6, 6, 6])
+    a = (4.0 / cfg.density) ** (1.0 / 3.0)
+    ref = fcc_lattice(6, a)
+    bl = cells * a / np.array(dims)
+    seen = np.zeros(ref.shape[0], bool)
+    for r in range(int(np.prod(dims))):
+        x, v, ids = local_block(cfg, cells, dims, r)
+        assert x.shape == v.shape == (ids.size, 3)
+        assert np.array_equal(x, ref[ids])
+        # owner by the reference formula (decomp.py:58-66), host-side
+        c = np.minimum(np.floor(x / bl).astype(np.int64), np.array(dims) - 1)
+        assert np.all(np.ravel_multi_index(tuple(c.T), dims) == r)
+        assert not seen[ids].any()
+        seen[ids] = True
+        assert np.abs(v.mean(axis=0)).max() < 1e-12
+    assert seen.all()
