@@ -288,6 +288,12 @@ int32_t pc_tile_plan_ints(void);
 int32_t pc_tile_stage_cap(void);
 int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw,
                  void* stream);
+/* As pc_tile_rows for a decomposed domain (ref decomp.py:143-260: owned rows
+ * + ghost rows in one local array): d_skip[i] != 0 marks ghost i; only the
+ * owned home particles are rows (pc_tile_build_domain numbers them the same
+ * way), so no row-warp runs ghost lanes. */
+int pc_tile_rows_domain(const int32_t* d_cell_start, const pc_grid* grid, const int32_t* d_skip,
+                        int32_t* d_rw, void* stream);
 /* Verlet build at cutoff2 (the reference's FP64 predicate behind an FP32
  * band prefilter) + round scheduling.  d_flag (3 int32, zeroed by the
  * caller): [0] bit 1 = a row-warp needs more than 8*q8 rounds ([2] = the
@@ -302,8 +308,10 @@ int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* 
  * md.py:176-188): cells, tiles and the FP32 prefilter use d_bplanar (ghosts
  * shifted by their periodic image into the local frame; grid/box = the local
  * grid and box), the exact FP64 predicate uses the raw positions d_planar and
- * the global box_exact (the reference's ghost convention), and rows i with
- * d_skip[i] != 0 (ghosts) get empty lists.  NULL d_bplanar / box_exact /
+ * the global box_exact (the reference's ghost convention), and particles i
+ * with d_skip[i] != 0 (ghosts) are never rows (no list, no force entry; the
+ * rows of a tile are its owned home particles, d_rw0 from
+ * pc_tile_rows_domain with the same d_skip).  NULL d_bplanar / box_exact /
  * d_skip: pc_tile_build.  d_tile_ghost (nullable, one int per tile): 1 when
  * the tile's staged neighbourhood holds a ghost row (d_skip), else 0 -- the
  * interior / boundary split of pc_tile_force. */
@@ -468,6 +476,13 @@ int pc_lj_pair(const double* d_dx, const double* d_r2, int64_t n, double eps, do
  * outside the global box -> d_flag bit 0 (ref decomp.py:58-66). */
 int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
                 int32_t* d_owner, int32_t* d_flag, void* stream);
+/* pc_owner_of over a decomposed domain's owned + ghost rows (the migrate's
+ * first step, ref decomp.py:86-88 drops ghosts): rows with d_skip[i] != 0
+ * get owner skip_owner (an out-of-range key the partition drops) and are not
+ * checked -- their positions are not maintained between refreshes. */
+int pc_owner_of_domain(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
+                       const int32_t* d_skip, int32_t skip_owner, int32_t* d_owner,
+                       int32_t* d_flag, void* stream);
 /* Wrapped position outside the box on a non-periodic axis -> d_flag bit 3
  * (ref decomp.py:92-96). */
 int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* box,

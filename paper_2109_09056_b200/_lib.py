@@ -106,6 +106,8 @@ SIGNATURES = {
     "pc_pos_planar": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp]),
     "pc_owner_of": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_vp,
                                    c_vp]),
+    "pc_owner_of_domain": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcGrid), c_vp, c_i32,
+                                           c_vp, c_vp, c_vp]),
     "pc_check_nonperiodic": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcBox), c_vp,
                                             c_vp]),
     "pc_halo_plan": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
@@ -129,6 +131,7 @@ SIGNATURES = {
     "pc_cell_zsort": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pc_tile_stage_cap": (c_i32, []),
     "pc_tile_rows": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp]),
+    "pc_tile_rows_domain": (ctypes.c_int, [c_vp, ctypes.POINTER(PcGrid), c_vp, c_vp, c_vp]),
     "pc_tile_build": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
                                      ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp, c_vp,
                                      c_vp, c_vp, c_vp, c_vp]),

@@ -27,9 +27,14 @@ struct HaloTable {
 // owner = ravel(min(floor((x - low) / bl), dims - 1)); outside the global
 // box -> flag bit 0 (ValueError, ref decomp.py:62-63).
 __global__ void owner_kernel(const double* __restrict__ x, int64_t n, int d, pc_grid g,
-                             int* __restrict__ owner, int* __restrict__ flag) {
+                             int* __restrict__ owner, int* __restrict__ flag,
+                             const int* __restrict__ skip, int skip_owner) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (skip && skip[i]) {        // a ghost row: dropped by the migrate, no check
+    owner[i] = skip_owner;
+    return;
+  }
   int c[3] = {0, 0, 0};
   bool outside = false;
 #pragma unroll
@@ -342,9 +347,15 @@ extern "C" {
 
 int pc_owner_of(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
                 int32_t* d_owner, int32_t* d_flag, void* stream) {
+  return pc_owner_of_domain(d_x, n, d, fabric, nullptr, 0, d_owner, d_flag, stream);
+}
+
+int pc_owner_of_domain(const double* d_x, int64_t n, int32_t d, const pc_grid* fabric,
+                       const int32_t* d_skip, int32_t skip_owner, int32_t* d_owner,
+                       int32_t* d_flag, void* stream) {
   if (n <= 0) return PC_OK;
-  owner_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_x, n, d, *fabric,
-                                                                           d_owner, d_flag);
+  owner_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      d_x, n, d, *fabric, d_owner, d_flag, d_skip, skip_owner);
   return check_launch("pc_owner_of");
 }
 

@@ -226,10 +226,14 @@ __device__ __forceinline__ int home_row(const TileSetup& T, int u, int& c) {
   return T.home_start[c] + (u - T.home_pre[c]);
 }
 
-// per tile: row-warps = ceil(home rows / 32)
-__global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __restrict__ rw) {
+// per tile: row-warps = ceil(home rows / 32); with `skip` (a decomposed
+// domain's ghost flags) only the owned home rows are rows.  One warp per tile
+// (the owned count is a ballot sweep over the tile's ~300 home particles).
+__global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __restrict__ rw,
+                                 const int* __restrict__ skip) {
   const TileDims d = tile_dims(g);
-  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (tile >= d.ntiles) return;
   const int tz = tile % d.ntz, t2 = tile / d.ntz;
   const int ty = t2 % d.nty, tx = t2 / d.nty;
@@ -239,12 +243,18 @@ __global__ void tile_rows_kernel(const int* __restrict__ cs, pc_grid g, int* __r
   for (int hx = 0; hx < bx; ++hx)
     for (int hy = 0; hy < by; ++hy) {
       const int c0 = ((x0 + hx) * g.nc[1] + (y0 + hy)) * g.nc[2] + z0;
-      h += cs[c0 + bz] - cs[c0];
+      const int j0 = cs[c0], j1 = cs[c0 + bz];
+      if (skip) {
+        for (int j = j0; j < j1; j += 32)
+          h += __popc(__ballot_sync(0xffffffffu, j + lane < j1 && !skip[j + lane]));
+      } else {
+        h += j1 - j0;
+      }
     }
   // at least one row-warp per tile: a tile without home rows still gets an
   // (empty) item, so the force kernel's warp that takes it releases the
   // staging buffer the tile was loaded into (nothing else would)
-  rw[tile] = max(1, (h + 31) >> 5);
+  if (lane == 0) rw[tile] = max(1, (h + 31) >> 5);
 }
 
 // ---- TMA / mbarrier helpers ----------------------------------------------
@@ -581,6 +591,42 @@ __device__ __forceinline__ int slot_index(const TileSetup& T, int s) {
   return T.seg_src[e] + (s - T.seg_dst[e]);
 }
 
+// Decomposed domain (`skip` = ghost flags): the tile's rows are its OWNED
+// home particles only, numbered in (home column, z) order -- ghost rows carry
+// no list, and a row-warp mixing owned and ghost lanes would run its ghost
+// lanes idle in the build, the order pass and every force pass.  Lane L of
+// row-warp w gets the (32 w + L)-th owned home slot (-1: none) and its home
+// column; one ballot scan of the home slots per row-warp.
+__device__ __forceinline__ int owned_row_slot(const TileSetup& T, const int* __restrict__ skip,
+                                              int w, int lane, int& col) {
+  const int target = 32 * w + lane;
+  int base = 0, mine = -1;
+  col = 0;
+  for (int c = 0; c < kBX * kBY; ++c) {
+    const int hx = c / kBY, hy = c - hx * kBY;
+    if (hx >= T.bx || hy >= T.by) continue;
+    const int hcol = (hx + 1) * kSY + (hy + 1);
+    const int s0 = T.cell_lo[hcol][1], s1 = T.cell_hi[hcol][T.bz];
+    const int e = hcol * 3 + 1;                  // home cells: the in-range segment
+    const int off = T.seg_src[e] - T.seg_dst[e];
+    for (int s = s0; s < s1 && base < 32 * w + 32; s += 32) {
+      const int sl = s + lane;
+      const bool own = sl < s1 && !skip[off + sl];
+      const unsigned bal = __ballot_sync(0xffffffffu, own);
+      const int n = target - base;
+      const bool in = n >= 0 && n < __popc(bal);
+      const int src = in ? (int)__fns(bal, 0, n + 1) : 0;
+      const int got = __shfl_sync(0xffffffffu, sl, src);
+      if (in) {
+        mine = got;
+        col = c;
+      }
+      base += __popc(bal);
+    }
+  }
+  return mine;
+}
+
 // Build.  Particles are z-sorted inside every cell (pc_cell_zsort at the
 // rebuild), so each staged column -- cells in z order, each cell z-sorted --
 // is one z-sorted run of slots, and the home rows of a column are z-sorted
@@ -627,7 +673,8 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
     return;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nrw = max(1, (T.H + 31) >> 5);      // as tile_rows_kernel
+  // as tile_rows_kernel (owned home rows only when `skip` is given)
+  const int nrw = skip ? rw0[blockIdx.x + 1] - rw0[blockIdx.x] : max(1, (T.H + 31) >> 5);
   const int bz = T.bz;
   if (warp == 0) {                       // compacted plan of this tile
     int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
@@ -681,7 +728,9 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
   for (int w = warp; w < nrw; w += kBuildWarps) {
     const int u = w * 32 + lane;
-    const bool act = u < T.H;
+    int ocol = 0;
+    const int opos = skip ? owned_row_slot(T, skip, w, lane, ocol) : -1;
+    const bool act = skip ? opos >= 0 : u < T.H;
     int cnt = 0, a = -1, pos = -1, nband = 0;
     if (act) {
       // hit list: entry k of this lane's row at shared byte address hbase + 64 k
@@ -692,16 +741,16 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       int c = 0;
 #pragma unroll
       for (int q = 1; q < kBX * kBY; ++q) c += (u >= T.home_pre[q]) ? 1 : 0;
+      if (skip) c = ocol;
       const int hx = c / kBY, hy = c - hx * kBY;
       const int hcol = (hx + 1) * kSY + (hy + 1);
-      pos = T.cell_lo[hcol][1] + (u - T.home_pre[c]);
+      pos = skip ? opos : T.cell_lo[hcol][1] + (u - T.home_pre[c]);
       int k = 1;
       for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
       a = slot_index(T, pos);
       const float4 me = cz[pos];
-      // rows flagged in `skip` (ghosts of a decomposed domain) keep an empty
-      // list: zero force, and they are never a row of the force pass's pairs
-      const bool scan = !(skip && skip[a]);
+      // (with `skip`, ghosts of a decomposed domain are never rows)
+      const bool scan = true;
       // every stencil column is swept over the same z-window |dz| < h,
       // h = sqrt(hi2) (lateral pruning would only shorten some lanes'
       // windows; the warp runs the longest anyway)
@@ -1525,10 +1574,16 @@ int pc_cell_zsort(const double* d_z, int64_t z_stride, const int32_t* d_cell_sta
 }
 
 int pc_tile_rows(const int32_t* d_cell_start, const pc_grid* grid, int32_t* d_rw, void* stream) {
+  return pc_tile_rows_domain(d_cell_start, grid, nullptr, d_rw, stream);
+}
+
+int pc_tile_rows_domain(const int32_t* d_cell_start, const pc_grid* grid, const int32_t* d_skip,
+                        int32_t* d_rw, void* stream) {
   const int nt = tile_dims(*grid).ntiles;
   if (nt <= 0) return PC_OK;
-  tile_rows_kernel<<<(nt + 127) / 128, 128, 0, as_stream(stream)>>>(d_cell_start, *grid, d_rw);
-  return check_launch("pc_tile_rows");
+  tile_rows_kernel<<<(nt + 7) / 8, 256, 0, as_stream(stream)>>>(d_cell_start, *grid, d_rw,
+                                                                 d_skip);
+  return check_launch("pc_tile_rows_domain");
 }
 
 int pc_tile_build(const double* d_planar, int64_t planar_stride, const int32_t* d_cell_start,

@@ -290,12 +290,11 @@ class DomainEngine:
         owner = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         if n:
-            call("pc_owner_of", ptr(x), n, 3, self.fabric.pc_grid(), ptr(owner), ptr(flag),
-                 stream())
-            if self.n_total != self.n_owned:
-                owner[:n] = torch.where(self.is_ghost[:n] != 0,
-                                        torch.full_like(owner[:n], self.fabric.n_ranks),
-                                        owner[:n])
+            # ghost rows: key n_ranks, unchecked (the tile force pass does not
+            # advance them; the refresh or this rebuild replaces them)
+            call("pc_owner_of_domain", ptr(x), n, 3, self.fabric.pc_grid(),
+                 ptr(self.is_ghost) if self.n_total != self.n_owned else None,
+                 self.fabric.n_ranks, ptr(owner), ptr(flag), stream())
         # stable grouping by owner (decomp.py:97-99); the group starts and the
         # outside-box flag come back in one device->host read
         nr = self.fabric.n_ranks
@@ -572,7 +571,8 @@ class DomainEngine:
             call("pc_pos_planar", ptr(self.binpos), n, ptr(self.bpl), self._ps, s)
         nt = int(lib.pc_tile_count(g))
         rw = torch.empty(nt, dtype=torch.int32, device=dev)
-        call("pc_tile_rows", ptr(cell_start), g, ptr(rw), s)
+        # rows = owned home particles only (ghost rows carry no list)
+        call("pc_tile_rows_domain", ptr(cell_start), g, ptr(self.is_ghost), ptr(rw), s)
         self._rw0 = _kernels.scan_i32(rw)
         bound = n // 32 + nt + 1
         self._ntiles = nt
