@@ -118,16 +118,28 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def static_traffic():
-    """ncu DRAM read+write per launch per atom of the force kernel, from the
-    committed capture (an ncu replay cannot run inside the timed region)."""
+def _force_capture():
     p = os.path.join(ROOT, "profiles", "force_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return float(d["bytes_per_launch_per_atom"]), d.get("source", p)
+            return json.load(f), p
     except Exception:
+        return None, p
+
+
+def static_traffic():
+    """ncu DRAM read+write per launch per atom of the force kernel, from the
+    committed capture (an ncu replay cannot run inside the timed region)."""
+    d, p = _force_capture()
+    if d is None:
         return None, None
+    return float(d["bytes_per_launch_per_atom"]), d.get("source", p)
+
+
+def static_inst_per_atom():
+    """ncu warp instructions per atom of one force launch (same capture)."""
+    d, _ = _force_capture()
+    return None if d is None else d.get("warp_instructions_per_atom")
 
 
 class ClockSampler:
@@ -244,6 +256,11 @@ def _sum_ms(pairs):
     return float(sum(a.elapsed_time(b) for a, b in pairs))
 
 
+def _sm_count():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -338,6 +355,19 @@ def run_ours(args):
                 "force_launches": n_force, "per": "force pass per step (sum of its launches)",
                 "limiter": "not HBM: instruction issue and shared-memory wavefronts of the "
                            "exact FP64 pair test (ncu, profiles/, DESIGN.md §5)"}
+    # the force kernel is instruction-issue bound, not HBM bound: its issue
+    # roofline = warp instructions per launch (ncu count per atom x atoms)
+    # / live launch time, against 4 warp instructions per clock per SM
+    ipa = static_inst_per_atom()
+    if ipa is not None and mode == "tile":
+        sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+        peak_i = _sm_count() * 4 * sm_clk
+        ach_i = ipa * n_local / (force_ms * 1e-3)
+        roofline["issue"] = {"achieved_warp_inst_per_s": ach_i, "peak_warp_inst_per_s": peak_i,
+                             "frac": ach_i / peak_i,
+                             "source": "static: ncu smsp__inst_executed.sum per atom "
+                                       "(profiles/force_traffic.json) x atoms / live launch "
+                                       "time; peak = SMs x 4 schedulers x median SM clock"}
     per_gpu_rate = value / world
     b_step = step_bytes(kmean, args.rebuild)
     roofline_step = {"bound": "hbm", "achieved": per_gpu_rate * b_step / 1e9, "peak": peak,

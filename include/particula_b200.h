@@ -504,16 +504,21 @@ int pc_halo_force_add(double* d_f3, int64_t f_stride, const int32_t* d_rows, int
  * slot `slot` in chunk c (C = pc_halo_select_chunks(n)); after an exclusive
  * scan of d_hist (pc_scan_i32 -> d_off, slot s starts at d_off[s * C]),
  * pc_halo_select_place writes d_out_idx[k] (particle index) and the ghost
- * row d_out_rows[k] = (x, y, z, id bits, shift of the winning image). */
+ * row d_out_rows[k] = (x, y, z, id bits, shift of the winning image).
+ * h_in_lo / h_in_hi (nullable, 3 doubles each, d = 3): an interior box of
+ * the source block -- the block shrunk by the halo width and a relative
+ * margin -- whose particles are farther than the width from every other
+ * block and skip the image tests (same export set). */
 int64_t pc_halo_select_chunks(int64_t n);
 int pc_halo_select_count(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
                          const int32_t* h_slot, const double* h_shift, const double* h_lo,
                          const double* h_hi, int32_t n_slots, double w2, int32_t* d_hist,
-                         void* stream);
+                         void* stream, const double* h_in_lo, const double* h_in_hi);
 int pc_halo_select_place(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
                          const int32_t* h_slot, const double* h_shift, const double* h_lo,
                          const double* h_hi, int32_t n_slots, double w2, const int32_t* d_off,
-                         int32_t* d_out_idx, double* d_out_rows, void* stream);
+                         int32_t* d_out_idx, double* d_out_rows, void* stream,
+                         const double* h_in_lo, const double* h_in_hi);
 /* Halo export planning for one source rank (ref decomp.py:143-228): n_off
  * candidate images in product order (host arrays: destination slot, shift,
  * destination box lo/hi, each d wide); per particle and slot the best image

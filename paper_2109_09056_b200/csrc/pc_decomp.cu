@@ -20,7 +20,11 @@ struct HaloTable {
   int n_off;                       // offsets in product order (<= 26)
   int n_slots;                     // distinct destinations
   int d;                           // dimensionality
+  int has_in;                      // in_lo / in_hi valid
   double w2;
+  // interior box (selection only): a particle strictly inside it is farther
+  // than the halo width from every other block, so it exports nothing
+  double in_lo[3], in_hi[3];
   HaloOffset off[kMaxSlots];
 };
 
@@ -138,6 +142,9 @@ __device__ __forceinline__ int halo_best_offset(const double* xi, const HaloTabl
 __device__ __forceinline__ unsigned halo_select_mask(const double* xi, const HaloTable& t,
                                                      bool ident) {
   unsigned m = 0u;
+  if (t.has_in && xi[0] > t.in_lo[0] && xi[0] < t.in_hi[0] && xi[1] > t.in_lo[1] &&
+      xi[1] < t.in_hi[1] && xi[2] > t.in_lo[2] && xi[2] < t.in_hi[2])
+    return 0u;                     // deep inside the own block (most particles)
   if (ident) {
     for (int k = 0; k < t.n_off; ++k)
       if (dist2_box(xi, t.off[k], t.d) < t.w2) m |= 1u << k;
@@ -369,7 +376,8 @@ int pc_check_nonperiodic(const double* d_x, int64_t n, int32_t d, const pc_box* 
 
 static int make_halo_table(const char* who, int32_t d, int32_t n_off, const int32_t* h_slot,
                            const double* h_shift, const double* h_lo, const double* h_hi,
-                           int32_t n_slots, double w2, HaloTable& t) {
+                           int32_t n_slots, double w2, HaloTable& t,
+                           const double* h_in_lo = nullptr, const double* h_in_hi = nullptr) {
   if (n_off > kMaxSlots || n_slots > kMaxSlots || d < 1 || d > 3) {
     set_error("%s: too many offsets or bad dimension", who);
     return PC_ERR_VALUE;
@@ -378,6 +386,11 @@ static int make_halo_table(const char* who, int32_t d, int32_t n_off, const int3
   t.n_slots = n_slots;
   t.d = d;
   t.w2 = w2;
+  t.has_in = h_in_lo && h_in_hi && d == 3;
+  for (int a = 0; a < 3; ++a) {
+    t.in_lo[a] = t.has_in ? h_in_lo[a] : 0.0;
+    t.in_hi[a] = t.has_in ? h_in_hi[a] : 0.0;
+  }
   for (int k = 0; k < n_off; ++k) {
     t.off[k].slot = h_slot[k];
     for (int a = 0; a < 3; ++a) {
@@ -394,11 +407,11 @@ int64_t pc_halo_select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChun
 int pc_halo_select_count(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
                          const int32_t* h_slot, const double* h_shift, const double* h_lo,
                          const double* h_hi, int32_t n_slots, double w2, int32_t* d_hist,
-                         void* stream) {
+                         void* stream, const double* h_in_lo, const double* h_in_hi) {
   if (n <= 0) return PC_OK;
   HaloTable t;
   const int rc = make_halo_table("pc_halo_select_count", d, n_off, h_slot, h_shift, h_lo, h_hi,
-                                 n_slots, w2, t);
+                                 n_slots, w2, t, h_in_lo, h_in_hi);
   if (rc != PC_OK) return rc;
   const int64_t nch = pc_halo_select_chunks(n);
   halo_select_count_kernel<<<(unsigned)nch, kSelChunk, 0, as_stream(stream)>>>(d_pos4, n, t,
@@ -409,11 +422,12 @@ int pc_halo_select_count(const double* d_pos4, int64_t n, int32_t d, int32_t n_o
 int pc_halo_select_place(const double* d_pos4, int64_t n, int32_t d, int32_t n_off,
                          const int32_t* h_slot, const double* h_shift, const double* h_lo,
                          const double* h_hi, int32_t n_slots, double w2, const int32_t* d_off,
-                         int32_t* d_out_idx, double* d_out_rows, void* stream) {
+                         int32_t* d_out_idx, double* d_out_rows, void* stream,
+                         const double* h_in_lo, const double* h_in_hi) {
   if (n <= 0) return PC_OK;
   HaloTable t;
   const int rc = make_halo_table("pc_halo_select_place", d, n_off, h_slot, h_shift, h_lo, h_hi,
-                                 n_slots, w2, t);
+                                 n_slots, w2, t, h_in_lo, h_in_hi);
   if (rc != PC_OK) return rc;
   const int64_t nch = pc_halo_select_chunks(n);
   halo_select_place_kernel<<<(unsigned)nch, kSelChunk, 0, as_stream(stream)>>>(

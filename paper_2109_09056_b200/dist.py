@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes
 import itertools
+import os
 
 import numpy as np
 import torch
@@ -390,10 +391,17 @@ class DomainEngine:
         slot, shift = o["slot"].ctypes.data_as(vp), o["shift"].ctypes.data_as(vp)
         lo, hi = o["lo"].ctypes.data_as(vp), o["hi"].ctypes.data_as(vp)
         w2 = float(self.halo_width * self.halo_width)
+        # interior of the own block (shrunk by the width, with margin): its
+        # particles are farther than the width from every other block
+        lb = self.fabric.local_box(self.rank)
+        pad = self.halo_width * (1.0 + 1e-9) + 1e-9 * float(np.max(self.fabric.global_box.lengths))
+        self._in_lo = np.ascontiguousarray(lb.low + pad, dtype=np.float64)
+        self._in_hi = np.ascontiguousarray(lb.high - pad, dtype=np.float64)
+        in_lo, in_hi = self._in_lo.ctypes.data_as(vp), self._in_hi.ctypes.data_as(vp)
         nch = int(_lib.load().pc_halo_select_chunks(n))
         hist = torch.empty(ns * nch, dtype=torch.int32, device=self.device)
         call("pc_halo_select_count", ptr(self.pos), n, 3, len(o["slot"]), slot, shift, lo, hi,
-             ns, w2, ptr(hist), stream())
+             ns, w2, ptr(hist), stream(), in_lo, in_hi)
         pos = _kernels.scan_i32(hist)
         starts = pos[0: ns * nch + 1: nch].cpu().numpy()        # ns + 1 per-slot bounds
         total = int(starts[ns])
@@ -401,7 +409,7 @@ class DomainEngine:
             ix_all = torch.empty(total, dtype=torch.int32, device=self.device)
             buf_all = torch.empty((total, HALO_W), dtype=torch.float64, device=self.device)
             call("pc_halo_select_place", ptr(self.pos), n, 3, len(o["slot"]), slot, shift, lo,
-                 hi, ns, w2, ptr(pos), ptr(ix_all), ptr(buf_all), stream())
+                 hi, ns, w2, ptr(pos), ptr(ix_all), ptr(buf_all), stream(), in_lo, in_hi)
             k = 0
             while k < ns:                                       # contiguous per destination
                 dst, k1 = o["dests"][k], k
@@ -523,6 +531,14 @@ class DomainEngine:
             self.rebuilds += 1
             self._t1("neighbor", e0)
             return
+        self._sell_build(srt.cell_start)
+        self.rebuilds += 1
+        self._t1("neighbor", e0)
+
+    def _sell_build(self, cell_start):
+        """SELL Verlet build of all rows (ghost rows emptied); also the
+        fallback of a failed tile build (verify_build)."""
+        n, s = self.n_total, stream()
         self.mode = "half" if self.half else "sell"
         used = ctypes.c_int32(0)
         # half list: the per-particle kernel, whose half test compares global
@@ -532,12 +548,12 @@ class DomainEngine:
         while True:
             self.build_flag.zero_()
             if staged:
-                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                call("pc_nbr_build_sell", ptr(self.pos), n, ptr(cell_start), self._grid,
                      self._lbox, self._search2, self.ell_width, self.cap, ptr(self.cnt),
                      ptr(self.nbr), ptr(self.build_flag), ctypes.byref(used), s,
                      ptr(self.binpos), self._gbox, 0)
             else:
-                call("pc_nbr_build", ptr(self.pos), n, ptr(srt.cell_start), self._grid,
+                call("pc_nbr_build", ptr(self.pos), n, ptr(cell_start), self._grid,
                      self._lbox, self._search2, int(self.half), _lib.PC_NBR_SELL, 0,
                      ptr(self.cnt), None, ptr(self.nbr), self.cap, self.ell_width,
                      ptr(self.build_flag), s, ptr(self.binpos), self._gbox)
@@ -558,8 +574,6 @@ class DomainEngine:
             if int(self.build_flag[0].item()) & _lib.FLAG_OVERFLOW:
                 raise RuntimeError("deterministic mode: a Verlet row exceeds 256 entries")
         self.used_staged = bool(used.value)
-        self.rebuilds += 1
-        self._t1("neighbor", e0)
 
     def _tile_build(self, cell_start) -> bool:
         """Tile round lists of all rows (ghost rows empty, pc_tile_build_domain);
@@ -594,10 +608,12 @@ class DomainEngine:
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
              ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s, ptr(self.bpl),
              self._gbox, ptr(self.is_ghost), ptr(self._tghost))
-        fl = int(self.build_flag[0].item())
-        if fl & (_lib.FLAG_STAGE | _lib.FLAG_OVERFLOW):
-            self.tile_failures += 1
-            return False
+        # no host read of the build flags here: the step's force is launched
+        # speculatively on these lists and verify_build checks the flags after
+        # it (a failed build -- a neighbourhood beyond the staging area or a
+        # row beyond the list capacity -- redoes list and force on SELL)
+        self._spec = True
+        self._spec_cell_start = cell_start
         # interior tiles (no ghost staged) first, then boundary tiles, each in
         # ascending tile order; bounds stay on the device ([0, n_int, nt])
         self._tsplit, bounds = _kernels.stable_partition(self._tghost[:nt], 2)
@@ -716,6 +732,30 @@ class DomainEngine:
             b.record()
             ev.append((a, b))
         self._t1("force", e0)
+
+    def save_spec(self):
+        """Before the force on speculatively built tile lists: keep what that
+        force changes (velocities: fused kick; error flags)."""
+        if getattr(self, "_spec", False):
+            self._spec_vel = self.vel.clone()
+            self._spec_flag = self.flag.clone()
+
+    def verify_build(self, kick_dtm):
+        """After that force: read the tile build's flags (the rebuild's only
+        host read of them, with the force already queued); on a failed build
+        restore the saved state and redo the list and the force on SELL."""
+        if not getattr(self, "_spec", False):
+            return
+        self._spec = False
+        fl = int(self.build_flag[0].item())
+        if fl & (_lib.FLAG_STAGE | _lib.FLAG_OVERFLOW):
+            self.vel.copy_(self._spec_vel)
+            self.flag.copy_(self._spec_flag)
+            self._advanced = False
+            self.tile_failures += 1
+            self._sell_build(self._spec_cell_start)
+            self.force(kick_dtm)
+        self._spec_vel = self._spec_flag = None
 
     # ---- half list: reverse halo + kick (K12) ---------------------------------
     def reverse_out(self):
@@ -864,7 +904,15 @@ class _StepLogic:
         for e in self._engines():
             e.sort_and_build()
 
-    overlap = True      # split the force around the ghost refresh (tile path)
+    # Split the force around the ghost refresh (tile path): interior tiles'
+    # pass while the all-to-all is in flight, then the boundary tiles'.  Off
+    # by default (PC_OVERLAP=1 or `.overlap = True` turns it on): the split
+    # costs a second launch ramp and CTA tail (+35 us per 1M-atom rank per
+    # step, profiles/r02l/overlap_timing.txt), and NCCL's all-to-all runs as
+    # SM kernels, which cannot start beside the persistent force kernel that
+    # holds every SM's registers -- so the exchange does not actually run
+    # under the interior pass.
+    overlap = os.environ.get("PC_OVERLAP", "0") == "1"
 
     def step(self, step_index: int):
         for e in self._engines():
@@ -884,11 +932,14 @@ class _StepLogic:
     def _forces(self, dtm):
         engines = self._engines()
         for e in engines:
+            e.save_spec()
             e.force(dtm)
         if engines and engines[0].half:
             self._reverse()            # ghost forces -> owners (K12)
             for e in engines:
                 e.kick(dtm)
+        for e in engines:              # after a rebuild: tile build flags
+            e.verify_build(dtm)
 
     def _init_forces(self):
         self._rebuild_all()
