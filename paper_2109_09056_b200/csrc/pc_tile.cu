@@ -82,6 +82,8 @@ struct TileSetup {
   int seg_src[kSegs];          // even-aligned first index of the copied run
   int seg_len[kSegs];          // copied elements (even, 0 = empty)
   int seg_dst[kSegs];          // first slot
+  int seg_tf[kSegs];           // true particle range [tf, te) of the segment (build v2: pads)
+  int seg_te[kSegs];
   float seg_shift[kSegs][3];   // periodic image (build prefilter only; exact multiples of L in FP64 below)
   int cell_lo[kSCols][kSZ];    // slot range of each staged cell (build only)
   int cell_hi[kSCols][kSZ];
@@ -137,17 +139,21 @@ __device__ void tile_setup(int tile, const pc_grid& g, const pc_box& b,
     } else {
       if (zhi >= nz && b.periodic[2]) { za = zb = 0; shz = 1.f; }
     }
-    int src = 0, len = 0;
+    int src = 0, len = 0, tf = 0, te = 0;
     if (ok && zb >= za) {
       const int base = (gx * ny + gy) * nz;
       const int first = cs[base + za], end = cs[base + zb + 1];
       if (end > first) {
         src = first & ~1;
         len = ((end + 1) & ~1) - src;
+        tf = first;
+        te = end;
       }
     }
     T.seg_src[e] = src;
     T.seg_len[e] = len;
+    T.seg_tf[e] = tf;
+    T.seg_te[e] = te;
     T.seg_shift[e][0] = shx;
     T.seg_shift[e][1] = shy;
     T.seg_shift[e][2] = shz;
@@ -309,6 +315,36 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// ---- two pairs per call: the FP32 LJ magnitude as packed f32x2 ------------
+// sm_100 issues FADD2/FMUL2/FFMA2 (two FP32 lanes per thread, one issue
+// slot): the seven FP32 instructions of a pair's LJ magnitude become 3.5 per
+// pair.  Same per-element rounding as the scalar form (fma.rn / mul.rn on
+// each half); the row's u and sr6 sums are kept as two partial sums.
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pk2(float a, float b) {
+  f32x2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2_t mul2(f32x2_t a, f32x2_t b) {
+  f32x2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2_t add2(f32x2_t a, f32x2_t b) {
+  f32x2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2_t fma2(f32x2_t a, f32x2_t b, f32x2_t c) {
+  f32x2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
 }
 
 // ---- per-tile plan (written by the build, read by the force kernel) --------
@@ -873,6 +909,350 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
 }
 
+// ---- build v2: flattened spherical windows, planar FP32, packed tests -------
+// Per row (one lane): the 9 stencil columns' z-windows are cut to the sphere,
+// h_c^2 = rs^2 - (lateral distance from the row to column c)^2, and stored
+// as a per-lane piece table; the lane then sweeps its pieces back to back
+// (no per-column warp-wide maximum: a warp runs the maximum over lanes of the
+// lanes' total window, ~0.64x the candidate steps of the per-column sweep),
+// four candidates per step from planar FP32 copies (three LDS.128) with the
+// displacement and r^2 of two candidates per FADD2/FFMA2.
+//
+// Build layout: every staged column is one contiguous, z-sorted run at a
+// 4-aligned build slot with >= 3 dummy slots (coordinates 1e30) after it, so
+// a 4-candidate step aligned down from a window start or running past its end
+// reads only the same column (outside the window: farther than the search
+// radius by construction) or dummies -- no masks.  Inside a column the run
+// keeps the force kernel's staging layout (its even-alignment pad slots hold
+// x = y = 1e30 and a z that keeps the run sorted), so build slot = force slot
+// + D[column] and hits are stored as force slots directly.  The row's own
+// slot is a hit (r^2 = 0) and is removed after the sweep.
+constexpr int kB2Warps = 9;
+constexpr int kB2Cap = kStageCap + kSCols * 8;
+constexpr int kB2Pieces = 9;
+constexpr float kB2Margin = 1e-4f;   // lateral / z-window slack (FP32 staging error ~1e-6)
+
+struct Build2Tables {
+  int D[kSCols];                  // build slot = force slot + D[col]
+  int cbeg[kSCols], cend[kSCols]; // force-slot range of each staged column
+  int B[kSCols + 1];              // build-slot start of each column run
+  int run_lo[kSCols][kTZ + 1];    // build-slot run of cells k-1..k+1 of column col (k = 1..bz)
+  int run_hi[kSCols][kTZ + 1];
+  float cxl[kSX], cxh[kSX], cyl[kSY], cyh[kSY];   // column extents relative to the tile centre
+};
+
+__global__ void __launch_bounds__(kB2Warps * 32, 2)
+tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
+                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
+                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
+                   int* __restrict__ flag, const double* __restrict__ bpl, pc_box e,
+                   const int* __restrict__ skip, int* __restrict__ tile_ghost) {
+  extern __shared__ __align__(16) float b2s[];
+  float* __restrict__ sxp = b2s;
+  float* __restrict__ syp = b2s + kB2Cap;
+  float* __restrict__ szp = b2s + 2 * kB2Cap;
+  uint16_t* hits_all = reinterpret_cast<uint16_t*>(b2s + 3 * kB2Cap);
+  uint32_t* pcs_all =
+      reinterpret_cast<uint32_t*>(hits_all + kB2Warps * (kHitCap + kHitSlack) * 32);
+  __shared__ TileSetup T;
+  __shared__ Build2Tables Q;
+  tile_setup<true>(blockIdx.x, g, b, cs, T);
+  if (T.S > p.max_stage) {
+    // as tile_build_kernel: flag, keep one empty row-warp (force-pass safety)
+    const int r0 = rw0[blockIdx.x];
+    if (threadIdx.x < 32) rowidx[(int64_t)r0 * 32 + threadIdx.x] = -1;
+    if (threadIdx.x == 0) {
+      atomicOr(flag, kFlagStage);
+      atomicMax(flag + 1, T.S);
+      int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
+      pg[0] = 0;
+      pg[1] = 0;
+      pg[2] = 1;
+      pg[3] = r0;
+      rounds[r0] = 0;
+      if (tile_ghost) tile_ghost[blockIdx.x] = 1;
+    }
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nrw = skip ? rw0[blockIdx.x + 1] - rw0[blockIdx.x] : max(1, (T.H + 31) >> 5);
+  const int bz = T.bz;
+  if (warp == 0) {                       // compacted plan of this tile (force kernel)
+    int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
+    int base = 0;
+    for (int e0 = 0; e0 < kSegs; e0 += 32) {
+      const int ee = e0 + lane;
+      const bool ne = ee < kSegs && T.seg_len[ee] > 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, ne);
+      if (ne) {
+        const int k = base + __popc(bal & ((1u << lane) - 1u));
+        pg[4 + 3 * k] = T.seg_src[ee];
+        pg[5 + 3 * k] = T.seg_len[ee];
+        pg[6 + 3 * k] = T.seg_dst[ee];
+      }
+      base += __popc(bal);
+    }
+    if (lane == 0) {
+      pg[0] = base;
+      pg[1] = T.S;
+      pg[2] = nrw;
+      pg[3] = rw0[blockIdx.x];
+    }
+  } else if (warp == 1 && lane == 0) {   // column runs of the build layout
+    int Bc = 0;
+    for (int c = 0; c < kSCols; ++c) {
+      const int fb = T.seg_dst[3 * c], fe = T.seg_dst[3 * c + 2] + T.seg_len[3 * c + 2];
+      Q.cbeg[c] = fb;
+      Q.cend[c] = fe;
+      Q.B[c] = Bc;
+      Q.D[c] = Bc - fb;
+      if (fe > fb) Bc = (Bc + (fe - fb) + 3 + 3) & ~3;
+    }
+    Q.B[kSCols] = Bc;
+  } else if (warp == 2 && lane < kSX + kSY) {
+    // staged column sxo spans grid column x0 - 1 + sxo: relative to the tile
+    // centre [(sxo - 1 - bx/2) w, (sxo - bx/2) w) (periodic images included)
+    if (lane < kSX) {
+      Q.cxl[lane] = (float)((lane - 1 - 0.5 * T.bx) * g.width[0]);
+      Q.cxh[lane] = (float)((lane - 0.5 * T.bx) * g.width[0]);
+    } else {
+      const int l = lane - kSX;
+      Q.cyl[l] = (float)((l - 1 - 0.5 * T.by) * g.width[1]);
+      Q.cyh[l] = (float)((l - 0.5 * T.by) * g.width[1]);
+    }
+  }
+  __syncthreads();
+  // runs of cells k-1..k+1 per column (non-empty cells of a column are
+  // contiguous in both layouts; the pads between its segments are dummies)
+  for (int t = threadIdx.x; t < kSCols * kTZ; t += blockDim.x) {
+    const int col = t / kTZ, k = 1 + t % kTZ;
+    int lo = 0x7fffffff, hi = -1;
+    if (k <= bz)
+      for (int kk = k - 1; kk <= k + 1; ++kk) {
+        const int l = T.cell_lo[col][kk], h = T.cell_hi[col][kk];
+        if (h > l) {
+          lo = min(lo, l);
+          hi = max(hi, h);
+        }
+      }
+    if (hi < 0) lo = hi = 0;
+    Q.run_lo[col][k] = lo + Q.D[col];
+    Q.run_hi[col][k] = hi + Q.D[col];
+  }
+  const int64_t ps = p.ps;
+  int ghost_seen = 0;
+  // stage: one warp per segment; pads (even-alignment extras of the force
+  // layout) become x = y = 1e30 with the z of the nearest true particle
+  for (int s = warp; s < kSegs; s += kB2Warps) {
+    const int len = T.seg_len[s];
+    if (len == 0) continue;
+    const int col = s / 3;
+    const int src = T.seg_src[s], dst = T.seg_dst[s] + Q.D[col];
+    const int tf = T.seg_tf[s], te = T.seg_te[s];
+    const double sx = (double)T.seg_shift[s][0] * b.length[0] - T.ox;
+    const double sy = (double)T.seg_shift[s][1] * b.length[1] - T.oy;
+    const double sz = (double)T.seg_shift[s][2] * b.length[2] - T.oz;
+    for (int t = lane; t < len; t += 32) {
+      const int idx = src + t;
+      const int j = min(max(idx, tf), te - 1);
+      const bool pad = idx != j;
+      const float qx = (float)(bpl[j] + sx), qy = (float)(bpl[ps + j] + sy);
+      szp[dst + t] = (float)(bpl[2 * ps + j] + sz);
+      sxp[dst + t] = pad ? 1e30f : qx;
+      syp[dst + t] = pad ? 1e30f : qy;
+      if (tile_ghost && skip) ghost_seen |= skip[idx];
+    }
+  }
+  if (threadIdx.x < kSCols) {            // dummy gap after each column run
+    const int c = threadIdx.x;
+    for (int t = Q.B[c] + (Q.cend[c] - Q.cbeg[c]); t < Q.B[c + 1]; ++t) {
+      sxp[t] = 1e30f;
+      syp[t] = 1e30f;
+      szp[t] = 1e30f;
+    }
+  }
+  ghost_seen = __syncthreads_or(ghost_seen);
+  if (tile_ghost && threadIdx.x == 0) tile_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
+
+  const float hi2 = p.hi2;
+  // window sphere (search radius^2 plus slack) and the FP32 band: a hit with
+  // r^2 >= lo2 is decided by the reference's FP64 predicate
+  const float hw2 = hi2 * 1.00002f + kB2Margin;
+  const float bmid = 0.5f * (p.lo2 + hi2), bhalf = 0.5f * (hi2 - p.lo2) * 1.001f;
+  uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
+  uint32_t* pcs = pcs_all + warp * kB2Pieces * 32 + lane;                  // [piece][lane]
+  for (int w = warp; w < nrw; w += kB2Warps) {
+    const int u = w * 32 + lane;
+    int ocol = 0;
+    const int opos = skip ? owned_row_slot(T, skip, w, lane, ocol) : -1;
+    const bool act = skip ? opos >= 0 : u < T.H;
+    int cnt = 0, a = -1, pos = -1;
+    bool band = false;
+    float mx = 0.f, my = 0.f, mz = 0.f;
+    if (act) {
+      const uint32_t hbase = smem_u32(hits);
+      const uint32_t hend = hbase + (uint32_t)(kHitCap - 1) * 64u;
+      int c = 0;
+#pragma unroll
+      for (int q = 1; q < kBX * kBY; ++q) c += (u >= T.home_pre[q]) ? 1 : 0;
+      if (skip) c = ocol;
+      const int hx = c / kBY, hy = c - hx * kBY;
+      const int hcol = (hx + 1) * kSY + (hy + 1);
+      pos = skip ? opos : T.cell_lo[hcol][1] + (u - T.home_pre[c]);   // force slot
+      int k = 1;
+      for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
+      a = T.seg_src[hcol * 3 + 1] + (pos - T.seg_dst[hcol * 3 + 1]);
+      const int pb = pos + Q.D[hcol];
+      mx = sxp[pb];
+      my = syp[pb];
+      mz = szp[pb];
+      // windows -> piece table (non-empty pieces only, column order)
+      int np = 0;
+#pragma unroll 1
+      for (int dxo = 0; dxo < 3; ++dxo) {
+        const int sxo = hx + dxo;
+        const float ddx = fmaxf(0.f, fmaxf(Q.cxl[sxo] - mx, mx - Q.cxh[sxo]) - kB2Margin);
+#pragma unroll
+        for (int dyo = 0; dyo < 3; ++dyo) {
+          const int syo = hy + dyo;
+          const int col = sxo * kSY + syo;
+          const float ddy = fmaxf(0.f, fmaxf(Q.cyl[syo] - my, my - Q.cyh[syo]) - kB2Margin);
+          const float d2 = fmaf(ddx, ddx, ddy * ddy);
+          if (d2 >= hw2) continue;
+          const float h = sqrtf(hw2 - d2) * 1.0001f + kB2Margin;
+          const float zlo = mz - h, zhi = mz + h;
+          int lo = Q.run_lo[col][k], h1 = Q.run_hi[col][k];
+          int hi = lo, h3 = h1;
+          while (lo < h1) {                      // first z >= zlo
+            const int mid = (lo + h1) >> 1;
+            if (szp[mid] < zlo) lo = mid + 1; else h1 = mid;
+          }
+          hi = lo;
+          while (hi < h3) {                      // first z > zhi
+            const int mid = (hi + h3) >> 1;
+            if (szp[mid] <= zhi) hi = mid + 1; else h3 = mid;
+          }
+          if (hi > lo) {
+            pcs[np * 32] = (uint32_t)lo | ((uint32_t)hi << 12) | ((uint32_t)col << 24);
+            ++np;
+          }
+        }
+      }
+      // sweep: four candidates per step, pieces back to back
+      const f32x2_t nx2 = pk2(-mx, -mx), ny2 = pk2(-my, -my), nz2 = pk2(-mz, -mz);
+      const f32x2_t nb2 = pk2(-bmid, -bmid);
+      float amin = 1e30f;
+      uint32_t ha = hbase, hself = hbase;
+      int pi = 0, i = 0, end = 0, dd = 0;
+      if (np > 0) {
+        const uint32_t pc = pcs[0];
+        i = (int)(pc & 0xFFFu) & ~3;
+        end = (int)((pc >> 12) & 0xFFFu);
+        dd = Q.D[pc >> 24];
+        if ((int)(pc >> 24) == hcol) hself = ha;
+      }
+      while (pi < np) {
+        const float4 X = *reinterpret_cast<const float4*>(sxp + i);
+        const float4 Y = *reinterpret_cast<const float4*>(syp + i);
+        const float4 Z = *reinterpret_cast<const float4*>(szp + i);
+        const f32x2_t dx01 = add2(pk2(X.x, X.y), nx2), dx23 = add2(pk2(X.z, X.w), nx2);
+        const f32x2_t dy01 = add2(pk2(Y.x, Y.y), ny2), dy23 = add2(pk2(Y.z, Y.w), ny2);
+        const f32x2_t dz01 = add2(pk2(Z.x, Z.y), nz2), dz23 = add2(pk2(Z.z, Z.w), nz2);
+        // fmaf(dz, dz, fmaf(dy, dy, dx * dx)) per candidate, as the band bound assumes
+        const f32x2_t r01 = fma2(dz01, dz01, fma2(dy01, dy01, mul2(dx01, dx01)));
+        const f32x2_t r23 = fma2(dz23, dz23, fma2(dy23, dy23, mul2(dx23, dx23)));
+        float r0, r1, r2, r3, t0, t1, t2, t3;
+        upk2(r01, r0, r1);
+        upk2(r23, r2, r3);
+        upk2(add2(r01, nb2), t0, t1);
+        upk2(add2(r23, nb2), t2, t3);
+        amin = fminf(amin, fminf(fminf(fabsf(t0), fabsf(t1)), fminf(fabsf(t2), fabsf(t3))));
+        const int v = i - dd;                   // force slot of candidate 0
+        const uint32_t o1 = ha + (r0 < hi2 ? 64u : 0u);
+        const uint32_t o2 = o1 + (r1 < hi2 ? 64u : 0u);
+        const uint32_t o3 = o2 + (r2 < hi2 ? 64u : 0u);
+        st_shared_u16(ha, (uint16_t)v);
+        st_shared_u16(o1, (uint16_t)(v + 1));
+        st_shared_u16(o2, (uint16_t)(v + 2));
+        st_shared_u16(o3, (uint16_t)(v + 3));
+        ha = min(o3 + (r3 < hi2 ? 64u : 0u), hend);
+        i += 4;
+        if (i >= end) {
+          if (++pi < np) {
+            const uint32_t pc = pcs[pi * 32];
+            i = (int)(pc & 0xFFFu) & ~3;
+            end = (int)((pc >> 12) & 0xFFFu);
+            dd = Q.D[pc >> 24];
+            if ((int)(pc >> 24) == hcol) hself = ha;
+          }
+        }
+      }
+      cnt = (int)((ha - hbase) >> 6);
+      if (cnt >= kHitCap - 1) {
+        cnt = kHitCap;                          // (possible) overflow: flagged below
+      } else {
+        // remove the row's own slot (r^2 = 0, in its home column's piece):
+        // the last entry takes its place
+        int ks = (int)((hself - hbase) >> 6);
+        while (ks < cnt - 1 && hits[ks * 32] != (uint16_t)pos) ++ks;
+        hits[ks * 32] = hits[(cnt - 1) * 32];
+        --cnt;
+        band = amin <= bhalf;
+      }
+    }
+    // hits inside the FP32 band: the reference's FP64 predicate decides (rare)
+    if (__any_sync(0xffffffffu, band)) {
+      if (band) {
+        int m = 0;
+        for (int t = 0; t < cnt; ++t) {
+          const int v = hits[t * 32];
+          int col = 0;
+          while (col < kSCols - 1 && !(v >= Q.cbeg[col] && v < Q.cend[col])) ++col;
+          const int q = v + Q.D[col];
+          const float dx = sxp[q] - mx, dy = syp[q] - my, dz = szp[q] - mz;
+          const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          bool keep = rr < p.lo2;
+          if (!keep) {
+            int s = col * 3;
+            while (s < col * 3 + 2 && !(T.seg_len[s] > 0 && v >= T.seg_dst[s] &&
+                                        v < T.seg_dst[s] + T.seg_len[s]))
+              ++s;
+            keep = exact_pair_pl(pl, ps, a, T.seg_src[s] + (v - T.seg_dst[s]), e, p.cutoff2);
+          }
+          if (keep) hits[m++ * 32] = (uint16_t)v;
+        }
+        cnt = m;
+      }
+    }
+    const int rw = rw0[blockIdx.x] + w;
+    rowidx[(int64_t)rw * 32 + lane] = a;
+    const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+    if (cmax >= kHitCap) {
+      if (lane == 0) {
+        atomicOr(flag, kFlagOverflow);
+        atomicMax(flag + 2, 1 << 20);
+        rounds[rw] = 0;
+      }
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    const int cap = 8 * p.Q8;
+    uint4* lout = list + (int64_t)rw * p.Q8 * 32 + lane;
+    const int R = p.sched == 0   ? cm_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                  : p.sched == 4 ? rr_rows(hits, cnt, lane, p.max_stage, lout, cap)
+                                 : plain_rows(hits, cnt, lane, p.max_stage, lout, cap);
+    if (lane == 0) {
+      rounds[rw] = ((R + 7) & ~7) > cap ? 0 : R;
+      if (((R + 7) & ~7) > cap) {
+        atomicOr(flag, kFlagOverflow);
+        atomicMax(flag + 2, R);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void pos_from_planar_kernel(const double* __restrict__ pl, int64_t ps, int n,
                                        double* __restrict__ pos4) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -939,11 +1319,30 @@ struct TileForceParams {
   int64_t ps;
 };
 
+#ifndef PC_FORCE_TILEBAR
+#define PC_FORCE_TILEBAR 0      // 1: waits on a per-tile mbarrier (hardware-suspended try_wait) instead of polling which buffer holds the tile
+#endif
+// Per-tile barriers: tile sequence index k completes phase k / kTileBars of
+// tbar[k % kTileBars] (armed by its loader, completed by its bulk copies);
+// bufof[] names the buffer it was staged into.  A warp holding an item of
+// tile k waits with parity (k / kTileBars) & 1, which is right once tile
+// k - kTileBars has completed: items are claimed in order and at most 4
+// tiles are resident, so tile k - 128 still in flight would need ~90 later
+// tiles fully processed through the other buffers during one bulk copy.
+constexpr int kTileBars = 128;
+#ifndef PC_FORCE_GUARD
+#define PC_FORCE_GUARD 1
+#endif
 struct ForceShared {
+#if PC_FORCE_TILEBAR
+  uint64_t tbar[kTileBars];
+  volatile unsigned char bufof[kTileBars];
+#else
   uint64_t bar[kNBuf];
   volatile int seq[kNBuf];   // tile sequence index held by each buffer (-1: none)
   int par[kNBuf];            // mbarrier parity of the current use
   int uses[kNBuf];
+#endif
   int done[kNBuf];           // finished row-warps of the current tile
   int next_item;
   int loaded;                // tickets: next tile sequence index to load
@@ -1016,6 +1415,100 @@ __device__ __forceinline__ void tile_pair(const char* __restrict__ st, uint32_t 
   fz = fma(-fmd, dz, fz);
 }
 
+// FP64 half of a pair: displacement (minimum image near periodic faces),
+// exact r^2 and cutoff test; returns the narrowed r^2 of an interacting pair,
+// else 1e30 (the FP32 terms then vanish exactly)
+template <bool MI>
+__device__ __forceinline__ float pair_geom(const char* __restrict__ st, uint32_t off, double xi,
+                                           double yi, double zi, bool nx, bool ny, bool nz,
+                                           const pc_box& b, const TileForceParams& p, double& dx,
+                                           double& dy, double& dz, bool& overlap) {
+  const double* q = reinterpret_cast<const double*>(st + off);
+  dx = __dsub_rn(q[0], xi);
+  dy = __dsub_rn(q[kStageStride], yi);
+  dz = __dsub_rn(q[2 * kStageStride], zi);
+  if (MI) {
+    if (nx) dx = min_image_wrapped(dx, b.length[0], b.mi_thresh[0]);
+    if (ny) dy = min_image_wrapped(dy, b.length[1], b.mi_thresh[1]);
+    if (nz) dz = min_image_wrapped(dz, b.length[2], b.mi_thresh[2]);
+  }
+  const double r2 = r2_exact(dx, dy, dz);
+  overlap |= r2 < p.overlap2;
+  return r2 < p.cutoff2 ? d2f_fast(r2) : 1e30f;
+}
+
+template <bool MI, bool UNIT_SIGMA>
+__device__ __forceinline__ void tile_pair2(const char* __restrict__ st, uint32_t w, double xi,
+                                           double yi, double zi, bool nx, bool ny, bool nz,
+                                           const pc_box& b, const TileForceParams& p,
+                                           double& fx, double& fy, double& fz, f32x2_t& su2,
+                                           f32x2_t& s62, bool& overlap) {
+  double dxa, dya, dza, dxb, dyb, dzb;
+  const float ra = pair_geom<MI>(st, w & 0xFFFFu, xi, yi, zi, nx, ny, nz, b, p, dxa, dya, dza,
+                                 overlap);
+  const float rb = pair_geom<MI>(st, w >> 16, xi, yi, zi, nx, ny, nz, b, p, dxb, dyb, dzb,
+                                 overlap);
+  const f32x2_t inv = pk2(rcp_approx(ra), rcp_approx(rb));
+  const f32x2_t sr2 = UNIT_SIGMA ? inv : mul2(pk2(p.sig2, p.sig2), inv);
+  const f32x2_t sr6 = mul2(mul2(sr2, sr2), sr2);
+  // u = 2 sr12 - sr6 = sr6 (2 sr6 - 1) (pair virial); fm = u / r^2
+  const f32x2_t u = mul2(sr6, fma2(pk2(2.0f, 2.0f), sr6, pk2(-1.0f, -1.0f)));
+  const f32x2_t fm = mul2(u, inv);
+  su2 = add2(su2, u);
+  s62 = add2(s62, sr6);
+  float fa, fb;
+  upk2(fm, fa, fb);
+  const double fda = (double)fa, fdb = (double)fb;
+  fx = fma(-fda, dxa, fx);
+  fy = fma(-fda, dya, fy);
+  fz = fma(-fda, dza, fz);
+  fx = fma(-fdb, dxb, fx);
+  fy = fma(-fdb, dyb, fy);
+  fz = fma(-fdb, dzb, fz);
+}
+
+#ifndef PC_FORCE_PACKED
+#define PC_FORCE_PACKED 1       // FP32 LJ terms of two pairs as f32x2 (FFMA2/FMUL2/FADD2)
+#endif
+
+template <bool MI, bool UNIT_SIGMA, int B>
+__device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
+                                          const uint4* __restrict__ lp, uint4 first, int R,
+                                          double xi, double yi, double zi, bool nx, bool ny,
+                                          bool nz, const pc_box& b, const TileForceParams& p,
+                                          double& fx, double& fy, double& fz, float& su,
+                                          float& s6, bool& overlap) {
+  const char* __restrict__ st =
+      B >= 0 ? reinterpret_cast<const char*>(pc_force_dyn) + (size_t)B * 3 * kStageStride * 8
+             : st_rt;
+  const int G = R >> 3;
+  const int tail = R & 7;
+  f32x2_t su2 = 0ull, s62 = 0ull;   // (+0.0f, +0.0f)
+  uint4 nxt = first;
+  for (int gi = 0; gi < G; ++gi) {
+    const uint4 q = nxt;
+    if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
+    if (PC_FORCE_PREFETCH && gi + 2 < G) prefetch_l2(lp + (gi + 2) * 32);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      tile_pair2<MI, UNIT_SIGMA>(st, w[h], xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, su2, s62,
+                                 overlap);
+  }
+  // open group: pairs in twos (an odd tail's partner is a padding dummy:
+  // far and NaN-free, it adds exactly 0)
+  for (int j = 0; j < tail; j += 2) {
+    const uint32_t w = (j >> 1) == 0 ? nxt.x : ((j >> 1) == 1 ? nxt.y : ((j >> 1) == 2 ? nxt.z : nxt.w));
+    tile_pair2<MI, UNIT_SIGMA>(st, w, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, su2, s62,
+                               overlap);
+  }
+  float a0, a1, c0, c1;
+  upk2(su2, a0, a1);
+  upk2(s62, c0, c1);
+  su = a0 + a1;
+  s6 = c0 + c1;
+}
+
 template <bool MI, bool UNIT_SIGMA, int B>
 __device__ __forceinline__ void tile_row(const char* __restrict__ st_rt,
                                          const uint4* __restrict__ lp, uint4 first, int R,
@@ -1064,24 +1557,38 @@ __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ 
   const int* gp = plan + (int64_t)tile * kPlanInts;
   const int m = gp[0], S = gp[1];
   double* st = stage + (int64_t)b * 3 * kStageStride;
+#if PC_FORCE_TILEBAR
+  uint64_t* bar = &F.tbar[k % kTileBars];
+  if (lane == 0) {
+    F.done[b] = 0;
+    // the previous use of this barrier (tile k - kTileBars) has completed
+    if (PC_FORCE_GUARD && k >= kTileBars) mbar_wait(bar, (uint32_t)((k / kTileBars) - 1) & 1u);
+    F.bufof[k % kTileBars] = (unsigned char)b;
+    mbar_expect_tx(bar, (uint32_t)S * 24u);     // arrive: release (bufof visible to waiters)
+  }
+#else
+  uint64_t* bar = &F.bar[b];
   if (lane == 0) {
     F.done[b] = 0;
     F.par[b] = F.uses[b] & 1;
     F.uses[b] += 1;
-    mbar_expect_tx(&F.bar[b], (uint32_t)S * 24u);
+    mbar_expect_tx(bar, (uint32_t)S * 24u);
   }
+#endif
   __syncwarp();
   for (int e = lane; e < m; e += 32) {
     const int src = gp[4 + 3 * e], len = gp[5 + 3 * e], dst = gp[6 + 3 * e];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      bulk_g2s(st + a * kStageStride + dst, pl + a * ps + src, (uint32_t)len * 8u, &F.bar[b]);
+      bulk_g2s(st + a * kStageStride + dst, pl + a * ps + src, (uint32_t)len * 8u, bar);
   }
+#if !PC_FORCE_TILEBAR
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
     F.seq[b] = k;
   }
+#endif
 }
 
 template <bool UNIT_SIGMA>
@@ -1133,11 +1640,15 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       F.tiles = tiles;
       F.t0 = t0;
       F.next_item = 0;
+#if PC_FORCE_TILEBAR
+      for (int q = 0; q < kTileBars; ++q) mbar_init(&F.tbar[q], 1);
+#else
       for (int q = 0; q < kNBuf; ++q) {
         F.seq[q] = -1;
         F.uses[q] = 0;
         mbar_init(&F.bar[q], 1);
       }
+#endif
       F.loaded = min(K, nbuf);
     }
     __syncwarp();
@@ -1235,6 +1746,10 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       }
     }
     // buffer holding tile k (loaded in ticket order; spin until published)
+#if PC_FORCE_TILEBAR
+    mbar_wait(&F.tbar[k % kTileBars], (uint32_t)(k / kTileBars) & 1u);
+    const int bsel = F.bufof[k % kTileBars];
+#else
     int bsel = -1;
     for (;;) {
 #pragma unroll
@@ -1245,6 +1760,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     }
     __threadfence_block();
     mbar_wait(&F.bar[bsel], (uint32_t)F.par[bsel]);
+#endif
     const char* st = reinterpret_cast<const char*>(stage + (int64_t)bsel * 3 * kStageStride);
 
     const bool nx = act && b.periodic[0] && (xi - b.low[0] < p.guard || b.high[0] - xi <= p.guard);
@@ -1254,12 +1770,17 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     float su = 0.f, s6 = 0.f;
     bool overlap = false;
     const bool mi = __any_sync(0xffffffffu, nx || ny || nz);
+#if PC_FORCE_PACKED
+#define PC_ROWFN tile_row2
+#else
+#define PC_ROWFN tile_row
+#endif
 #define PC_ROW(BB)                                                                            \
   if (mi)                                                                                     \
-    tile_row<true, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, \
+    PC_ROWFN<true, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy, fz, \
                                    su, s6, overlap);                                          \
   else                                                                                        \
-    tile_row<false, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy,   \
+    PC_ROWFN<false, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy,   \
                                     fz, su, s6, overlap);
 #if PC_FORCE_STATIC_BUF
     static_assert(kNBuf == 4, "one code path per staging buffer");
@@ -1295,7 +1816,9 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     if (last) {
       int kn = 0;
       if (lane == 0) {
+#if !PC_FORCE_TILEBAR
         F.seq[bsel] = -1;
+#endif
         kn = atomicAdd(&F.loaded, 1);
       }
       kn = __shfl_sync(0xffffffffu, kn, 0);
@@ -1532,7 +2055,7 @@ tile_decode_kernel(const int* __restrict__ plan, int Q8, int max_stage,
 using namespace pc;
 
 namespace {
-int g_build_smem = 0, g_force_smem = 0;
+int g_build_smem = 0, g_build2_smem = 0, g_force_smem = 0;
 }
 
 extern "C" {
@@ -1626,18 +2149,39 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   p.max_stage = kStageCap;
   p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 3;
   p.ps = planar_stride;
-  const int smem = kStageCap * (int)sizeof(float4) +
-                   kBuildWarps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t);
-  if (smem > g_build_smem) {
-    if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // PC_TILE_BUILD=1: the per-column sweep (r01 / r02 build); default 2:
+  // flattened spherical windows (tile_build2_kernel)
+  static const int version = getenv("PC_TILE_BUILD") ? atoi(getenv("PC_TILE_BUILD")) : 2;
+  const int nt = tile_dims(*grid).ntiles;
+  if (version == 1) {
+    const int smem = kStageCap * (int)sizeof(float4) +
+                     kBuildWarps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t);
+    if (smem > g_build_smem) {
+      if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem) != cudaSuccess) {
+        set_error("pc_tile_build: %d B of shared memory not available", smem);
+        return PC_ERR_CAPACITY;
+      }
+      g_build_smem = smem;
+    }
+    tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
+        d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
+        reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
+        box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
+    return check_launch("pc_tile_build");
+  }
+  const int smem = 3 * kB2Cap * (int)sizeof(float) +
+                   kB2Warps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t) +
+                   kB2Warps * 32 * kB2Pieces * (int)sizeof(uint32_t);
+  if (smem > g_build2_smem) {
+    if (cudaFuncSetAttribute(tile_build2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess) {
       set_error("pc_tile_build: %d B of shared memory not available", smem);
       return PC_ERR_CAPACITY;
     }
-    g_build_smem = smem;
+    g_build2_smem = smem;
   }
-  const int nt = tile_dims(*grid).ntiles;
-  tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
+  tile_build2_kernel<<<nt, kB2Warps * 32, smem, as_stream(stream)>>>(
       d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
       reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
       box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
@@ -1683,7 +2227,7 @@ int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
   }
   const int buf_bytes = 3 * kStageStride * (int)sizeof(double);
   const int pre_bytes = (2 * K + 1) * (int)sizeof(int);
-  const int static_bytes = 512;
+  const int static_bytes = (int)sizeof(ForceShared) + 256;
   int nbuf = kNBuf;
   while (nbuf > 2 && nbuf * buf_bytes + pre_bytes + static_bytes > smem_max) --nbuf;
   const int smem = nbuf * buf_bytes + pre_bytes + K * (int)sizeof(int);

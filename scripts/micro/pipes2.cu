@@ -21,6 +21,13 @@ __global__ void k(float* out, int iters, double a, float af, int ai) {
       if (OP == 8) q[t] = (q[t] ^ ai) + (q[t] >> 3);          // ALU
       if (OP == 9) d[t] = (d[t] < a) ? d[t] + 1.0 : d[t];     // DSETP + DADD + sel
       if (OP == 10) { double r; asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d[t])); d[t] = r + a; }
+      if (OP == 11) d[t] = (double)f[t] * a + d[t], f[t] = f[t] + af; // F2F.F64.F32 + DFMA + FADD
+      if (OP == 12) {                                           // FFMA2 (two FP32 lanes per op)
+        unsigned long long x, y = ((unsigned long long)__float_as_uint(af) << 32) | __float_as_uint(af);
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(f[t]), "f"(f[(t + 1) & 7]));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(x) : "l"(y));
+        float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x)); f[t] = lo + hi * 0.f;
+      }
     }
   }
   float s = 0;
@@ -44,5 +51,6 @@ int main() {
   run<3>("F2F.F64.F32+DMUL (pairs)", 8); run<4>("FFMA", 8); run<5>("IADD+I2F (pairs)", 8);
   run<6>("__frcp_rn (+FADD)", 8); run<7>("rcp.approx.f32 (+FADD)", 8); run<8>("LOP/SHF/IADD (x3)", 8);
   run<9>("DSETP+DADD+FSEL", 8); run<10>("MUFU.RCP64H(+DADD)", 8);
+  run<11>("F2F.F64.F32+DFMA+FADD (trip)", 8); run<12>("FFMA2 (+pack)", 8);
   return 0;
 }
