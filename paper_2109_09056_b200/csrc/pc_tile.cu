@@ -927,10 +927,17 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
 // x = y = 1e30 and a z that keeps the run sorted), so build slot = force slot
 // + D[column] and hits are stored as force slots directly.  The row's own
 // slot is a hit (r^2 = 0) and is removed after the sweep.
-constexpr int kB2Warps = 9;
+// warps per CTA: two CTAs per SM in 227 KB (the flat variant also keeps a
+// per-lane piece table)
+__host__ __device__ constexpr int b2_warps(bool flat) { return flat ? 9 : 10; }
 constexpr int kB2Cap = kStageCap + kSCols * 8;
 constexpr int kB2Pieces = 9;
 constexpr float kB2Margin = 1e-4f;   // lateral / z-window slack (FP32 staging error ~1e-6)
+
+#ifndef PC_B2_ZTAB
+#define PC_B2_ZTAB 0     // 1: window bounds from a per-column z index instead of two binary searches (hot config build 4.31 vs 3.81 ms: the index fill is a serial phase between two barriers, profiles/r02t)
+#endif
+constexpr int kZB = 16;  // z-index boundaries per staged cell
 
 struct Build2Tables {
   int D[kSCols];                  // build slot = force slot + D[col]
@@ -939,21 +946,40 @@ struct Build2Tables {
   int run_lo[kSCols][kTZ + 1];    // build-slot run of cells k-1..k+1 of column col (k = 1..bz)
   int run_hi[kSCols][kTZ + 1];
   float cxl[kSX], cxh[kSX], cyl[kSY], cyh[kSY];   // column extents relative to the tile centre
+#if PC_B2_ZTAB
+  // z index of every column run: boundaries Z_q = zbase + q dzq (kZB per
+  // staged cell, q = 0..zq); ztab[col][q] = first build slot of the run with
+  // z >= Z_q (the run's end if none) -- a window's bounds in two loads
+  uint16_t ztab[kSCols][(kTZ + 2) * kZB + 1];
+  float zbase, dzq, idzq;
+  int zq;
+#endif
 };
 
-__global__ void __launch_bounds__(kB2Warps * 32, 2)
+// largest q in [-1, zq] with Z_q <= z (Z_q = fmaf(q, dzq, zbase), monotone)
+__device__ __forceinline__ int zq_of(float z, float zbase, float dzq, float idzq, int zq) {
+  int q = (int)floorf((z - zbase) * idzq);
+  q = min(max(q, -1), zq);
+  if (q >= 0 && fmaf((float)q, dzq, zbase) > z) --q;
+  if (q < zq && fmaf((float)(q + 1), dzq, zbase) <= z) ++q;
+  return q;
+}
+
+template <bool FLAT>
+__global__ void __launch_bounds__(b2_warps(FLAT) * 32, 2)
 tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
                    TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
                    int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
                    int* __restrict__ flag, const double* __restrict__ bpl, pc_box e,
                    const int* __restrict__ skip, int* __restrict__ tile_ghost) {
+  constexpr int kW = b2_warps(FLAT);
   extern __shared__ __align__(16) float b2s[];
   float* __restrict__ sxp = b2s;
   float* __restrict__ syp = b2s + kB2Cap;
   float* __restrict__ szp = b2s + 2 * kB2Cap;
   uint16_t* hits_all = reinterpret_cast<uint16_t*>(b2s + 3 * kB2Cap);
   uint32_t* pcs_all =
-      reinterpret_cast<uint32_t*>(hits_all + kB2Warps * (kHitCap + kHitSlack) * 32);
+      reinterpret_cast<uint32_t*>(hits_all + kW * (kHitCap + kHitSlack) * 32);
   __shared__ TileSetup T;
   __shared__ Build2Tables Q;
   tile_setup<true>(blockIdx.x, g, b, cs, T);
@@ -998,17 +1024,30 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
       pg[2] = nrw;
       pg[3] = rw0[blockIdx.x];
     }
-  } else if (warp == 1 && lane == 0) {   // column runs of the build layout
-    int Bc = 0;
-    for (int c = 0; c < kSCols; ++c) {
-      const int fb = T.seg_dst[3 * c], fe = T.seg_dst[3 * c + 2] + T.seg_len[3 * c + 2];
+  } else if (warp == 1) {                // column runs of the build layout
+    // column c takes align4(len + 3) build slots (>= 3 trailing dummies);
+    // starts by a warp scan
+    static_assert(kSCols <= 32, "one lane per staged column");
+    const int c = lane;
+    int fb = 0, fe = 0;
+    if (c < kSCols) {
+      fb = T.seg_dst[3 * c];
+      fe = T.seg_dst[3 * c + 2] + T.seg_len[3 * c + 2];
+    }
+    const int foot = fe > fb ? (fe - fb + 3 + 3) & ~3 : 0;
+    int inc = foot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (c < kSCols) {
       Q.cbeg[c] = fb;
       Q.cend[c] = fe;
-      Q.B[c] = Bc;
-      Q.D[c] = Bc - fb;
-      if (fe > fb) Bc = (Bc + (fe - fb) + 3 + 3) & ~3;
+      Q.B[c] = inc - foot;
+      Q.D[c] = inc - foot - fb;
     }
-    Q.B[kSCols] = Bc;
+    if (c == kSCols - 1) Q.B[kSCols] = inc;
   } else if (warp == 2 && lane < kSX + kSY) {
     // staged column sxo spans grid column x0 - 1 + sxo: relative to the tile
     // centre [(sxo - 1 - bx/2) w, (sxo - bx/2) w) (periodic images included)
@@ -1043,7 +1082,7 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
   int ghost_seen = 0;
   // stage: one warp per segment; pads (even-alignment extras of the force
   // layout) become x = y = 1e30 with the z of the nearest true particle
-  for (int s = warp; s < kSegs; s += kB2Warps) {
+  for (int s = warp; s < kSegs; s += kW) {
     const int len = T.seg_len[s];
     if (len == 0) continue;
     const int col = s / 3;
@@ -1073,6 +1112,23 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
   }
   ghost_seen = __syncthreads_or(ghost_seen);
   if (tile_ghost && threadIdx.x == 0) tile_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
+#if PC_B2_ZTAB
+  const float zbase = (float)((-1.0 - 0.5 * bz) * g.width[2]);
+  const float dzq = (float)(g.width[2] / kZB), idzq = 1.0f / dzq;
+  const int zq = (bz + 2) * kZB;
+  // slot s of a run is the first slot with z >= Z_q for q in (q(z_{s-1}), q(z_s)]
+  for (int c = 0; c < kSCols; ++c) {
+    const int b0 = Q.B[c], len = Q.cend[c] - Q.cbeg[c];
+    for (int t = threadIdx.x; t < len; t += blockDim.x) {
+      const int qs = zq_of(szp[b0 + t], zbase, dzq, idzq, zq);
+      const int qp = t > 0 ? zq_of(szp[b0 + t - 1], zbase, dzq, idzq, zq) : -1;
+      for (int q = qp + 1; q <= qs; ++q) Q.ztab[c][q] = (uint16_t)(b0 + t);
+      if (t == len - 1)
+        for (int q = qs + 1; q <= zq; ++q) Q.ztab[c][q] = (uint16_t)(b0 + len);
+    }
+  }
+  __syncthreads();
+#endif
 
   const float hi2 = p.hi2;
   // window sphere (search radius^2 plus slack) and the FP32 band: a hit with
@@ -1081,7 +1137,7 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
   const float bmid = 0.5f * (p.lo2 + hi2), bhalf = 0.5f * (hi2 - p.lo2) * 1.001f;
   uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
   uint32_t* pcs = pcs_all + warp * kB2Pieces * 32 + lane;                  // [piece][lane]
-  for (int w = warp; w < nrw; w += kB2Warps) {
+  for (int w = warp; w < nrw; w += kW) {
     const int u = w * 32 + lane;
     int ocol = 0;
     const int opos = skip ? owned_row_slot(T, skip, w, lane, ocol) : -1;
@@ -1106,59 +1162,21 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
       mx = sxp[pb];
       my = syp[pb];
       mz = szp[pb];
-      // windows -> piece table (non-empty pieces only, column order)
-      int np = 0;
-#pragma unroll 1
-      for (int dxo = 0; dxo < 3; ++dxo) {
-        const int sxo = hx + dxo;
-        const float ddx = fmaxf(0.f, fmaxf(Q.cxl[sxo] - mx, mx - Q.cxh[sxo]) - kB2Margin);
-#pragma unroll
-        for (int dyo = 0; dyo < 3; ++dyo) {
-          const int syo = hy + dyo;
-          const int col = sxo * kSY + syo;
-          const float ddy = fmaxf(0.f, fmaxf(Q.cyl[syo] - my, my - Q.cyh[syo]) - kB2Margin);
-          const float d2 = fmaf(ddx, ddx, ddy * ddy);
-          if (d2 >= hw2) continue;
-          const float h = sqrtf(hw2 - d2) * 1.0001f + kB2Margin;
-          const float zlo = mz - h, zhi = mz + h;
-          int lo = Q.run_lo[col][k], h1 = Q.run_hi[col][k];
-          int hi = lo, h3 = h1;
-          while (lo < h1) {                      // first z >= zlo
-            const int mid = (lo + h1) >> 1;
-            if (szp[mid] < zlo) lo = mid + 1; else h1 = mid;
-          }
-          hi = lo;
-          while (hi < h3) {                      // first z > zhi
-            const int mid = (hi + h3) >> 1;
-            if (szp[mid] <= zhi) hi = mid + 1; else h3 = mid;
-          }
-          if (hi > lo) {
-            pcs[np * 32] = (uint32_t)lo | ((uint32_t)hi << 12) | ((uint32_t)col << 24);
-            ++np;
-          }
-        }
-      }
-      // sweep: four candidates per step, pieces back to back
       const f32x2_t nx2 = pk2(-mx, -mx), ny2 = pk2(-my, -my), nz2 = pk2(-mz, -mz);
       const f32x2_t nb2 = pk2(-bmid, -bmid);
       float amin = 1e30f;
       uint32_t ha = hbase, hself = hbase;
-      int pi = 0, i = 0, end = 0, dd = 0;
-      if (np > 0) {
-        const uint32_t pc = pcs[0];
-        i = (int)(pc & 0xFFFu) & ~3;
-        end = (int)((pc >> 12) & 0xFFFu);
-        dd = Q.D[pc >> 24];
-        if ((int)(pc >> 24) == hcol) hself = ha;
-      }
-      while (pi < np) {
+      // four candidates at build slots i..i+3 (4-aligned): displacement and
+      // r^2 two candidates per FADD2 / FFMA2 (fmaf(dz, dz, fmaf(dy, dy, dx*dx))
+      // per candidate, as the band bound assumes); every candidate is stored
+      // at the running hit address, which advances on a hit
+      auto step4 = [&](int i, int dd) {
         const float4 X = *reinterpret_cast<const float4*>(sxp + i);
         const float4 Y = *reinterpret_cast<const float4*>(syp + i);
         const float4 Z = *reinterpret_cast<const float4*>(szp + i);
         const f32x2_t dx01 = add2(pk2(X.x, X.y), nx2), dx23 = add2(pk2(X.z, X.w), nx2);
         const f32x2_t dy01 = add2(pk2(Y.x, Y.y), ny2), dy23 = add2(pk2(Y.z, Y.w), ny2);
         const f32x2_t dz01 = add2(pk2(Z.x, Z.y), nz2), dz23 = add2(pk2(Z.z, Z.w), nz2);
-        // fmaf(dz, dz, fmaf(dy, dy, dx * dx)) per candidate, as the band bound assumes
         const f32x2_t r01 = fma2(dz01, dz01, fma2(dy01, dy01, mul2(dx01, dx01)));
         const f32x2_t r23 = fma2(dz23, dz23, fma2(dy23, dy23, mul2(dx23, dx23)));
         float r0, r1, r2, r3, t0, t1, t2, t3;
@@ -1176,15 +1194,95 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
         st_shared_u16(o2, (uint16_t)(v + 2));
         st_shared_u16(o3, (uint16_t)(v + 3));
         ha = min(o3 + (r3 < hi2 ? 64u : 0u), hend);
-        i += 4;
-        if (i >= end) {
-          if (++pi < np) {
-            const uint32_t pc = pcs[pi * 32];
-            i = (int)(pc & 0xFFFu) & ~3;
-            end = (int)((pc >> 12) & 0xFFFu);
-            dd = Q.D[pc >> 24];
-            if ((int)(pc >> 24) == hcol) hself = ha;
+      };
+      // z-window of stencil column (sxo, syo): the sphere's chord at the
+      // row's lateral distance to the column; [lo, hi) in build slots
+      auto window = [&](int sxo, int syo, int col, int& lo, int& hi) {
+        const float ddx = fmaxf(0.f, fmaxf(Q.cxl[sxo] - mx, mx - Q.cxh[sxo]) - kB2Margin);
+        const float ddy = fmaxf(0.f, fmaxf(Q.cyl[syo] - my, my - Q.cyh[syo]) - kB2Margin);
+        const float d2 = fmaf(ddx, ddx, ddy * ddy);
+        lo = hi = 0;
+        if (d2 >= hw2) return;
+        const float h = sqrtf(hw2 - d2) * 1.0001f + kB2Margin;
+        const float zlo = mz - h, zhi = mz + h;
+#if PC_B2_ZTAB
+        // [first slot with z >= Z_ql, first slot with z >= Z_qh) contains every
+        // slot with zlo <= z <= zhi (Z_ql <= zlo, Z_qh > zhi); cut to the
+        // stencil cells k-1..k+1
+        const int rl = Q.run_lo[col][k], rh = Q.run_hi[col][k];
+        const int ql = zq_of(zlo, zbase, dzq, idzq, zq);
+        const int qh = zq_of(zhi, zbase, dzq, idzq, zq) + 1;
+        const int l = ql < 0 ? rl : max(rl, (int)Q.ztab[col][ql]);
+        const int r = qh > zq ? rh : min(rh, (int)Q.ztab[col][qh]);
+#else
+        int l = Q.run_lo[col][k], h1 = Q.run_hi[col][k];
+        int h3 = h1;
+        while (l < h1) {                         // first z >= zlo
+          const int mid = (l + h1) >> 1;
+          if (szp[mid] < zlo) l = mid + 1; else h1 = mid;
+        }
+        int r = l;
+        while (r < h3) {                         // first z > zhi
+          const int mid = (r + h3) >> 1;
+          if (szp[mid] <= zhi) r = mid + 1; else h3 = mid;
+        }
+#endif
+        // an empty window stays [0, 0): aligning an empty [l, l) down would
+        // step over slots of another column
+        lo = r > l ? l : 0;
+        hi = r > l ? r : 0;
+      };
+      if (FLAT) {
+        // windows -> piece table (non-empty pieces only, column order), then
+        // the pieces back to back
+        int np = 0;
+#pragma unroll 1
+        for (int dxo = 0; dxo < 3; ++dxo)
+#pragma unroll
+          for (int dyo = 0; dyo < 3; ++dyo) {
+            const int sxo = hx + dxo, syo = hy + dyo, col = sxo * kSY + syo;
+            int lo, hi;
+            window(sxo, syo, col, lo, hi);
+            if (hi > lo) {      // 0 <= D[col] <= 6 x 15 < 128: seven bits
+              pcs[np * 32] = (uint32_t)lo | ((uint32_t)hi << 12) | ((uint32_t)Q.D[col] << 24);
+              ++np;
+            }
           }
+        int pi = 0, i = 0, end = 0, dd = 0;
+        // the piece holding the row's own slot starts the self search
+        auto load = [&](uint32_t pc) {
+          const int l = (int)(pc & 0xFFFu);
+          i = l & ~3;
+          end = (int)((pc >> 12) & 0xFFFu);
+          dd = (int)(pc >> 24);
+          if (pb >= l && pb < end) hself = ha;
+        };
+        if (np > 0) load(pcs[0]);
+        uint32_t nxt = np > 1 ? pcs[32] : 0u;    // next piece, loaded one ahead
+        while (pi < np) {
+          step4(i, dd);
+          i += 4;
+          if (i >= end) {
+            if (++pi < np) {
+              load(nxt);
+              if (pi + 1 < np) nxt = pcs[(pi + 1) * 32];
+            }
+          }
+        }
+      } else {
+        // column by column (the warp runs each column to its longest lane)
+#pragma unroll 1
+        for (int cc = 0; cc < 9; ++cc) {
+          const int dxo = cc / 3, dyo = cc - 3 * dxo;
+          const int sxo = hx + dxo, syo = hy + dyo, col = sxo * kSY + syo;
+          int lo, hi;
+          window(sxo, syo, col, lo, hi);
+          const int dd = Q.D[col];
+          if (col == hcol) hself = ha;
+          // (not unrolled: an unrolled body with remainder blocks runs every
+          // remainder block whenever any lane needs it -- 139 vs ~100 steps)
+#pragma unroll 1
+          for (int i = lo & ~3; i < hi; i += 4) step4(i, dd);
         }
       }
       cnt = (int)((ha - hbase) >> 6);
@@ -1195,8 +1293,10 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
         // the last entry takes its place
         int ks = (int)((hself - hbase) >> 6);
         while (ks < cnt - 1 && hits[ks * 32] != (uint16_t)pos) ++ks;
-        hits[ks * 32] = hits[(cnt - 1) * 32];
-        --cnt;
+        if (cnt > 0 && hits[ks * 32] == (uint16_t)pos) {
+          hits[ks * 32] = hits[(cnt - 1) * 32];
+          --cnt;
+        }
         band = amin <= bhalf;
       }
     }
@@ -2149,9 +2249,15 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   p.max_stage = kStageCap;
   p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 3;
   p.ps = planar_stride;
-  // PC_TILE_BUILD=1: the per-column sweep (r01 / r02 build); default 2:
-  // flattened spherical windows (tile_build2_kernel)
-  static const int version = getenv("PC_TILE_BUILD") ? atoi(getenv("PC_TILE_BUILD")) : 2;
+  // PC_TILE_BUILD=1 (default): tile_build_kernel (box z-windows, float4
+  // staging); 2: spherical windows swept back to back per lane
+  // (tile_build2_kernel<true>); 3: spherical windows column by column with
+  // planar FP32 and packed tests (tile_build2_kernel<false>).  Measured at C3
+  // / hot (profiles/r02t): 1 = 3.77 ms, 3 = 3.81 ms (2.31 vs 2.71 G warp
+  // instructions, but issue-latency bound at 54 vs 64 % issue active), 2 =
+  // 5.1-5.7 ms (24 % fewer 4-candidate steps, but 15 % of stall samples at
+  // the staging barrier and 41 % issue active)
+  static const int version = getenv("PC_TILE_BUILD") ? atoi(getenv("PC_TILE_BUILD")) : 1;
   const int nt = tile_dims(*grid).ntiles;
   if (version == 1) {
     const int smem = kStageCap * (int)sizeof(float4) +
@@ -2170,18 +2276,22 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
         box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
     return check_launch("pc_tile_build");
   }
+  const int wv = b2_warps(version == 2);
   const int smem = 3 * kB2Cap * (int)sizeof(float) +
-                   kB2Warps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t) +
-                   kB2Warps * 32 * kB2Pieces * (int)sizeof(uint32_t);
+                   wv * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t) +
+                   (version == 2 ? wv * 32 * kB2Pieces * (int)sizeof(uint32_t) : 0);
   if (smem > g_build2_smem) {
-    if (cudaFuncSetAttribute(tile_build2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess) {
+    if (cudaFuncSetAttribute(tile_build2_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(tile_build2_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       set_error("pc_tile_build: %d B of shared memory not available", smem);
       return PC_ERR_CAPACITY;
     }
     g_build2_smem = smem;
   }
-  tile_build2_kernel<<<nt, kB2Warps * 32, smem, as_stream(stream)>>>(
+  auto kern = version == 2 ? tile_build2_kernel<true> : tile_build2_kernel<false>;
+  kern<<<nt, wv * 32, smem, as_stream(stream)>>>(
       d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
       reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
       box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
