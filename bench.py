@@ -85,7 +85,19 @@ def parse_args():
                          "per-particle SELL list")
     ap.add_argument("--gather", choices=["planar", "pos4"], default="planar",
                     help="SELL force-kernel neighbor gather layout")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: per-step ghost refresh as one NCCL all_to_all_single "
+                         "(default) or direct peer-memory stores between the ranks' "
+                         "processes (dist.P2PTransport: CUDA IPC windows over NVLink)")
     return ap.parse_args()
+
+
+def make_transport(args):
+    """The N-rank transport: None (DistMD's NCCLTransport) or P2PTransport."""
+    if getattr(args, "transport", "nccl") != "p2p":
+        return None
+    from paper_2109_09056_b200.dist import P2PTransport
+    return P2PTransport()
 
 
 def dist_env():
@@ -283,7 +295,7 @@ def run_ours(args):
         from paper_2109_09056_b200.dist import DistMD, rank_dims_for
         dims = rank_dims_for(world)
         cfg.rank_dims = dims
-        drv = DistMD(cfg, cells=gc, local_init=True)
+        drv = DistMD(cfg, cells=gc, local_init=True, transport=make_transport(args))
         eng = drv.engine
     else:
         drv = pc.md.MDDriver(cfg, time_phases=False, planar_gather=args.gather == "planar",
@@ -397,7 +409,7 @@ def run_ours(args):
                       dict(tile=args.path == "tile", half_list=args.list == "half",
                            planar_gather=args.gather == "planar"))
     elif not args.no_e2e:
-        e2e = run_e2e_dist(pc, kw, args.e2e_steps or max(K, 100), gc, world)
+        e2e = run_e2e_dist(pc, kw, args.e2e_steps or max(K, 100), gc, world, args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -426,6 +438,7 @@ def run_ours(args):
                 "config": {"workload": workload, "global_atoms": n_global,
                            "atoms_per_gpu": n_global / world, "rank0_owned_atoms": n_local,
                            "parallelism": f"domain x{world}" if world > 1 else "single domain",
+                           "halo_transport": args.transport if world > 1 else None,
                            "l2": "working set > L2 (Verlet list ~170 B/atom), no flush",
                            "mean_neighbors": kmean},
                 "roofline": roofline, "roofline_step": roofline_step,
@@ -466,7 +479,7 @@ def run_e2e(pc, kw, steps, driver_options=None):
                                         "rows (D2H at the end)"}
 
 
-def run_e2e_dist(pc, kw, steps, cells, world):
+def run_e2e_dist(pc, kw, steps, cells, world, args=None):
     """The N-GPU end-to-end leg through the public multi-GPU API: every rank
     uploads its own block of the lattice from pinned host memory
     (DistMD(state=...)) inside the timed region, runs the steps keeping each
@@ -487,7 +500,7 @@ def run_e2e_dist(pc, kw, steps, cells, world):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    drv = DistMD(cfg, cells=cells, state=(x, v, ids))
+    drv = DistMD(cfg, cells=cells, state=(x, v, ids), transport=make_transport(args))
     hist[0] = drv.engine.local_diagnostics()
     for s in range(1, steps + 1):
         drv.step(s)

@@ -544,6 +544,32 @@ int pc_halo_pack_planar(const double* d_planar, int64_t planar_stride, const int
                         int64_t m, double* d_buf, void* stream);
 int pc_halo_unpack(const double* d_buf, const int32_t* d_rows, int64_t m, double* d_pos,
                    double* d_planar, int64_t planar_stride, void* stream);
+/* Peer-memory halo exchange between processes (CUDA IPC over NVLink): the
+ * per-step refresh / reverse all-to-all of ref decomp.py:231-260 / 263-300
+ * (the exchange `_step` of md.py:192-200 runs every step) without NCCL.
+ * A window = [2 parities x cap rows x width f64][arrive: world i64][ack:
+ * world i64]; step k uses parity k & 1.  _window_alloc: cudaMalloc (zeroed)
+ * + the IPC handle (pc_p2p_handle_bytes() bytes) into h_handle; _open /
+ * _close map / unmap a peer's window.  _put: rows [src0, src0 + count) of
+ * d_send to each destination window's parity block at row dst0 (table of
+ * pc_p2p_dest_bytes()-byte entries {window, src0, count, dst0} in device
+ * memory); _signal: flags[me] = value in each window of such a table
+ * (flag_off in doubles from the window base); _wait: until the own
+ * window's flags[ranks[t]] >= target (spin limit -> *d_err = 1). */
+int pc_p2p_window_bytes(int64_t cap_rows, int32_t width, int32_t world, int64_t* bytes);
+int pc_p2p_window_alloc(int64_t cap_rows, int32_t width, int32_t world, void** d_window,
+                        void* h_handle);
+int pc_p2p_window_free(void* d_window);
+int32_t pc_p2p_handle_bytes(void);
+int32_t pc_p2p_dest_bytes(void);
+int pc_p2p_open(const void* h_handle, void** d_peer);
+int pc_p2p_close(void* d_peer);
+int pc_p2p_put(const double* d_send, const void* d_dests, int32_t n_dst, int64_t max_rows,
+               int32_t width, int64_t cap_rows, int32_t parity, void* stream);
+int pc_p2p_signal(const void* d_dests, int32_t n_dst, int64_t flag_off, int32_t me,
+                  int64_t value, void* stream);
+int pc_p2p_wait(const void* d_window, int64_t flag_off, const int32_t* d_ranks, int32_t n,
+                int64_t target, int32_t* d_err, int64_t spin_limit, void* stream);
 /* dst[idx[k]] += src[k] over rows of w doubles, idx distinct per call
  * (one destination's ghost block of ref decomp.py:281-289). */
 int pc_scatter_add(double* d_dst, const int32_t* d_idx, int64_t m, int32_t w,

@@ -181,6 +181,16 @@ SIGNATURES = {
     "pc_box_wrap": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcBox), c_vp]),
     "pc_box_min_image": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(PcBox), c_vp]),
     "pc_lj_pair": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
+    "pc_p2p_window_bytes": (ctypes.c_int, [c_i64, c_i32, c_i32, ctypes.POINTER(c_i64)]),
+    "pc_p2p_window_alloc": (ctypes.c_int, [c_i64, c_i32, c_i32, ctypes.POINTER(c_vp), c_vp]),
+    "pc_p2p_window_free": (ctypes.c_int, [c_vp]),
+    "pc_p2p_handle_bytes": (c_i32, []),
+    "pc_p2p_dest_bytes": (c_i32, []),
+    "pc_p2p_open": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "pc_p2p_close": (ctypes.c_int, [c_vp]),
+    "pc_p2p_put": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp]),
+    "pc_p2p_signal": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i32, c_i64, c_vp]),
+    "pc_p2p_wait": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_i64, c_vp, c_i64, c_vp]),
 }
 
 _lib = None

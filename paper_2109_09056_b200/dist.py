@@ -1003,6 +1003,8 @@ class FabricMD(_StepLogic):
             e.force(self._dtm, part="boundary")
 
     def diagnostics(self):
+        if self._p2p:
+            self.transport.check_errors()
         if self.deterministic:          # exact per-atom sums, order-independent
             dev = self.engines[0].device
             limbs = torch.zeros(20, dtype=torch.int64, device=dev)
@@ -1122,6 +1124,168 @@ class NCCLTransport:
         return t
 
 
+class _Raw:
+    """A device address where the C-ABI shims expect a tensor (ptr(t))."""
+
+    def __init__(self, addr: int):
+        self.addr = int(addr)
+
+    def data_ptr(self) -> int:
+        return self.addr
+
+
+class P2PTransport(NCCLTransport):
+    """NCCLTransport whose per-step all-to-alls (the ghost refresh of
+    md.py:192-200 / decomp.py:231-260 and the reverse halo of
+    decomp.py:263-300) move rows by direct peer-memory stores between the
+    ranks' processes (CUDA IPC windows, NVLink), with device-side arrival /
+    acknowledgement flags -- no NCCL kernel and no host round trip per step
+    (pc_p2p_*, csrc/pc_p2p.cu).  The rebuild-time exchanges (counts,
+    migrate, halo plan) stay on torch.distributed.
+
+    A channel is prepared collectively after every rebuild with the new
+    split sizes (``prepare``); windows are sized to the largest receive of
+    any rank and re-allocated (all ranks together) only when that grows.
+    Per call k: acknowledge step k - 1's unpack to its sources, wait until
+    every destination acknowledged step k - 2 (parity reuse), store this
+    rank's rows into each destination's parity-(k & 1) block, raise the
+    destinations' arrival flags, wait for every source's step-k flag."""
+
+    SPIN_LIMIT = 1 << 25          # x 200 ns: ~7 s before a wait reports failure
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self._chan = {}
+        self._peer_maps = {}      # (rank, handle bytes) -> mapped address
+
+    # -- collective plan -------------------------------------------------
+    def _allgather_bytes(self, b: bytes):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, b, group=self.group)
+        return out
+
+    def prepare(self, key, send_split, recv_split, width, device):
+        """Collective: every rank calls it with its own split sizes (rows to /
+        from each rank, rank order).  Returns nothing; raises if a previous
+        wait of this channel failed."""
+        lib = _lib.load()
+        torch.cuda.synchronize()
+        ch = self._chan.get(key)
+        if ch is not None:
+            self._check(ch)
+        send = np.asarray(list(send_split), np.int64)
+        rows = self._allgather_bytes(send.tobytes())
+        C = np.stack([np.frombuffer(r, np.int64) for r in rows])      # [src, dst]
+        need = int(C.sum(axis=0).max())
+        me, world = self.rank, self.world
+        if ch is None or ch["cap"] < need or ch["width"] != width:
+            if ch is not None:
+                self.dist.barrier(group=self.group)       # nobody writes the old windows now
+                self._free(ch)
+            cap = int(need * 1.25) + 64
+            win = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(int(lib.pc_p2p_handle_bytes()))
+            _lib.check(lib.pc_p2p_window_alloc(cap, width, world, ctypes.byref(win), h),
+                       "pc_p2p_window_alloc")
+            handles = self._allgather_bytes(h.raw)
+            peers = {}
+            for r in range(world):
+                if r == me:
+                    peers[r] = int(win.value)
+                    continue
+                hb = handles[r]
+                if (r, hb) not in self._peer_maps:
+                    addr = ctypes.c_void_p()
+                    buf = ctypes.create_string_buffer(hb, len(hb))
+                    _lib.check(lib.pc_p2p_open(buf, ctypes.byref(addr)), "pc_p2p_open")
+                    self._peer_maps[(r, hb)] = int(addr.value)
+                peers[r] = self._peer_maps[(r, hb)]
+            ch = {"cap": cap, "width": width, "window": int(win.value), "peers": peers,
+                  "handles": handles, "step": 0,
+                  "err": torch.zeros(1, dtype=torch.int32, device=device)}
+            self._chan[key] = ch
+        cap = ch["cap"]
+        arrive = 2 * cap * width                 # flag regions, in doubles from the base
+        ch["arrive_off"], ch["ack_off"] = arrive, arrive + world
+        src0 = np.concatenate(([0], np.cumsum(C[me])))[:-1]
+        dsts = [d for d in range(world) if C[me, d] > 0]
+        srcs = [s for s in range(world) if C[s, me] > 0]
+        rec = np.dtype([("w", np.uint64), ("src0", np.int64), ("count", np.int64),
+                        ("dst0", np.int64)])
+        assert rec.itemsize == int(lib.pc_p2p_dest_bytes())
+        tabs = []
+        for par in (0, 1):
+            t = np.zeros(len(dsts), rec)
+            for i, d in enumerate(dsts):
+                t[i] = (ch["peers"][d], src0[d], C[me, d], int(C[:me, d].sum()) + par * cap)
+            tabs.append(torch.from_numpy(t.view(np.uint8).copy()).to(device))
+        ack = np.zeros(len(srcs), rec)
+        for i, s in enumerate(srcs):
+            ack[i] = (ch["peers"][s], 0, 0, 0)
+        ch.update(put=tabs, n_dst=len(dsts), max_rows=int(C[me].max()) if world else 0,
+                  ack_tab=torch.from_numpy(ack.view(np.uint8).copy()).to(device),
+                  n_src=len(srcs),
+                  dst_ranks=torch.tensor(dsts, dtype=torch.int32, device=device),
+                  src_ranks=torch.tensor(srcs, dtype=torch.int32, device=device),
+                  recv_rows=int(C[:, me].sum()), send=tuple(send.tolist()),
+                  recv=tuple(int(v) for v in recv_split))
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+
+    def _check(self, ch):
+        if int(ch["err"].item()):
+            raise RuntimeError("P2P halo exchange: a peer flag wait timed out")
+
+    def _free(self, ch):
+        lib = _lib.load()
+        for (r, hb), addr in list(self._peer_maps.items()):
+            if r != self.rank and ch["handles"][r] == hb:
+                _lib.check(lib.pc_p2p_close(ctypes.c_void_p(addr)), "pc_p2p_close")
+                del self._peer_maps[(r, hb)]
+        _lib.check(lib.pc_p2p_window_free(ctypes.c_void_p(ch["window"])), "pc_p2p_window_free")
+
+    # -- per step ----------------------------------------------------------
+    def channel_alltoall(self, key, send):
+        """The prepared channel's all-to-all of ``send`` ((rows, width) f64,
+        destination-rank order, the prepared split sizes): returns the
+        received rows (source-rank order) as a device address in this rank's
+        window, valid until this channel's call after next."""
+        self.channel_send(key, send)
+        return self.channel_recv(key)
+
+    def channel_send(self, key, send):
+        """First half of channel_alltoall: acknowledge, wait for the parity
+        block, store, raise the arrival flags (the stream does not wait for
+        the sources yet -- work enqueued next overlaps their stores)."""
+        ch = self._chan[key]
+        s = stream()
+        ch["step"] += 1
+        k = ch["step"]
+        if k > 1:      # the previous step's rows are unpacked (stream order): acknowledge
+            call("pc_p2p_signal", ptr(ch["ack_tab"]), ch["n_src"], ch["ack_off"], self.rank,
+                 k - 1, s)
+        if k > 2:      # destinations have unpacked step k - 2 (this parity block is free)
+            call("pc_p2p_wait", ctypes.c_void_p(ch["window"]), ch["ack_off"], ptr(ch["dst_ranks"]),
+                 ch["n_dst"], k - 2, ptr(ch["err"]), self.SPIN_LIMIT, s)
+        tab = ch["put"][k & 1]
+        call("pc_p2p_put", ptr(send), ptr(tab), ch["n_dst"], ch["max_rows"], ch["width"],
+             0, 0, s)
+        call("pc_p2p_signal", ptr(tab), ch["n_dst"], ch["arrive_off"], self.rank, k, s)
+
+    def channel_recv(self, key):
+        """Second half: the stream waits for every source's step flag; the
+        received rows' address."""
+        ch = self._chan[key]
+        k = ch["step"]
+        call("pc_p2p_wait", ctypes.c_void_p(ch["window"]), ch["arrive_off"], ptr(ch["src_ranks"]),
+             ch["n_src"], k, ptr(ch["err"]), self.SPIN_LIMIT, stream())
+        return _Raw(ch["window"] + (k & 1) * ch["cap"] * ch["width"] * 8)
+
+    def check_errors(self):
+        for ch in self._chan.values():
+            self._check(ch)
+
+
 def local_block(cfg: MDConfig, cells, rank_dims, rank: int):
     """This rank's block of the fcc lattice (ids = the global lattice order)
     with per-rank seeded velocities, as numpy (x, v, ids): the input of a run
@@ -1203,18 +1367,41 @@ class DistMD(_StepLogic):
     def _engines(self):
         return [self.engine]
 
+    @property
+    def _p2p(self) -> bool:
+        return isinstance(self.transport, P2PTransport)
+
+    def _rebuild_all(self):
+        super()._rebuild_all()
+        if self._p2p:
+            # the per-step channels follow the new halo plan (collective)
+            e = self.engine
+            self.transport.prepare("refresh", e.send_split, e.recv_split, 3, self.device)
+            if e.half:
+                self.transport.prepare("reverse", e.recv_split, e.send_split, 3, self.device)
+
     def _reverse(self):
         """Ghost forces back to their owners: one all-to-all, the transpose of
         the per-step refresh (split sizes swapped)."""
         e = self.engine
         buf = e.reverse_pack()
+        if self._p2p:
+            e.reverse_add(self.transport.channel_alltoall("reverse", buf))
+            return
         e.reverse_add(self.transport.alltoall(buf, e.recv_split, e.send_split, self.device))
 
     def _refresh_overlapped(self):
-        """Pack, start the all-to-all (NCCL stream), interior force on the
-        compute stream meanwhile, then wait, unpack, boundary force."""
+        """Pack, start the all-to-all (NCCL stream; P2P: the stores and
+        flags), interior force on the compute stream meanwhile, then wait,
+        unpack, boundary force."""
         e = self.engine
         buf = e.refresh_pack()
+        if self._p2p:
+            self.transport.channel_send("refresh", buf)
+            e.force(self._dtm, part="interior")
+            e.refresh_unpack(self.transport.channel_recv("refresh"))
+            e.force(self._dtm, part="boundary")
+            return
         work, recv = self.transport.alltoall_async(buf, e.send_split, e.recv_split, self.device)
         e.force(self._dtm, part="interior")
         e.refresh_unpack(work())
@@ -1227,6 +1414,9 @@ class DistMD(_StepLogic):
             # until the next rebuild), one unpack -- a few host calls per step
             # whatever the number of neighbour ranks
             buf = e.refresh_pack()
+            if self._p2p:
+                e.refresh_unpack(self.transport.channel_alltoall("refresh", buf))
+                return
             e.refresh_unpack(self.transport.alltoall(buf, e.send_split, e.recv_split,
                                                       self.device))
             return
@@ -1235,6 +1425,8 @@ class DistMD(_StepLogic):
         getattr(e, in_name)(inbox)
 
     def diagnostics(self):
+        if self._p2p:
+            self.transport.check_errors()
         if self.deterministic:
             # exact integer limbs per rank, summed over ranks (20 int64): the
             # energies equal the single-domain ones bit for bit

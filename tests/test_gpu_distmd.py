@@ -27,22 +27,29 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None, half=False):
+def _worker(rank, world, port, q, steps, det=False, overlap=None, kw=None, half=False,
+            p2p=False, state=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         import paper_2109_09056_b200 as pc
-        from paper_2109_09056_b200.dist import DistMD
-        drv = DistMD(pc.md.MDConfig(**(kw or KW)), deterministic=det, half_list=half)
+        from paper_2109_09056_b200.dist import DistMD, P2PTransport
+        tr = P2PTransport() if p2p else None
+        drv = DistMD(pc.md.MDConfig(**(kw or KW)), deterministic=det, half_list=half,
+                     transport=tr)
         if overlap is not None:
             drv.overlap = overlap
         es = [drv.diagnostics()["E_total"]]
         for s in range(1, steps + 1):
             drv.step(s)
             es.append(drv.diagnostics()["E_total"])
-        if overlap is None:
+        if state:
+            gid, x, v = drv.engine.owned_state()
+            o = np.argsort(gid)
+            q.put((rank, np.array(es), gid[o], x[o], v[o]))
+        elif overlap is None:
             q.put((rank, np.array(es), drv.engine.n_owned))
         else:
             gid, x, v = drv.engine.owned_state()
@@ -189,3 +196,48 @@ def test_distmd_half_list_two_processes():
         assert p.exitcode == 0
     for _, es, _ in out:
         assert np.max(np.abs(es - ref) / np.abs(ref)) < 1e-9
+
+
+def _run(world, **kw):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = dict(kw)
+    steps = args.pop("steps")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, steps), kwargs=args)
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("world,half,overlap", [(2, False, False), (2, False, True),
+                                                 (4, False, False), (2, True, False)])
+def test_distmd_p2p_transport_bitwise(world, half, overlap):
+    """The per-step refresh (and the half list's reverse halo) as direct
+    peer-memory stores between the ranks' processes (P2PTransport: CUDA IPC
+    windows, device-side arrival / acknowledgement flags; here two / four
+    processes on one GPU) gives positions and velocities bitwise equal to the
+    all-to-all transport on every rank, and the same energy series (1e-12),
+    over several rebuilds (rebuild every 5 steps: the channels are re-planned
+    each time); the half list (FP64 atomics on both sides of a pair, not
+    bitwise reproducible run to run) within 1e-10."""
+    kw = dict(KW, lattice_cells=8)
+    res = {}
+    for p2p in (False, True):
+        res[p2p] = _run(world, steps=17, kw=kw, half=half, p2p=p2p, state=True,
+                        overlap=overlap)
+    for a, b in zip(res[False], res[True]):
+        assert np.array_equal(a[2], b[2])
+        if half:
+            # the half list accumulates both sides of a pair with FP64
+            # atomics: not bitwise reproducible between two runs
+            assert np.max(np.abs(a[3] - b[3])) < 1e-10 and np.max(np.abs(a[4] - b[4])) < 1e-9
+            assert np.max(np.abs(a[1] - b[1]) / np.abs(a[1])) < 1e-10
+            continue
+        assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+        assert np.max(np.abs(a[1] - b[1]) / np.abs(a[1])) < 1e-12

@@ -486,6 +486,35 @@ def test_md_engine_forces_vs_oracle(pc, oracle, cells, temp, steps):
     assert abs(d["PE"] - peref.sum()) <= ENERGY_TOL * abs(peref.sum())
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,temp", [(12, 1.44), (16, 3.0)])
+def test_md_engine_virial_vs_oracle(pc, oracle, cells, temp):
+    """The pair virial W = sum over pairs of r.F (tile force kernel: per-row
+    FP32 sums of u = 2 sr12 - sr6, FP64 per-warp partials, one fixed
+    reduction; north_star's "FP64 energy/virial reduction") against the FP64
+    pair sum over the oracle's neighbour pairs on the same positions, and the
+    pressure (2 KE + W) / 3V of the same diagnostics call."""
+    cfg = pc.md.MDConfig(lattice_cells=cells, density=0.8442, temperature=temp, cutoff=2.5,
+                         skin=0.3, rebuild_stride=20, seed=7, steps=0)
+    drv = pc.md.MDDriver(cfg)
+    assert drv.mode == "tile"
+    for s in range(1, 8):
+        drv.step(s)
+    x, _ = drv.gather_state()
+    d = drv.diagnostics()
+    pi, pj = oracle.neighbor_pairs(x, drv.box.low, drv.box.high, [True] * 3, 2.5 * 1.0000001)
+    L = drv.box.lengths
+    dx = x[pj] - x[pi]
+    dx -= L * np.round(dx / L)
+    r2 = np.einsum("ij,ij->i", dx, dx)
+    r2 = r2[r2 < 6.25]
+    sr6 = (1.0 / r2) ** 3
+    w_ref = 0.5 * np.sum(24.0 * (2.0 * sr6 * sr6 - sr6))      # ordered pairs: each twice
+    assert abs(d["virial"] - w_ref) <= 1e-6 * abs(w_ref) + 1e-9 * len(r2)
+    p_ref = (2.0 * d["KE"] + w_ref) / (3.0 * np.prod(L))
+    assert abs(d["pressure"] - p_ref) <= 1e-6 * abs(p_ref) + 1e-12
+
+
 def test_md_engine_empty_tiles(pc, oracle):
     """A lattice at the usual density filling half the box volume (a corner
     cube; the rest vacuum): whole tiles have no rows (28^3 cells: ~5 tiles per
