@@ -268,9 +268,24 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+#ifndef PC_BUILD_PREFETCH
+#define PC_BUILD_PREFETCH 1   // build sweep: next four candidates loaded one step ahead
+#endif
+#ifndef PC_STS_CLOBBER
+#define PC_STS_CLOBBER 0   // 1: "memory" clobber on the hit stores (serialises the candidate steps' loads behind them)
+#endif
+// Hit-list store of the build sweeps.  Without a "memory" clobber the
+// compiler may issue the next step's staging loads before this step's hit
+// stores (different arrays); every sweep ends with compiler_fence() before
+// the hit list is read back.
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+#if PC_STS_CLOBBER
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+#else
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v));
+#endif
 }
+__device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -825,11 +840,33 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
           // running hit offset (a non-hit's store is overwritten by the next
           // hit); one short dependency chain per step instead of per candidate
           int i = s0;
+#if PC_BUILD_PREFETCH
+          // the next step's four candidates are loaded before this step's
+          // tests and hit stores (register double buffer)
+          float4 nq[4];
+          if (i + 4 <= s1) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nq[u] = cz[i + u];
+          }
+#endif
           for (; i + 4 <= s1; i += 4) {
             bool h[4];
+#if PC_BUILD_PREFETCH
+            float4 cq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cq[u] = nq[u];
+            if (i + 8 <= s1) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) nq[u] = cz[i + 4 + u];
+            }
+#endif
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
+#if PC_BUILD_PREFETCH
+              const float4 q = cq[u];
+#else
               const float4 q = cz[i + u];
+#endif
               const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
               const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
               h[u] = rr < p.hi2;
@@ -857,6 +894,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
           }
         }
       }
+      compiler_fence();
       cnt = (int)((ha - hbase) >> 6);
       if (cnt >= kHitCap - 1) cnt = kHitCap;        // (possible) overflow
       nband = mx >= p.lo2 ? 1 : 0;
@@ -1285,6 +1323,7 @@ tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc
           for (int i = lo & ~3; i < hi; i += 4) step4(i, dd);
         }
       }
+      compiler_fence();
       cnt = (int)((ha - hbase) >> 6);
       if (cnt >= kHitCap - 1) {
         cnt = kHitCap;                          // (possible) overflow: flagged below

@@ -1003,8 +1003,6 @@ class FabricMD(_StepLogic):
             e.force(self._dtm, part="boundary")
 
     def diagnostics(self):
-        if self._p2p:
-            self.transport.check_errors()
         if self.deterministic:          # exact per-atom sums, order-independent
             dev = self.engines[0].device
             limbs = torch.zeros(20, dtype=torch.int64, device=dev)

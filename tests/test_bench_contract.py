@@ -63,14 +63,18 @@ def _torchrun(args, env_extra, timeout=600):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scaling", ["strong", "weak"])
-def test_two_rank_line(scaling):
+@pytest.mark.parametrize("scaling,transport", [("strong", "nccl"), ("weak", "nccl"),
+                                               ("strong", "p2p")])
+def test_two_rank_line(scaling, transport):
     """The N-GPU path (torchrun, DistMD, max-over-ranks timing) with two ranks
     sharing one GPU over gloo (PC_BENCH_BACKEND; the driver runs NCCL).
     strong: the 16^3-cell system split over 2x1x1; weak: a 16^3-cell block per
-    rank (32x16x16 global)."""
+    rank (32x16x16 global); p2p: the per-step halo by peer-memory stores
+    (dist.P2PTransport) instead of the all-to-all."""
     d = _torchrun(["--gpus", "2", "--cells", "16", "--steps", "10", "--warmup", "3",
-                   "--scaling", scaling], {"PC_BENCH_BACKEND": "gloo"})
+                   "--scaling", scaling, "--transport", transport],
+                  {"PC_BENCH_BACKEND": "gloo"})
+    assert d["config"]["halo_transport"] == transport
     assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0
     n = 4 * 16 ** 3 * (2 if scaling == "weak" else 1)
     c = d["config"]
