@@ -269,10 +269,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 #ifndef PC_BUILD_PREFETCH
-#define PC_BUILD_PREFETCH 1   // build sweep: next four candidates loaded one step ahead
+#define PC_BUILD_PREFETCH 0   // 1: build sweep loads the next four candidates one step ahead (C3 build + order 6.57 vs 5.59 ms, hot build 4.63 vs 3.76 ms: slower, profiles/r02w)
 #endif
 #ifndef PC_STS_CLOBBER
-#define PC_STS_CLOBBER 0   // 1: "memory" clobber on the hit stores (serialises the candidate steps' loads behind them)
+#define PC_STS_CLOBBER 0   // 1: "memory" clobber on the hit stores (no measurable difference, profiles/r02w)
 #endif
 // Hit-list store of the build sweeps.  Without a "memory" clobber the
 // compiler may issue the next step's staging loads before this step's hit

@@ -511,8 +511,10 @@ def test_md_engine_virial_vs_oracle(pc, oracle, cells, temp):
     sr6 = (1.0 / r2) ** 3
     w_ref = 0.5 * np.sum(24.0 * (2.0 * sr6 * sr6 - sr6))      # ordered pairs: each twice
     assert abs(d["virial"] - w_ref) <= 1e-6 * abs(w_ref) + 1e-9 * len(r2)
+    # P = (2 KE + W) / 3V is a difference of large terms in a hot liquid: its
+    # tolerance is the virial's, carried through
     p_ref = (2.0 * d["KE"] + w_ref) / (3.0 * np.prod(L))
-    assert abs(d["pressure"] - p_ref) <= 1e-6 * abs(p_ref) + 1e-12
+    assert abs(d["pressure"] - p_ref) <= (1e-6 * abs(w_ref) + 1e-9 * len(r2)) / (3.0 * np.prod(L))
 
 
 def test_md_engine_empty_tiles(pc, oracle):
