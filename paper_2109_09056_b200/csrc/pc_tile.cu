@@ -1689,12 +1689,34 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st_rt,
 }
 
 // whole warp: stage tile sequence k of this CTA into buffer b
+#ifndef PC_FORCE_HEADPF
+#define PC_FORCE_HEADPF 0       // list groups (+ the row indices) of the staged tile's row-warps the loader L2-prefetches (0: none); 1 / 2: no gain (C3 force 1060-1062 vs 1059 us, profiles/r02x)
+#endif
 __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ stage, int b,
                                            int k, const int* __restrict__ plan,
-                                           const double* __restrict__ pl, int64_t ps, int lane) {
+                                           const double* __restrict__ pl, int64_t ps, int lane,
+                                           const uint4* __restrict__ list,
+                                           const int* __restrict__ rowidx, int Q8) {
   const int tile = tile_at(F.tiles, F.t0, k);
   const int* gp = plan + (int64_t)tile * kPlanInts;
   const int m = gp[0], S = gp[1];
+#if PC_FORCE_HEADPF
+  {
+    // the warps that take this tile's row-warps start each with a list
+    // group and row-index load from HBM (~1 us); into L2 now, while the
+    // tiles in flight are computed
+    constexpr int L = 4 * PC_FORCE_HEADPF + 1;     // 128-B lines per row-warp
+    const int nrw = gp[2], rw0 = gp[3];
+    for (int t = lane; t < nrw * L; t += 32) {
+      const int w = t / L, part = t - L * w;
+      const int64_t rw = rw0 + w;
+      if (part < L - 1)
+        prefetch_l2(reinterpret_cast<const char*>(list + rw * Q8 * 32) + part * 128);
+      else
+        prefetch_l2(rowidx + rw * 32);
+    }
+  }
+#endif
   double* st = stage + (int64_t)b * 3 * kStageStride;
 #if PC_FORCE_TILEBAR
   uint64_t* bar = &F.tbar[k % kTileBars];
@@ -1791,7 +1813,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       F.loaded = min(K, nbuf);
     }
     __syncwarp();
-    for (int q = 0; q < min(K, nbuf); ++q) force_load(F, stage, q, q, plan, pl, p.ps, lane);
+    for (int q = 0; q < min(K, nbuf); ++q) force_load(F, stage, q, q, plan, pl, p.ps, lane, list, rowidx, p.Q8);
   } else if (warp == 1) {
     for (int q = 0; q < nbuf; ++q)
       if (lane < kNDummy)
@@ -1961,7 +1983,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
         kn = atomicAdd(&F.loaded, 1);
       }
       kn = __shfl_sync(0xffffffffu, kn, 0);
-      if (kn < K) force_load(F, stage, bsel, kn, plan, pl, p.ps, lane);
+      if (kn < K) force_load(F, stage, bsel, kn, plan, pl, p.ps, lane, list, rowidx, p.Q8);
     }
     if (overlap) atomicOr(flag, kFlagOverlap);
     double ke = 0.0, px = 0.0, py = 0.0, pz = 0.0, ped = 0.0;
