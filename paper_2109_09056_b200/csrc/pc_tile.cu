@@ -67,6 +67,9 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_AHEAD
 #define PC_FORCE_AHEAD 0        // 1: L2 prefetch of the list head / row indices of item i + kForceWarps (2: two list groups); C3 force 1157 / 1154 vs 1134 us without (profiles/r02f), off
 #endif
+#ifndef PC_FORCE_PFDIST
+#define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched
+#endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
@@ -1627,7 +1630,7 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
     if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
-    if (PC_FORCE_PREFETCH && gi + 2 < G) prefetch_l2(lp + (gi + 2) * 32);
+    if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int h = 0; h < 4; ++h)
@@ -1667,7 +1670,7 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st_rt,
     if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
     // the group after next into L2 (no register: the list streams from HBM
     // at ~1 us latency, one group of compute ahead is not always enough)
-    if (PC_FORCE_PREFETCH && gi + 2 < G) prefetch_l2(lp + (gi + 2) * 32);
+    if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
