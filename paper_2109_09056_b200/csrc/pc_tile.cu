@@ -68,7 +68,7 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #define PC_FORCE_AHEAD 0        // 1: L2 prefetch of the list head / row indices of item i + kForceWarps (2: two list groups); C3 force 1157 / 1154 vs 1134 us without (profiles/r02f), off
 #endif
 #ifndef PC_FORCE_PFDIST
-#define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched
+#define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
 #endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities

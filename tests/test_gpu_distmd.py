@@ -216,7 +216,8 @@ def _run(world, **kw):
 
 
 @pytest.mark.parametrize("world,half,overlap", [(2, False, False), (2, False, True),
-                                                 (4, False, False), (2, True, False)])
+                                                 (4, False, False), (2, True, False),
+                                                 (8, False, False)])
 def test_distmd_p2p_transport_bitwise(world, half, overlap):
     """The per-step refresh (and the half list's reverse halo) as direct
     peer-memory stores between the ranks' processes (P2PTransport: CUDA IPC
