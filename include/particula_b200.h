@@ -321,6 +321,18 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
                          void* stream, const double* d_bplanar, const pc_box* box_exact,
                          const int32_t* d_skip, int32_t* d_tile_ghost);
+/* pc_tile_build_domain with the round order of pc_tile_order applied inside
+ * the build (order_kind 1: residue round-robin, each row-warp's list read
+ * back from L2 right after it is written -- the same lists as pc_tile_build +
+ * pc_tile_order(kind 1), without the separate pass over HBM; 0: the build's
+ * order).  d_skip / d_bplanar / box_exact / d_tile_ghost nullable as in
+ * pc_tile_build_domain. */
+int pc_tile_build_ordered(const double* d_planar, int64_t planar_stride,
+                          const int32_t* d_cell_start, const pc_grid* grid, const pc_box* box,
+                          double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
+                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
+                          void* stream, const double* d_bplanar, const pc_box* box_exact,
+                          const int32_t* d_skip, int32_t* d_tile_ghost, int32_t order_kind);
 /* Reorder the rounds of every row-warp (after pc_tile_build, same list):
  * residue round-robin per row so that the 16 lanes of a half-warp read 16
  * distinct shared-memory bank pairs in most rounds.  rw_bound >= the total

@@ -152,6 +152,10 @@ SIGNATURES = {
                                             ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp,
                                             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                             ctypes.POINTER(PcBox), c_vp, c_vp]),
+    "pc_tile_build_ordered": (ctypes.c_int, [c_vp, c_i64, c_vp, ctypes.POINTER(PcGrid),
+                                             ctypes.POINTER(PcBox), c_dbl, c_i32, c_vp, c_vp,
+                                             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                             ctypes.POINTER(PcBox), c_vp, c_vp, c_i32]),
     "pc_tile_force": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32,
                                      ctypes.POINTER(PcBox), ctypes.POINTER(PcLJ), c_dbl, c_vp,
                                      c_i64, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp,

@@ -681,6 +681,86 @@ __device__ __forceinline__ int owned_row_slot(const TileSetup& T, const int* __r
   return mine;
 }
 
+// Residue round-robin order of one row-warp's list, in place (the lane's own
+// column of uint4 groups at lp; the list was just written by this warp, so it
+// is read back from L2): the algorithm of tile_order_kernel<true> below with
+// a u16 per-class state (next | end << 8, positions <= kHitCap < 256).
+// st: this warp's [16][32] u16 table + lane; Bm: >= kHitCap + 1 rows of
+// [k][32] u16 + lane (the build's hit buffer, free once the list is out).
+__device__ __forceinline__ void rr_order_rowwarp(uint4* __restrict__ lp, int R,
+                                                 uint16_t* __restrict__ st,
+                                                 uint16_t* __restrict__ Bm, int lane,
+                                                 int dummy0) {
+  const uint32_t dmin = (uint32_t)dummy0 * 8u;
+  const int G = (R + 7) >> 3;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) st[c * 32] = 0;
+  int cnt = 0;                                          // real entries precede padding
+  uint4 qn = lp[0];
+  for (int g = 0; g < G; ++g) {                         // per-class counts
+    const uint4 q = qn;
+    if (g + 1 < G) qn = lp[(g + 1) * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+      const uint32_t real = v < dmin ? 1u : 0u;
+      st[((v >> 3) & 15) * 32] += (uint16_t)real;
+      cnt += (int)real;
+    }
+  }
+  uint32_t run = 0u;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {                        // next | end << 8
+    const uint32_t n = st[c * 32];
+    st[c * 32] = (uint16_t)(run | ((run + n) << 8));
+    run += n;
+  }
+  unsigned ne = 0u;
+  qn = lp[0];
+  for (int g = 0; g < G; ++g) {                         // class-major scatter -> Bm
+    const uint4 q = qn;
+    if (g + 1 < G) qn = lp[(g + 1) * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+      const bool real = v < dmin;
+      const int c = (v >> 3) & 15;
+      const uint32_t e = st[c * 32];
+      st[c * 32] = (uint16_t)(e + (real ? 1u : 0u));
+      ne |= real ? 1u << c : 0u;
+      Bm[(real ? (int)(e & 0xFFu) : kHitCap) * 32] = (uint16_t)v;
+    }
+  }
+  uint32_t beg = 0u;                                    // rewind next to begin(c) = end(c - 1)
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const uint32_t end = (uint32_t)st[c * 32] >> 8;
+    st[c * 32] = (uint16_t)(beg | (end << 8));
+    beg = end;
+  }
+  for (int g = 0; g < G; ++g) {                         // emit 8 rounds per uint4
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = g * 8 + t;
+      const bool real = r < cnt;
+      const int pref = (lane + r) & 15;
+      const unsigned rot = ((ne >> pref) | (ne << (16 - pref))) & 0xFFFFu;
+      const int c = (pref + __ffs(rot) - 1) & 15;
+      const uint32_t e = st[c * 32];
+      const int pos = (int)(e & 0xFFu);
+      st[c * 32] = (uint16_t)(e + (real ? 1u : 0u));
+      if (real && (uint32_t)pos + 1u == (e >> 8)) ne &= ~(1u << c);
+      const uint32_t vb = Bm[(real ? pos : kHitCap) * 32];
+      const uint32_t v = real ? vb : (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+      o[t >> 1] |= (t & 1) ? (v << 16) : v;
+    }
+    lp[g * 32] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // Build.  Particles are z-sorted inside every cell (pc_cell_zsort at the
 // rebuild), so each staged column -- cells in z order, each cell z-sorted --
 // is one z-sorted run of slots, and the home rows of a column are z-sorted
@@ -693,7 +773,14 @@ __device__ __forceinline__ int owned_row_slot(const TileSetup& T, const int* __r
 // (ascending slots).  Candidates outside the FP32 band decide in FP32;
 // inside it the reference's FP64 predicate decides (exact).
 
-__global__ void __launch_bounds__(kBuildWarps * 32, 2)
+// ORD: the residue round-robin order of every row-warp is applied right
+// after its list is written (rr_order_rowwarp, list read back from L2),
+// instead of a separate pc_tile_order pass over HBM; nine warps (the
+// per-warp class table needs the shared memory of the tenth).
+__host__ __device__ constexpr int build_warps(bool ord) { return ord ? 9 : kBuildWarps; }
+
+template <bool ORD>
+__global__ void __launch_bounds__(build_warps(ORD) * 32, 2)
 tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
@@ -756,7 +843,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   int ghost_seen = 0;        // a ghost row among the staged particles (tile_ghost)
   // stage: slot order, one warp per segment (a segment is ~40 particles:
   // all threads walking every segment left 7 of 8 idle)
-  for (int e = threadIdx.x >> 5; e < kSegs; e += kBuildWarps) {
+  for (int e = threadIdx.x >> 5; e < kSegs; e += build_warps(ORD)) {
     const int len = T.seg_len[e];
     if (len == 0) continue;
     const int src = T.seg_src[e], dst = T.seg_dst[e];
@@ -780,7 +867,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   if (tile_ghost && threadIdx.x == 0) tile_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
 
   uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
-  for (int w = warp; w < nrw; w += kBuildWarps) {
+  for (int w = warp; w < nrw; w += build_warps(ORD)) {
     const int u = w * 32 + lane;
     int ocol = 0;
     const int opos = skip ? owned_row_slot(T, skip, w, lane, ocol) : -1;
@@ -947,6 +1034,13 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
       }
     }
     __syncwarp();
+    if (ORD && R > 0 && ((R + 7) & ~7) <= cap) {
+      uint16_t* st = reinterpret_cast<uint16_t*>(
+                         hits_all + build_warps(ORD) * (kHitCap + kHitSlack) * 32) +
+                     warp * 16 * 32 + lane;
+      rr_order_rowwarp(lout, R, st, hits, lane, p.max_stage);
+      __syncwarp();
+    }
   }
 }
 
@@ -2075,6 +2169,127 @@ constexpr int kOrdWarps = 8;
 #endif
 constexpr int kOrdSmem = kOrdWarps * ((kHitCap + 1) * 32 * 2 + 16 * 32 * 4);
 
+// Residue round-robin order, r02 rewrite (PC_TILE_ORDER_IMPL=1 keeps the r01
+// kernel below): the same rounds bit for bit, fewer instructions per entry.
+// Groups of eight rounds that hold only real entries in every lane (below
+// the warp's shortest row) take paths without the real / padding selects;
+// the non-empty-class mask is derived from the counts and kept doubled
+// (bits c and c + 16), so the preferred rotation is one shift.
+__global__ void __launch_bounds__(kOrdWarps * 32, 3)
+tile_order_rr_kernel(uint4* __restrict__ list, const int* __restrict__ rounds,
+                     const int* __restrict__ rw_total, int Q8, int dummy0) {
+  extern __shared__ __align__(16) unsigned char osm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rw = blockIdx.x * kOrdWarps + warp;
+  if (rw >= *rw_total) return;
+  uint32_t* st = reinterpret_cast<uint32_t*>(osm) + warp * 16 * 32 + lane;   // [c][lane]
+  uint16_t* Bm = reinterpret_cast<uint16_t*>(osm + kOrdWarps * 16 * 32 * 4) +
+                 warp * (kHitCap + 1) * 32 + lane;    // [k][lane], row kHitCap: dump
+  const int R = rounds[rw];
+  if (R <= 0 || R > kHitCap) return;
+  uint4* lp = list + (int64_t)rw * Q8 * 32 + lane;
+  const uint32_t dmin = (uint32_t)dummy0 * 8u;
+  const int G = (R + 7) >> 3;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) st[c * 32] = 0u;
+  int cnt = 0;                                          // real entries precede padding
+  // the first read of the list comes from HBM: two groups in flight
+  uint4 qn = lp[0], qn2 = G > 1 ? lp[32] : make_uint4(0u, 0u, 0u, 0u);
+  for (int g = 0; g < G; ++g) {                         // per-class counts
+    const uint4 q = qn;
+    qn = qn2;
+    if (g + 2 < G) qn2 = lp[(g + 2) * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+      const uint32_t real = v < dmin ? 1u : 0u;
+      st[((v >> 3) & 15) * 32] += real;
+      cnt += (int)real;
+    }
+  }
+  const int gfull = __reduce_min_sync(0xffffffffu, cnt) >> 3;   // groups real in every lane
+  uint32_t run = 0u, ne = 0u;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {                        // next | end << 16
+    const uint32_t n = st[c * 32];
+    st[c * 32] = run | ((run + n) << 16);
+    ne |= n ? (1u << c) : 0u;
+    run += n;
+  }
+  qn = lp[0];
+  for (int g = 0; g < G; ++g) {                         // class-major scatter -> Bm
+    const uint4 q = qn;
+    if (g + 1 < G) qn = lp[(g + 1) * 32];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    if (g < gfull) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+        uint32_t* sc = st + ((v >> 3) & 15) * 32;
+        const uint32_t e = *sc;
+        *sc = e + 1u;
+        Bm[(e & 0xFFFFu) * 32] = (uint16_t)v;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t v = (t & 1) ? (w[t >> 1] >> 16) : (w[t >> 1] & 0xFFFFu);
+        const bool real = v < dmin;
+        uint32_t* sc = st + ((v >> 3) & 15) * 32;
+        const uint32_t e = *sc;
+        *sc = e + (real ? 1u : 0u);
+        Bm[(real ? (int)(e & 0xFFFFu) : kHitCap) * 32] = (uint16_t)v;
+      }
+    }
+  }
+  uint32_t beg = 0u;                                    // rewind next to begin(c) = end(c - 1)
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const uint32_t end = st[c * 32] >> 16;
+    st[c * 32] = beg | (end << 16);
+    beg = end;
+  }
+  uint32_t ne2 = ne | (ne << 16);                       // doubled: rotation = one shift
+  for (int g = 0; g < G; ++g) {                         // emit 8 rounds per uint4
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+    const int base = lane + g * 8;
+    if (g < gfull) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        // in round r lane l prefers residue (l + r) % 16, else the next
+        // non-empty one
+        const int pref = (base + t) & 15;
+        const int c = (pref + __ffs(ne2 >> pref) - 1) & 15;
+        uint32_t* sc = st + c * 32;
+        const uint32_t e = *sc;
+        const uint32_t pos = e & 0xFFFFu;
+        *sc = e + 1u;
+        if (pos + 1u == (e >> 16)) ne2 &= ~(0x10001u << c);
+        const uint32_t v = Bm[pos * 32];
+        o[t >> 1] |= (t & 1) ? (v << 16) : v;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int r = g * 8 + t;
+        const bool real = r < cnt;
+        const int pref = (base + t) & 15;
+        const int c = (pref + __ffs(ne2 >> pref) - 1) & 15;
+        uint32_t* sc = st + c * 32;
+        const uint32_t e = *sc;
+        const uint32_t pos = e & 0xFFFFu;
+        *sc = e + (real ? 1u : 0u);
+        if (real && pos + 1u == (e >> 16)) ne2 &= ~(0x10001u << c);
+        const uint32_t vb = Bm[(real ? (int)pos : kHitCap) * 32];
+        const uint32_t v = real ? vb : (uint32_t)(dummy0 + ((lane + r) & 15)) * 8u;
+        o[t >> 1] |= (t & 1) ? (v << 16) : v;
+      }
+    }
+    lp[g * 32] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // RR = false: class-major with the start rotated to the lane's residue (the
 // cheaper variant, simulated 1.9 passes per half-warp).  Per-class state
 // lives in a per-lane shared table st[c][lane] (conflict-free: bank = lane).
@@ -2288,6 +2503,17 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
                          void* stream, const double* d_bplanar, const pc_box* box_exact,
                          const int32_t* d_skip, int32_t* d_tile_ghost) {
+  return pc_tile_build_ordered(d_planar, planar_stride, d_cell_start, grid, box, cutoff2, q8,
+                               d_rw0, d_plan, d_rowidx, d_rounds, d_list, d_flag, stream,
+                               d_bplanar, box_exact, d_skip, d_tile_ghost, 0);
+}
+
+int pc_tile_build_ordered(const double* d_planar, int64_t planar_stride,
+                          const int32_t* d_cell_start, const pc_grid* grid, const pc_box* box,
+                          double cutoff2, int32_t q8, const int32_t* d_rw0, int32_t* d_plan,
+                          int32_t* d_rowidx, int32_t* d_rounds, void* d_list, int32_t* d_flag,
+                          void* stream, const double* d_bplanar, const pc_box* box_exact,
+                          const int32_t* d_skip, int32_t* d_tile_ghost, int32_t order_kind) {
   if (q8 <= 0 || planar_stride % 16) {
     set_error("pc_tile_build: bad list capacity or planar stride");
     return PC_ERR_VALUE;
@@ -2324,21 +2550,33 @@ int pc_tile_build_domain(const double* d_planar, int64_t planar_stride,
   static const int version = getenv("PC_TILE_BUILD") ? atoi(getenv("PC_TILE_BUILD")) : 1;
   const int nt = tile_dims(*grid).ntiles;
   if (version == 1) {
+    // order_kind 1: the residue round-robin order fused into the build
+    // (tile_build_kernel<true>); 0: the build's ascending order
+    const bool ord = order_kind == 1;
+    const int bw = build_warps(ord);
     const int smem = kStageCap * (int)sizeof(float4) +
-                     kBuildWarps * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t);
+                     bw * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t) +
+                     (ord ? bw * 16 * 32 * (int)sizeof(uint16_t) : 0);
     if (smem > g_build_smem) {
-      if (cudaFuncSetAttribute(tile_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem) != cudaSuccess) {
+      if (cudaFuncSetAttribute(tile_build_kernel<false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+          cudaFuncSetAttribute(tile_build_kernel<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         set_error("pc_tile_build: %d B of shared memory not available", smem);
         return PC_ERR_CAPACITY;
       }
       g_build_smem = smem;
     }
-    tile_build_kernel<<<nt, kBuildWarps * 32, smem, as_stream(stream)>>>(
+    auto kern = ord ? tile_build_kernel<true> : tile_build_kernel<false>;
+    kern<<<nt, bw * 32, smem, as_stream(stream)>>>(
         d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
         reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
         box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
     return check_launch("pc_tile_build");
+  }
+  if (order_kind != 0) {
+    set_error("pc_tile_build_ordered: the fused round order needs PC_TILE_BUILD=1");
+    return PC_ERR_VALUE;
   }
   const int wv = b2_warps(version == 2);
   const int smem = 3 * kB2Cap * (int)sizeof(float) +
@@ -2443,6 +2681,8 @@ int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_
     if (cudaFuncSetAttribute(tile_order_kernel<true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
         cudaFuncSetAttribute(tile_order_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(tile_order_rr_kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       set_error("pc_tile_order: %d B of shared memory not available", smem);
       return PC_ERR_CAPACITY;
@@ -2451,7 +2691,11 @@ int pc_tile_order(int32_t rw_bound, const int32_t* d_rw_total, const int32_t* d_
   }
   const int grid = (rw_bound + kOrdWarps - 1) / kOrdWarps;
   uint4* l = reinterpret_cast<uint4*>(d_list);
-  if (kind == 1)
+  static const int impl = getenv("PC_TILE_ORDER_IMPL") ? atoi(getenv("PC_TILE_ORDER_IMPL")) : 2;
+  if (kind == 1 && impl == 2)
+    tile_order_rr_kernel<<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
+        l, d_rounds, d_rw_total, q8, kStageCap);
+  else if (kind == 1)
     tile_order_kernel<true><<<grid, kOrdWarps * 32, smem, as_stream(stream)>>>(
         l, d_rounds, d_rw_total, q8, kStageCap);
   else

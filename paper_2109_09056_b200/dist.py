@@ -38,7 +38,7 @@ from ._lib import call, ptr, stream
 from .decomp import DomainFabric, decompose
 from .geometry import Box
 from .md import MDConfig, _CUTOFF_MARGIN, _lj_params, _PhaseTimer, _tile_order_kind, \
-    fcc_lattice, initial_velocities
+    _TILE_FUSED_ORDER, fcc_lattice, initial_velocities
 
 MIG_W = 7     # migrate row: x, y, z, vx, vy, vz, gid (int64 bits)
 HALO_W = 7    # halo row: x, y, z, gid bits, shift x, y, z
@@ -604,10 +604,12 @@ class DomainEngine:
                                        device=dev)
         self._tghost = torch.empty(max(nt, 1), dtype=torch.int32, device=dev)
         self.build_flag.zero_()
-        call("pc_tile_build_domain", ptr(self.pl), self._ps, ptr(cell_start), g, self._lbox,
+        kind = _tile_order_kind(self.cfg.rebuild_stride)
+        fused = _TILE_FUSED_ORDER and kind == 1
+        call("pc_tile_build_ordered", ptr(self.pl), self._ps, ptr(cell_start), g, self._lbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
              ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s, ptr(self.bpl),
-             self._gbox, ptr(self.is_ghost), ptr(self._tghost))
+             self._gbox, ptr(self.is_ghost), ptr(self._tghost), 1 if fused else 0)
         # no host read of the build flags here: the step's force is launched
         # speculatively on these lists and verify_build checks the flags after
         # it (a failed build -- a neighbourhood beyond the staging area or a
@@ -618,8 +620,9 @@ class DomainEngine:
         # ascending tile order; bounds stay on the device ([0, n_int, nt])
         self._tsplit, bounds = _kernels.stable_partition(self._tghost[:nt], 2)
         self._tbounds = bounds.contiguous()          # (a strided view of the scan)
-        call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds), ptr(self._tlist),
-             self._q8, _tile_order_kind(self.cfg.rebuild_stride), s)
+        if not fused:
+            call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds),
+                 ptr(self._tlist), self._q8, kind, s)
         self.mode = "tile"
         self.used_staged = True
         return True

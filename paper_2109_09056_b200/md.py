@@ -35,17 +35,24 @@ import torch
 
 # round order of the tile lists (PC_TILE_ORDER overrides: 0 off, 1 round-robin, 2 class-major)
 _TILE_ORDER_ENV = os.environ.get("PC_TILE_ORDER")
+# PC_TILE_FUSED=1: the round-robin order applied inside the build
+# (pc_tile_build_ordered) instead of the separate pc_tile_order pass -- the
+# same lists, but slower: C3 build + order 7.32 vs 5.58 ms (nine build warps
+# instead of ten; the order's ALU work does not hide behind the build's
+# latency, profiles/r02aa)
+_TILE_FUSED_ORDER = os.environ.get("PC_TILE_FUSED", "0") == "1"
 
 
 def _tile_order_kind(rebuild_stride: int) -> int:
-    """Round order of the tile lists: residue round-robin (1) pays off when
-    the list is reused for >= 8 steps (pc_tile_order ~256 us per rebuild vs
-    ~32 us per step saved in the force pass at 1M atoms); below that the
-    build's ascending order (0) is faster -- hot config (rebuild 5): 2.81e9 vs
-    2.66e9 atom-steps/s, rebuild 10: 3.54e9 vs 3.60e9."""
+    """Round order of the tile lists: residue round-robin (1) when the list
+    is reused for >= 5 steps, else the build's ascending order (0).  At C3
+    the r02 order pass costs ~1.5 ms per rebuild and saves ~340 us in every
+    force pass (1424 -> 1070 us): hot config (T = 3, rebuild 5) 3.69e9 vs
+    3.64e9 atom-steps/s (profiles/r02ab; with the r01 order pass rebuild 5
+    was a loss, r01k)."""
     if _TILE_ORDER_ENV is not None:
         return int(_TILE_ORDER_ENV)
-    return 1 if rebuild_stride >= 8 else 0
+    return 1 if rebuild_stride >= 5 else 0
 
 from . import _kernels, _lib, aosoa, decomp
 from ._lib import call, ptr, stream
@@ -465,12 +472,17 @@ class MDDriver:
             self._vir_part = torch.zeros((npart, 5), dtype=torch.float64, device=dev)
             self._vir = torch.zeros(5, dtype=torch.float64, device=dev)
         self.build_flag.zero_()
-        call("pc_tile_build", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
+        # bank-conflict-aware round order (lists unchanged as sets): fused into
+        # the build (default) or as the separate pc_tile_order pass
+        kind = _tile_order_kind(self.cfg.rebuild_stride)
+        fused = _TILE_FUSED_ORDER and kind == 1
+        call("pc_tile_build_ordered", ptr(self.pl), self._ps, ptr(cell_start), g, self._pbox,
              self._search2, self._q8, ptr(self._rw0), ptr(self._tplan), ptr(self._rowidx),
-             ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s)
-        # bank-conflict-aware round order (pc_tile_order; lists unchanged as sets)
-        call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds),
-             ptr(self._tlist), self._q8, _tile_order_kind(self.cfg.rebuild_stride), s)
+             ptr(self._rounds), ptr(self._tlist), ptr(self.build_flag), s, None, None, None,
+             None, 1 if fused else 0)
+        if not fused:
+            call("pc_tile_order", bound, ptr(self._rw0[nt:]), ptr(self._rounds),
+                 ptr(self._tlist), self._q8, kind, s)
         self.mode = "tile"
         self._nblk = npart
         self._spec = True

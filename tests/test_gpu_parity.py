@@ -487,6 +487,36 @@ def test_md_engine_forces_vs_oracle(pc, oracle, cells, temp, steps):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cells,temp", [(16, 1.44), (24, 3.0)])
+def test_tile_fused_round_order_equals_order_pass(pc, cells, temp, monkeypatch):
+    """The residue round-robin order applied inside the build
+    (pc_tile_build_ordered, kind 1; the default for rebuild strides >= 8)
+    writes the same list words as the build followed by the separate
+    pc_tile_order pass: same rounds per row-warp, same slots in the same
+    rounds, bit for bit."""
+    import torch
+    cfg = dict(lattice_cells=cells, density=0.8442, temperature=temp, cutoff=2.5, skin=0.3,
+               rebuild_stride=20, seed=11, steps=0)
+    lists = []
+    for fused in (True, False):
+        monkeypatch.setattr(pc.md, "_TILE_FUSED_ORDER", fused)
+        drv = pc.md.MDDriver(pc.md.MDConfig(**cfg))
+        assert drv.mode == "tile" and drv.tile_failures == 0
+        torch.cuda.synchronize()
+        nt = drv._ntiles
+        nrw = int(drv._rw0[nt].item())
+        rounds = drv._rounds[:nrw].cpu().numpy()
+        words = drv._tlist.view(torch.int32)[: nrw * drv._q8 * 128].cpu().numpy()
+        words = words.reshape(nrw, drv._q8, 128)
+        lists.append((rounds, words, drv._rowidx[: nrw * 32].cpu().numpy()))
+    (ra, wa, ia), (rb, wb, ib) = lists
+    assert np.array_equal(ra, rb) and np.array_equal(ia, ib)
+    for rw in range(len(ra)):
+        g = (int(ra[rw]) + 7) // 8
+        assert np.array_equal(wa[rw, :g], wb[rw, :g]), rw
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("cells,temp", [(12, 1.44), (16, 3.0)])
 def test_md_engine_virial_vs_oracle(pc, oracle, cells, temp):
     """The pair virial W = sum over pairs of r.F (tile force kernel: per-row
@@ -608,3 +638,42 @@ def test_md_engine_overlap_raises(pc):
     assert drv.mode == "tile"
     with pytest.raises(FloatingPointError):
         drv.check_errors()
+
+
+_ORDER_HASH = r"""
+import hashlib, sys, numpy as np, torch
+import paper_2109_09056_b200 as pc
+cfg = pc.md.MDConfig(lattice_cells=int(sys.argv[1]), density=0.8442, temperature=float(sys.argv[2]),
+                     cutoff=2.5, skin=0.3, rebuild_stride=20, seed=13, steps=0)
+drv = pc.md.MDDriver(cfg)
+assert drv.mode == "tile"
+torch.cuda.synchronize()
+nt = drv._ntiles
+nrw = int(drv._rw0[nt].item())
+rounds = drv._rounds[:nrw].cpu().numpy()
+words = drv._tlist.view(torch.int32)[: nrw * drv._q8 * 128].cpu().numpy().reshape(nrw, drv._q8, 128)
+h = hashlib.sha256(rounds.tobytes())
+for rw in range(nrw):
+    h.update(words[rw, : (int(rounds[rw]) + 7) // 8].tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,temp", [(16, 1.44), (24, 3.0)])
+def test_tile_order_rewrite_same_rounds(cells, temp):
+    """The r02 round-robin order kernel (tile_order_rr_kernel, default) emits
+    the same list words as the r01 kernel (PC_TILE_ORDER_IMPL=1): one hash
+    over every row-warp's rounds from two processes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for impl in ("1", "2"):
+        env = dict(os.environ, PC_TILE_ORDER_IMPL=impl, PC_TILE_FUSED="0", PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", _ORDER_HASH, str(cells), str(temp)], env=env,
+                           capture_output=True, text=True, timeout=300, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(r.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1]
