@@ -73,7 +73,10 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
-constexpr int kBuildWarps = 10;
+#ifndef PC_BUILD_WARPS
+#define PC_BUILD_WARPS 10       // build warps per CTA (2 CTAs per SM); 8 / 6: build +23 / +36 % (profiles/r02ad)
+#endif
+constexpr int kBuildWarps = PC_BUILD_WARPS;
 constexpr int kHitCap = 112;
 constexpr int kHitSlack = 3;   // spare rows per hit column (unclamped 4-candidate stores)
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
