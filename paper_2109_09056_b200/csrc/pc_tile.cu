@@ -88,8 +88,6 @@ struct TileSetup {
   int seg_src[kSegs];          // even-aligned first index of the copied run
   int seg_len[kSegs];          // copied elements (even, 0 = empty)
   int seg_dst[kSegs];          // first slot
-  int seg_tf[kSegs];           // true particle range [tf, te) of the segment (build v2: pads)
-  int seg_te[kSegs];
   float seg_shift[kSegs][3];   // periodic image (build prefilter only; exact multiples of L in FP64 below)
   int cell_lo[kSCols][kSZ];    // slot range of each staged cell (build only)
   int cell_hi[kSCols][kSZ];
@@ -145,21 +143,17 @@ __device__ void tile_setup(int tile, const pc_grid& g, const pc_box& b,
     } else {
       if (zhi >= nz && b.periodic[2]) { za = zb = 0; shz = 1.f; }
     }
-    int src = 0, len = 0, tf = 0, te = 0;
+    int src = 0, len = 0;
     if (ok && zb >= za) {
       const int base = (gx * ny + gy) * nz;
       const int first = cs[base + za], end = cs[base + zb + 1];
       if (end > first) {
         src = first & ~1;
         len = ((end + 1) & ~1) - src;
-        tf = first;
-        te = end;
       }
     }
     T.seg_src[e] = src;
     T.seg_len[e] = len;
-    T.seg_tf[e] = tf;
-    T.seg_te[e] = te;
     T.seg_shift[e][0] = shx;
     T.seg_shift[e][1] = shy;
     T.seg_shift[e][2] = shz;
@@ -1047,450 +1041,10 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
   }
 }
 
-// ---- build v2: flattened spherical windows, planar FP32, packed tests -------
-// Per row (one lane): the 9 stencil columns' z-windows are cut to the sphere,
-// h_c^2 = rs^2 - (lateral distance from the row to column c)^2, and stored
-// as a per-lane piece table; the lane then sweeps its pieces back to back
-// (no per-column warp-wide maximum: a warp runs the maximum over lanes of the
-// lanes' total window, ~0.64x the candidate steps of the per-column sweep),
-// four candidates per step from planar FP32 copies (three LDS.128) with the
-// displacement and r^2 of two candidates per FADD2/FFMA2.
-//
-// Build layout: every staged column is one contiguous, z-sorted run at a
-// 4-aligned build slot with >= 3 dummy slots (coordinates 1e30) after it, so
-// a 4-candidate step aligned down from a window start or running past its end
-// reads only the same column (outside the window: farther than the search
-// radius by construction) or dummies -- no masks.  Inside a column the run
-// keeps the force kernel's staging layout (its even-alignment pad slots hold
-// x = y = 1e30 and a z that keeps the run sorted), so build slot = force slot
-// + D[column] and hits are stored as force slots directly.  The row's own
-// slot is a hit (r^2 = 0) and is removed after the sweep.
-// warps per CTA: two CTAs per SM in 227 KB (the flat variant also keeps a
-// per-lane piece table)
-__host__ __device__ constexpr int b2_warps(bool flat) { return flat ? 9 : 10; }
-constexpr int kB2Cap = kStageCap + kSCols * 8;
-constexpr int kB2Pieces = 9;
-constexpr float kB2Margin = 1e-4f;   // lateral / z-window slack (FP32 staging error ~1e-6)
-
-#ifndef PC_B2_ZTAB
-#define PC_B2_ZTAB 0     // 1: window bounds from a per-column z index instead of two binary searches (hot config build 4.31 vs 3.81 ms: the index fill is a serial phase between two barriers, profiles/r02t)
-#endif
-constexpr int kZB = 16;  // z-index boundaries per staged cell
-
-struct Build2Tables {
-  int D[kSCols];                  // build slot = force slot + D[col]
-  int cbeg[kSCols], cend[kSCols]; // force-slot range of each staged column
-  int B[kSCols + 1];              // build-slot start of each column run
-  int run_lo[kSCols][kTZ + 1];    // build-slot run of cells k-1..k+1 of column col (k = 1..bz)
-  int run_hi[kSCols][kTZ + 1];
-  float cxl[kSX], cxh[kSX], cyl[kSY], cyh[kSY];   // column extents relative to the tile centre
-#if PC_B2_ZTAB
-  // z index of every column run: boundaries Z_q = zbase + q dzq (kZB per
-  // staged cell, q = 0..zq); ztab[col][q] = first build slot of the run with
-  // z >= Z_q (the run's end if none) -- a window's bounds in two loads
-  uint16_t ztab[kSCols][(kTZ + 2) * kZB + 1];
-  float zbase, dzq, idzq;
-  int zq;
-#endif
-};
-
-// largest q in [-1, zq] with Z_q <= z (Z_q = fmaf(q, dzq, zbase), monotone)
-__device__ __forceinline__ int zq_of(float z, float zbase, float dzq, float idzq, int zq) {
-  int q = (int)floorf((z - zbase) * idzq);
-  q = min(max(q, -1), zq);
-  if (q >= 0 && fmaf((float)q, dzq, zbase) > z) --q;
-  if (q < zq && fmaf((float)(q + 1), dzq, zbase) <= z) ++q;
-  return q;
-}
-
-template <bool FLAT>
-__global__ void __launch_bounds__(b2_warps(FLAT) * 32, 2)
-tile_build2_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_grid g, pc_box b,
-                   TileBuildParams p, const int* __restrict__ rw0, int* __restrict__ plan,
-                   int* __restrict__ rowidx, int* __restrict__ rounds, uint4* __restrict__ list,
-                   int* __restrict__ flag, const double* __restrict__ bpl, pc_box e,
-                   const int* __restrict__ skip, int* __restrict__ tile_ghost) {
-  constexpr int kW = b2_warps(FLAT);
-  extern __shared__ __align__(16) float b2s[];
-  float* __restrict__ sxp = b2s;
-  float* __restrict__ syp = b2s + kB2Cap;
-  float* __restrict__ szp = b2s + 2 * kB2Cap;
-  uint16_t* hits_all = reinterpret_cast<uint16_t*>(b2s + 3 * kB2Cap);
-  uint32_t* pcs_all =
-      reinterpret_cast<uint32_t*>(hits_all + kW * (kHitCap + kHitSlack) * 32);
-  __shared__ TileSetup T;
-  __shared__ Build2Tables Q;
-  tile_setup<true>(blockIdx.x, g, b, cs, T);
-  if (T.S > p.max_stage) {
-    // as tile_build_kernel: flag, keep one empty row-warp (force-pass safety)
-    const int r0 = rw0[blockIdx.x];
-    if (threadIdx.x < 32) rowidx[(int64_t)r0 * 32 + threadIdx.x] = -1;
-    if (threadIdx.x == 0) {
-      atomicOr(flag, kFlagStage);
-      atomicMax(flag + 1, T.S);
-      int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
-      pg[0] = 0;
-      pg[1] = 0;
-      pg[2] = 1;
-      pg[3] = r0;
-      rounds[r0] = 0;
-      if (tile_ghost) tile_ghost[blockIdx.x] = 1;
-    }
-    return;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nrw = skip ? rw0[blockIdx.x + 1] - rw0[blockIdx.x] : max(1, (T.H + 31) >> 5);
-  const int bz = T.bz;
-  if (warp == 0) {                       // compacted plan of this tile (force kernel)
-    int* pg = plan + (int64_t)blockIdx.x * kPlanInts;
-    int base = 0;
-    for (int e0 = 0; e0 < kSegs; e0 += 32) {
-      const int ee = e0 + lane;
-      const bool ne = ee < kSegs && T.seg_len[ee] > 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, ne);
-      if (ne) {
-        const int k = base + __popc(bal & ((1u << lane) - 1u));
-        pg[4 + 3 * k] = T.seg_src[ee];
-        pg[5 + 3 * k] = T.seg_len[ee];
-        pg[6 + 3 * k] = T.seg_dst[ee];
-      }
-      base += __popc(bal);
-    }
-    if (lane == 0) {
-      pg[0] = base;
-      pg[1] = T.S;
-      pg[2] = nrw;
-      pg[3] = rw0[blockIdx.x];
-    }
-  } else if (warp == 1) {                // column runs of the build layout
-    // column c takes align4(len + 3) build slots (>= 3 trailing dummies);
-    // starts by a warp scan
-    static_assert(kSCols <= 32, "one lane per staged column");
-    const int c = lane;
-    int fb = 0, fe = 0;
-    if (c < kSCols) {
-      fb = T.seg_dst[3 * c];
-      fe = T.seg_dst[3 * c + 2] + T.seg_len[3 * c + 2];
-    }
-    const int foot = fe > fb ? (fe - fb + 3 + 3) & ~3 : 0;
-    int inc = foot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    if (c < kSCols) {
-      Q.cbeg[c] = fb;
-      Q.cend[c] = fe;
-      Q.B[c] = inc - foot;
-      Q.D[c] = inc - foot - fb;
-    }
-    if (c == kSCols - 1) Q.B[kSCols] = inc;
-  } else if (warp == 2 && lane < kSX + kSY) {
-    // staged column sxo spans grid column x0 - 1 + sxo: relative to the tile
-    // centre [(sxo - 1 - bx/2) w, (sxo - bx/2) w) (periodic images included)
-    if (lane < kSX) {
-      Q.cxl[lane] = (float)((lane - 1 - 0.5 * T.bx) * g.width[0]);
-      Q.cxh[lane] = (float)((lane - 0.5 * T.bx) * g.width[0]);
-    } else {
-      const int l = lane - kSX;
-      Q.cyl[l] = (float)((l - 1 - 0.5 * T.by) * g.width[1]);
-      Q.cyh[l] = (float)((l - 0.5 * T.by) * g.width[1]);
-    }
-  }
-  __syncthreads();
-  // runs of cells k-1..k+1 per column (non-empty cells of a column are
-  // contiguous in both layouts; the pads between its segments are dummies)
-  for (int t = threadIdx.x; t < kSCols * kTZ; t += blockDim.x) {
-    const int col = t / kTZ, k = 1 + t % kTZ;
-    int lo = 0x7fffffff, hi = -1;
-    if (k <= bz)
-      for (int kk = k - 1; kk <= k + 1; ++kk) {
-        const int l = T.cell_lo[col][kk], h = T.cell_hi[col][kk];
-        if (h > l) {
-          lo = min(lo, l);
-          hi = max(hi, h);
-        }
-      }
-    if (hi < 0) lo = hi = 0;
-    Q.run_lo[col][k] = lo + Q.D[col];
-    Q.run_hi[col][k] = hi + Q.D[col];
-  }
-  const int64_t ps = p.ps;
-  int ghost_seen = 0;
-  // stage: one warp per segment; pads (even-alignment extras of the force
-  // layout) become x = y = 1e30 with the z of the nearest true particle
-  for (int s = warp; s < kSegs; s += kW) {
-    const int len = T.seg_len[s];
-    if (len == 0) continue;
-    const int col = s / 3;
-    const int src = T.seg_src[s], dst = T.seg_dst[s] + Q.D[col];
-    const int tf = T.seg_tf[s], te = T.seg_te[s];
-    const double sx = (double)T.seg_shift[s][0] * b.length[0] - T.ox;
-    const double sy = (double)T.seg_shift[s][1] * b.length[1] - T.oy;
-    const double sz = (double)T.seg_shift[s][2] * b.length[2] - T.oz;
-    for (int t = lane; t < len; t += 32) {
-      const int idx = src + t;
-      const int j = min(max(idx, tf), te - 1);
-      const bool pad = idx != j;
-      const float qx = (float)(bpl[j] + sx), qy = (float)(bpl[ps + j] + sy);
-      szp[dst + t] = (float)(bpl[2 * ps + j] + sz);
-      sxp[dst + t] = pad ? 1e30f : qx;
-      syp[dst + t] = pad ? 1e30f : qy;
-      if (tile_ghost && skip) ghost_seen |= skip[idx];
-    }
-  }
-  if (threadIdx.x < kSCols) {            // dummy gap after each column run
-    const int c = threadIdx.x;
-    for (int t = Q.B[c] + (Q.cend[c] - Q.cbeg[c]); t < Q.B[c + 1]; ++t) {
-      sxp[t] = 1e30f;
-      syp[t] = 1e30f;
-      szp[t] = 1e30f;
-    }
-  }
-  ghost_seen = __syncthreads_or(ghost_seen);
-  if (tile_ghost && threadIdx.x == 0) tile_ghost[blockIdx.x] = ghost_seen ? 1 : 0;
-#if PC_B2_ZTAB
-  const float zbase = (float)((-1.0 - 0.5 * bz) * g.width[2]);
-  const float dzq = (float)(g.width[2] / kZB), idzq = 1.0f / dzq;
-  const int zq = (bz + 2) * kZB;
-  // slot s of a run is the first slot with z >= Z_q for q in (q(z_{s-1}), q(z_s)]
-  for (int c = 0; c < kSCols; ++c) {
-    const int b0 = Q.B[c], len = Q.cend[c] - Q.cbeg[c];
-    for (int t = threadIdx.x; t < len; t += blockDim.x) {
-      const int qs = zq_of(szp[b0 + t], zbase, dzq, idzq, zq);
-      const int qp = t > 0 ? zq_of(szp[b0 + t - 1], zbase, dzq, idzq, zq) : -1;
-      for (int q = qp + 1; q <= qs; ++q) Q.ztab[c][q] = (uint16_t)(b0 + t);
-      if (t == len - 1)
-        for (int q = qs + 1; q <= zq; ++q) Q.ztab[c][q] = (uint16_t)(b0 + len);
-    }
-  }
-  __syncthreads();
-#endif
-
-  const float hi2 = p.hi2;
-  // window sphere (search radius^2 plus slack) and the FP32 band: a hit with
-  // r^2 >= lo2 is decided by the reference's FP64 predicate
-  const float hw2 = hi2 * 1.00002f + kB2Margin;
-  const float bmid = 0.5f * (p.lo2 + hi2), bhalf = 0.5f * (hi2 - p.lo2) * 1.001f;
-  uint16_t* hits = hits_all + warp * (kHitCap + kHitSlack) * 32 + lane;   // [k][lane]
-  uint32_t* pcs = pcs_all + warp * kB2Pieces * 32 + lane;                  // [piece][lane]
-  for (int w = warp; w < nrw; w += kW) {
-    const int u = w * 32 + lane;
-    int ocol = 0;
-    const int opos = skip ? owned_row_slot(T, skip, w, lane, ocol) : -1;
-    const bool act = skip ? opos >= 0 : u < T.H;
-    int cnt = 0, a = -1, pos = -1;
-    bool band = false;
-    float mx = 0.f, my = 0.f, mz = 0.f;
-    if (act) {
-      const uint32_t hbase = smem_u32(hits);
-      const uint32_t hend = hbase + (uint32_t)(kHitCap - 1) * 64u;
-      int c = 0;
-#pragma unroll
-      for (int q = 1; q < kBX * kBY; ++q) c += (u >= T.home_pre[q]) ? 1 : 0;
-      if (skip) c = ocol;
-      const int hx = c / kBY, hy = c - hx * kBY;
-      const int hcol = (hx + 1) * kSY + (hy + 1);
-      pos = skip ? opos : T.cell_lo[hcol][1] + (u - T.home_pre[c]);   // force slot
-      int k = 1;
-      for (int kk = 2; kk <= bz; ++kk) k += (pos >= T.cell_lo[hcol][kk]) ? 1 : 0;
-      a = T.seg_src[hcol * 3 + 1] + (pos - T.seg_dst[hcol * 3 + 1]);
-      const int pb = pos + Q.D[hcol];
-      mx = sxp[pb];
-      my = syp[pb];
-      mz = szp[pb];
-      const f32x2_t nx2 = pk2(-mx, -mx), ny2 = pk2(-my, -my), nz2 = pk2(-mz, -mz);
-      const f32x2_t nb2 = pk2(-bmid, -bmid);
-      float amin = 1e30f;
-      uint32_t ha = hbase, hself = hbase;
-      // four candidates at build slots i..i+3 (4-aligned): displacement and
-      // r^2 two candidates per FADD2 / FFMA2 (fmaf(dz, dz, fmaf(dy, dy, dx*dx))
-      // per candidate, as the band bound assumes); every candidate is stored
-      // at the running hit address, which advances on a hit
-      auto step4 = [&](int i, int dd) {
-        const float4 X = *reinterpret_cast<const float4*>(sxp + i);
-        const float4 Y = *reinterpret_cast<const float4*>(syp + i);
-        const float4 Z = *reinterpret_cast<const float4*>(szp + i);
-        const f32x2_t dx01 = add2(pk2(X.x, X.y), nx2), dx23 = add2(pk2(X.z, X.w), nx2);
-        const f32x2_t dy01 = add2(pk2(Y.x, Y.y), ny2), dy23 = add2(pk2(Y.z, Y.w), ny2);
-        const f32x2_t dz01 = add2(pk2(Z.x, Z.y), nz2), dz23 = add2(pk2(Z.z, Z.w), nz2);
-        const f32x2_t r01 = fma2(dz01, dz01, fma2(dy01, dy01, mul2(dx01, dx01)));
-        const f32x2_t r23 = fma2(dz23, dz23, fma2(dy23, dy23, mul2(dx23, dx23)));
-        float r0, r1, r2, r3, t0, t1, t2, t3;
-        upk2(r01, r0, r1);
-        upk2(r23, r2, r3);
-        upk2(add2(r01, nb2), t0, t1);
-        upk2(add2(r23, nb2), t2, t3);
-        amin = fminf(amin, fminf(fminf(fabsf(t0), fabsf(t1)), fminf(fabsf(t2), fabsf(t3))));
-        const int v = i - dd;                   // force slot of candidate 0
-        const uint32_t o1 = ha + (r0 < hi2 ? 64u : 0u);
-        const uint32_t o2 = o1 + (r1 < hi2 ? 64u : 0u);
-        const uint32_t o3 = o2 + (r2 < hi2 ? 64u : 0u);
-        st_shared_u16(ha, (uint16_t)v);
-        st_shared_u16(o1, (uint16_t)(v + 1));
-        st_shared_u16(o2, (uint16_t)(v + 2));
-        st_shared_u16(o3, (uint16_t)(v + 3));
-        ha = min(o3 + (r3 < hi2 ? 64u : 0u), hend);
-      };
-      // z-window of stencil column (sxo, syo): the sphere's chord at the
-      // row's lateral distance to the column; [lo, hi) in build slots
-      auto window = [&](int sxo, int syo, int col, int& lo, int& hi) {
-        const float ddx = fmaxf(0.f, fmaxf(Q.cxl[sxo] - mx, mx - Q.cxh[sxo]) - kB2Margin);
-        const float ddy = fmaxf(0.f, fmaxf(Q.cyl[syo] - my, my - Q.cyh[syo]) - kB2Margin);
-        const float d2 = fmaf(ddx, ddx, ddy * ddy);
-        lo = hi = 0;
-        if (d2 >= hw2) return;
-        const float h = sqrtf(hw2 - d2) * 1.0001f + kB2Margin;
-        const float zlo = mz - h, zhi = mz + h;
-#if PC_B2_ZTAB
-        // [first slot with z >= Z_ql, first slot with z >= Z_qh) contains every
-        // slot with zlo <= z <= zhi (Z_ql <= zlo, Z_qh > zhi); cut to the
-        // stencil cells k-1..k+1
-        const int rl = Q.run_lo[col][k], rh = Q.run_hi[col][k];
-        const int ql = zq_of(zlo, zbase, dzq, idzq, zq);
-        const int qh = zq_of(zhi, zbase, dzq, idzq, zq) + 1;
-        const int l = ql < 0 ? rl : max(rl, (int)Q.ztab[col][ql]);
-        const int r = qh > zq ? rh : min(rh, (int)Q.ztab[col][qh]);
-#else
-        int l = Q.run_lo[col][k], h1 = Q.run_hi[col][k];
-        int h3 = h1;
-        while (l < h1) {                         // first z >= zlo
-          const int mid = (l + h1) >> 1;
-          if (szp[mid] < zlo) l = mid + 1; else h1 = mid;
-        }
-        int r = l;
-        while (r < h3) {                         // first z > zhi
-          const int mid = (r + h3) >> 1;
-          if (szp[mid] <= zhi) r = mid + 1; else h3 = mid;
-        }
-#endif
-        // an empty window stays [0, 0): aligning an empty [l, l) down would
-        // step over slots of another column
-        lo = r > l ? l : 0;
-        hi = r > l ? r : 0;
-      };
-      if (FLAT) {
-        // windows -> piece table (non-empty pieces only, column order), then
-        // the pieces back to back
-        int np = 0;
-#pragma unroll 1
-        for (int dxo = 0; dxo < 3; ++dxo)
-#pragma unroll
-          for (int dyo = 0; dyo < 3; ++dyo) {
-            const int sxo = hx + dxo, syo = hy + dyo, col = sxo * kSY + syo;
-            int lo, hi;
-            window(sxo, syo, col, lo, hi);
-            if (hi > lo) {      // 0 <= D[col] <= 6 x 15 < 128: seven bits
-              pcs[np * 32] = (uint32_t)lo | ((uint32_t)hi << 12) | ((uint32_t)Q.D[col] << 24);
-              ++np;
-            }
-          }
-        int pi = 0, i = 0, end = 0, dd = 0;
-        // the piece holding the row's own slot starts the self search
-        auto load = [&](uint32_t pc) {
-          const int l = (int)(pc & 0xFFFu);
-          i = l & ~3;
-          end = (int)((pc >> 12) & 0xFFFu);
-          dd = (int)(pc >> 24);
-          if (pb >= l && pb < end) hself = ha;
-        };
-        if (np > 0) load(pcs[0]);
-        uint32_t nxt = np > 1 ? pcs[32] : 0u;    // next piece, loaded one ahead
-        while (pi < np) {
-          step4(i, dd);
-          i += 4;
-          if (i >= end) {
-            if (++pi < np) {
-              load(nxt);
-              if (pi + 1 < np) nxt = pcs[(pi + 1) * 32];
-            }
-          }
-        }
-      } else {
-        // column by column (the warp runs each column to its longest lane)
-#pragma unroll 1
-        for (int cc = 0; cc < 9; ++cc) {
-          const int dxo = cc / 3, dyo = cc - 3 * dxo;
-          const int sxo = hx + dxo, syo = hy + dyo, col = sxo * kSY + syo;
-          int lo, hi;
-          window(sxo, syo, col, lo, hi);
-          const int dd = Q.D[col];
-          if (col == hcol) hself = ha;
-          // (not unrolled: an unrolled body with remainder blocks runs every
-          // remainder block whenever any lane needs it -- 139 vs ~100 steps)
-#pragma unroll 1
-          for (int i = lo & ~3; i < hi; i += 4) step4(i, dd);
-        }
-      }
-      compiler_fence();
-      cnt = (int)((ha - hbase) >> 6);
-      if (cnt >= kHitCap - 1) {
-        cnt = kHitCap;                          // (possible) overflow: flagged below
-      } else {
-        // remove the row's own slot (r^2 = 0, in its home column's piece):
-        // the last entry takes its place
-        int ks = (int)((hself - hbase) >> 6);
-        while (ks < cnt - 1 && hits[ks * 32] != (uint16_t)pos) ++ks;
-        if (cnt > 0 && hits[ks * 32] == (uint16_t)pos) {
-          hits[ks * 32] = hits[(cnt - 1) * 32];
-          --cnt;
-        }
-        band = amin <= bhalf;
-      }
-    }
-    // hits inside the FP32 band: the reference's FP64 predicate decides (rare)
-    if (__any_sync(0xffffffffu, band)) {
-      if (band) {
-        int m = 0;
-        for (int t = 0; t < cnt; ++t) {
-          const int v = hits[t * 32];
-          int col = 0;
-          while (col < kSCols - 1 && !(v >= Q.cbeg[col] && v < Q.cend[col])) ++col;
-          const int q = v + Q.D[col];
-          const float dx = sxp[q] - mx, dy = syp[q] - my, dz = szp[q] - mz;
-          const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          bool keep = rr < p.lo2;
-          if (!keep) {
-            int s = col * 3;
-            while (s < col * 3 + 2 && !(T.seg_len[s] > 0 && v >= T.seg_dst[s] &&
-                                        v < T.seg_dst[s] + T.seg_len[s]))
-              ++s;
-            keep = exact_pair_pl(pl, ps, a, T.seg_src[s] + (v - T.seg_dst[s]), e, p.cutoff2);
-          }
-          if (keep) hits[m++ * 32] = (uint16_t)v;
-        }
-        cnt = m;
-      }
-    }
-    const int rw = rw0[blockIdx.x] + w;
-    rowidx[(int64_t)rw * 32 + lane] = a;
-    const int cmax = __reduce_max_sync(0xffffffffu, cnt);
-    if (cmax >= kHitCap) {
-      if (lane == 0) {
-        atomicOr(flag, kFlagOverflow);
-        atomicMax(flag + 2, 1 << 20);
-        rounds[rw] = 0;
-      }
-      __syncwarp();
-      continue;
-    }
-    __syncwarp();
-    const int cap = 8 * p.Q8;
-    uint4* lout = list + (int64_t)rw * p.Q8 * 32 + lane;
-    const int R = p.sched == 0   ? cm_rows(hits, cnt, lane, p.max_stage, lout, cap)
-                  : p.sched == 4 ? rr_rows(hits, cnt, lane, p.max_stage, lout, cap)
-                                 : plain_rows(hits, cnt, lane, p.max_stage, lout, cap);
-    if (lane == 0) {
-      rounds[rw] = ((R + 7) & ~7) > cap ? 0 : R;
-      if (((R + 7) & ~7) > cap) {
-        atomicOr(flag, kFlagOverflow);
-        atomicMax(flag + 2, R);
-      }
-    }
-    __syncwarp();
-  }
-}
+// (Build variants with per-lane spherical z-windows -- a flat piece sweep and
+// a column-lockstep sweep over planar FP32 copies with packed tests, and a
+// per-column z index -- were measured in r02q-r02t and removed: none beat
+// tile_build_kernel, profiles/r02t; source in git 4ae9a62.)
 
 __global__ void pos_from_planar_kernel(const double* __restrict__ pl, int64_t ps, int n,
                                        double* __restrict__ pos4) {
@@ -2437,7 +1991,7 @@ tile_decode_kernel(const int* __restrict__ plan, int Q8, int max_stage,
 using namespace pc;
 
 namespace {
-int g_build_smem = 0, g_build2_smem = 0, g_force_smem = 0;
+int g_build_smem = 0, g_force_smem = 0;
 }
 
 extern "C" {
@@ -2542,17 +2096,8 @@ int pc_tile_build_ordered(const double* d_planar, int64_t planar_stride,
   p.max_stage = kStageCap;
   p.sched = getenv("PC_TILE_SCHED") ? atoi(getenv("PC_TILE_SCHED")) : 3;
   p.ps = planar_stride;
-  // PC_TILE_BUILD=1 (default): tile_build_kernel (box z-windows, float4
-  // staging); 2: spherical windows swept back to back per lane
-  // (tile_build2_kernel<true>); 3: spherical windows column by column with
-  // planar FP32 and packed tests (tile_build2_kernel<false>).  Measured at C3
-  // / hot (profiles/r02t): 1 = 3.77 ms, 3 = 3.81 ms (2.31 vs 2.71 G warp
-  // instructions, but issue-latency bound at 54 vs 64 % issue active), 2 =
-  // 5.1-5.7 ms (24 % fewer 4-candidate steps, but 15 % of stall samples at
-  // the staging barrier and 41 % issue active)
-  static const int version = getenv("PC_TILE_BUILD") ? atoi(getenv("PC_TILE_BUILD")) : 1;
   const int nt = tile_dims(*grid).ntiles;
-  if (version == 1) {
+  {
     // order_kind 1: the residue round-robin order fused into the build
     // (tile_build_kernel<true>); 0: the build's ascending order
     const bool ord = order_kind == 1;
@@ -2577,30 +2122,6 @@ int pc_tile_build_ordered(const double* d_planar, int64_t planar_stride,
         box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
     return check_launch("pc_tile_build");
   }
-  if (order_kind != 0) {
-    set_error("pc_tile_build_ordered: the fused round order needs PC_TILE_BUILD=1");
-    return PC_ERR_VALUE;
-  }
-  const int wv = b2_warps(version == 2);
-  const int smem = 3 * kB2Cap * (int)sizeof(float) +
-                   wv * 32 * (kHitCap + kHitSlack) * (int)sizeof(uint16_t) +
-                   (version == 2 ? wv * 32 * kB2Pieces * (int)sizeof(uint32_t) : 0);
-  if (smem > g_build2_smem) {
-    if (cudaFuncSetAttribute(tile_build2_kernel<true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-        cudaFuncSetAttribute(tile_build2_kernel<false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
-      set_error("pc_tile_build: %d B of shared memory not available", smem);
-      return PC_ERR_CAPACITY;
-    }
-    g_build2_smem = smem;
-  }
-  auto kern = version == 2 ? tile_build2_kernel<true> : tile_build2_kernel<false>;
-  kern<<<nt, wv * 32, smem, as_stream(stream)>>>(
-      d_planar, d_cell_start, *grid, *box, p, d_rw0, d_plan, d_rowidx, d_rounds,
-      reinterpret_cast<uint4*>(d_list), d_flag, d_bplanar ? d_bplanar : d_planar,
-      box_exact ? *box_exact : *box, d_skip, d_tile_ghost);
-  return check_launch("pc_tile_build");
 }
 
 int pc_tile_force(const double* d_planar, int64_t planar_stride, int32_t ntiles,
