@@ -67,6 +67,12 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_AHEAD
 #define PC_FORCE_AHEAD 0        // 1: L2 prefetch of the list head / row indices of item i + kForceWarps (2: two list groups); C3 force 1157 / 1154 vs 1134 us without (profiles/r02f), off
 #endif
+#ifndef PC_FORCE_MIU
+#define PC_FORCE_MIU 1          // warp-uniform minimum-image axis flags (C3 force 1034 vs 1056 us, C2 169 vs 173 us, profiles/r02ah)
+#endif
+#ifndef PC_FORCE_LIST2
+#define PC_FORCE_LIST2 0        // 1: two list groups in registers ahead (instead of one): spills 36 B, C3 force 1081 vs 1057 us (profiles/r02x)
+#endif
 #ifndef PC_FORCE_PFDIST
 #define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
 #endif
@@ -1278,9 +1284,19 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   const int tail = R & 7;
   f32x2_t su2 = 0ull, s62 = 0ull;   // (+0.0f, +0.0f)
   uint4 nxt = first;
+#if PC_FORCE_LIST2
+  // two list groups in registers ahead of the one in use (the row's list is
+  // allocated for Q8 groups: reading one past the rounds is in bounds)
+  uint4 nxt2 = ld_stream(lp + 32);
+#endif
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
+#if PC_FORCE_LIST2
+    nxt = nxt2;
+    if (gi + 2 < G || (gi + 2 == G && tail)) nxt2 = ld_stream(lp + (gi + 2) * 32);
+#else
     if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
+#endif
     if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -1578,9 +1594,24 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
 #endif
     const char* st = reinterpret_cast<const char*>(stage + (int64_t)bsel * 3 * kStageStride);
 
+#if PC_FORCE_MIU
+    const bool nx = __any_sync(0xffffffffu, act && b.periodic[0] &&
+                               (xi - b.low[0] < p.guard || b.high[0] - xi <= p.guard));
+    const bool ny = __any_sync(0xffffffffu, act && b.periodic[1] &&
+                               (yi - b.low[1] < p.guard || b.high[1] - yi <= p.guard));
+#else
     const bool nx = act && b.periodic[0] && (xi - b.low[0] < p.guard || b.high[0] - xi <= p.guard);
     const bool ny = act && b.periodic[1] && (yi - b.low[1] < p.guard || b.high[1] - yi <= p.guard);
+#endif
+#if PC_FORCE_MIU
+    // warp-uniform axis flags: the minimum image is exact for every pair of a
+    // staged (wrapped) neighbourhood, so lanes away from the face may take it
+    // too, and the per-axis branches of the minimum-image body stay uniform
+    const bool nz = __any_sync(0xffffffffu, act && b.periodic[2] &&
+                               (zi - b.low[2] < p.guard || b.high[2] - zi <= p.guard));
+#else
     const bool nz = act && b.periodic[2] && (zi - b.low[2] < p.guard || b.high[2] - zi <= p.guard);
+#endif
     double fx = 0.0, fy = 0.0, fz = 0.0;
     float su = 0.f, s6 = 0.f;
     bool overlap = false;
