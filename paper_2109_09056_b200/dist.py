@@ -1135,6 +1135,22 @@ class _Raw:
         return self.addr
 
 
+def p2p_plan(C, me: int):
+    """Addressing of one rank's peer-memory all-to-all from the split matrix
+    C[src, dst] (rows src sends to dst): the rank's send buffer holds its
+    rows in destination order, and every receive window holds the rows of
+    all sources in source order (the all_to_all_single layout).  Returns
+    {"puts": [(dst, src0, count, dst0)], "dsts", "srcs"}: the put to dst
+    copies send rows [src0, src0 + count) to window rows [dst0, dst0 + count)."""
+    C = np.asarray(C, np.int64)
+    world = C.shape[0]
+    src0 = np.concatenate(([0], np.cumsum(C[me])))[:-1]
+    dsts = [d for d in range(world) if C[me, d] > 0]
+    srcs = [s for s in range(world) if C[s, me] > 0]
+    puts = [(d, int(src0[d]), int(C[me, d]), int(C[:me, d].sum())) for d in dsts]
+    return {"puts": puts, "dsts": dsts, "srcs": srcs}
+
+
 class P2PTransport(NCCLTransport):
     """NCCLTransport whose per-step all-to-alls (the ghost refresh of
     md.py:192-200 / decomp.py:231-260 and the reverse halo of
@@ -1208,17 +1224,16 @@ class P2PTransport(NCCLTransport):
         cap = ch["cap"]
         arrive = 2 * cap * width                 # flag regions, in doubles from the base
         ch["arrive_off"], ch["ack_off"] = arrive, arrive + world
-        src0 = np.concatenate(([0], np.cumsum(C[me])))[:-1]
-        dsts = [d for d in range(world) if C[me, d] > 0]
-        srcs = [s for s in range(world) if C[s, me] > 0]
+        plan = p2p_plan(C, me)
+        dsts, srcs = plan["dsts"], plan["srcs"]
         rec = np.dtype([("w", np.uint64), ("src0", np.int64), ("count", np.int64),
                         ("dst0", np.int64)])
         assert rec.itemsize == int(lib.pc_p2p_dest_bytes())
         tabs = []
         for par in (0, 1):
             t = np.zeros(len(dsts), rec)
-            for i, d in enumerate(dsts):
-                t[i] = (ch["peers"][d], src0[d], C[me, d], int(C[:me, d].sum()) + par * cap)
+            for i, (d, src0, cnt, dst0) in enumerate(plan["puts"]):
+                t[i] = (ch["peers"][d], src0, cnt, dst0 + par * cap)
             tabs.append(torch.from_numpy(t.view(np.uint8).copy()).to(device))
         ack = np.zeros(len(srcs), rec)
         for i, s in enumerate(srcs):

@@ -127,3 +127,28 @@ def test_local_blocks_tile_the_lattice(dims):
         seen[ids] = True
         assert np.abs(v.mean(axis=0)).max() < 1e-12
     assert seen.all()
+
+
+def test_p2p_plan_matches_all_to_all_layout():
+    """The peer-memory all-to-all's addressing (dist.p2p_plan: each rank's puts
+    from its destination-ordered send rows into every destination's
+    source-ordered window) reproduces all_to_all_single's result for random
+    split matrices, self-sends and empty pairs included (host logic of
+    P2PTransport; the device path is tests/test_gpu_distmd.py)."""
+    import numpy as np
+    from paper_2109_09056_b200.dist import p2p_plan
+    rng = np.random.default_rng(3)
+    for world in (1, 2, 4, 8):
+        for _ in range(5):
+            C = rng.integers(0, 6, (world, world)) * (rng.random((world, world)) < 0.7)
+            send = []
+            for s in range(world):         # row (s, d, k), destination order
+                send.append([(s, d, k) for d in range(world) for k in range(C[s, d])])
+            windows = [[None] * int(C[:, d].sum()) for d in range(world)]
+            for s in range(world):
+                for d, src0, cnt, dst0 in p2p_plan(C, s)["puts"]:
+                    windows[d][dst0:dst0 + cnt] = send[s][src0:src0 + cnt]
+            for d in range(world):
+                want = [(s, d, k) for s in range(world) for k in range(C[s, d])]
+                assert windows[d] == want
+                assert p2p_plan(C, d)["srcs"] == [s for s in range(world) if C[s, d] > 0]
