@@ -225,10 +225,12 @@ def run_reference(args):
         return
     kw = md_kwargs(args, args.cells)
     gc = global_cells(args, world)
-    # size the sample so warmup+steps finish in ~2 minutes of CPU time
+    # size the sample so warmup+steps finish in ~2 minutes of CPU time; at
+    # most 48^3 cells (442k atoms): the port's vectorised pair arrays and its
+    # setup (lattice, first list and force) grow with the sample too
     probe_rate, _, _ = cpu_oracle_rate(kw, 8, 2)
     budget_atoms = probe_rate * 120.0 / max(1, args.steps + args.warmup)
-    cells = max(6, min(gc[0], int((budget_atoms / 4) ** (1 / 3))))
+    cells = max(6, min(gc[0], 48, int((budget_atoms / 4) ** (1 / 3))))
     from oracle import particula_oracle as orc
     cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=args.steps))
     drv = orc.MDOracle(cfg)
