@@ -61,17 +61,8 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_VIRIAL
 #define PC_FORCE_VIRIAL 1       // rows sum u = 2 sr12 - sr6 and sr6: energy + pair virial
 #endif
-#ifndef PC_FORCE_NEXT
-#define PC_FORCE_NEXT 0         // 1: claim items one ahead (next row index loaded, its data L2-prefetched): spills 24 B, C3 force 1252 vs 1138 us (profiles/r02d), off
-#endif
-#ifndef PC_FORCE_AHEAD
-#define PC_FORCE_AHEAD 0        // 1: L2 prefetch of the list head / row indices of item i + kForceWarps (2: two list groups); C3 force 1157 / 1154 vs 1134 us without (profiles/r02f), off
-#endif
 #ifndef PC_FORCE_MIU
 #define PC_FORCE_MIU 1          // warp-uniform minimum-image axis flags (C3 force 1034 vs 1056 us, C2 169 vs 173 us, profiles/r02ah)
-#endif
-#ifndef PC_FORCE_LIST2
-#define PC_FORCE_LIST2 0        // 1: two list groups in registers ahead (instead of one): spills 36 B, C3 force 1081 vs 1057 us (profiles/r02x)
 #endif
 #ifndef PC_FORCE_PFDIST
 #define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
@@ -276,9 +267,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 #ifndef PC_BUILD_MASKTAIL
 #define PC_BUILD_MASKTAIL 1   // a piece's last 1-3 candidates as one masked 4-candidate step (build + order -0.3 %, profiles/r02ak)
-#endif
-#ifndef PC_BUILD_PREFETCH
-#define PC_BUILD_PREFETCH 0   // 1: build sweep loads the next four candidates one step ahead (C3 build + order 6.57 vs 5.59 ms, hot build 4.63 vs 3.76 ms: slower, profiles/r02w)
 #endif
 #ifndef PC_STS_CLOBBER
 #define PC_STS_CLOBBER 0   // 1: "memory" clobber on the hit stores (no measurable difference, profiles/r02w)
@@ -936,33 +924,11 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
           // running hit offset (a non-hit's store is overwritten by the next
           // hit); one short dependency chain per step instead of per candidate
           int i = s0;
-#if PC_BUILD_PREFETCH
-          // the next step's four candidates are loaded before this step's
-          // tests and hit stores (register double buffer)
-          float4 nq[4];
-          if (i + 4 <= s1) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) nq[u] = cz[i + u];
-          }
-#endif
           for (; i + 4 <= s1; i += 4) {
             bool h[4];
-#if PC_BUILD_PREFETCH
-            float4 cq[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cq[u] = nq[u];
-            if (i + 8 <= s1) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) nq[u] = cz[i + 4 + u];
-            }
-#endif
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-#if PC_BUILD_PREFETCH
-              const float4 q = cq[u];
-#else
               const float4 q = cz[i + u];
-#endif
               const float dx = q.x - me.x, dy = q.y - me.y, dz = q.z - me.z;
               const float rr = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
               h[u] = rr < p.hi2;
@@ -1133,9 +1099,6 @@ cell_zsort_kernel(const double* __restrict__ zp, int64_t zs, const int* __restri
 // tile into it, so staging overlaps the compute of the tiles in flight and
 // no warp idles at a tile boundary.
 constexpr int kNBuf = 4;       // max staging buffers (runtime: as many as fit)
-#ifndef PC_FORCE_STATIC_BUF
-#define PC_FORCE_STATIC_BUF 0   // 1: per-buffer code paths (buffer base in the LDS immediate): 1525 vs 1133 us at C3 (i-cache), off
-#endif
 extern __shared__ __align__(16) double pc_force_dyn[];
 
 struct TileForceParams {
@@ -1147,30 +1110,14 @@ struct TileForceParams {
   int64_t ps;
 };
 
-#ifndef PC_FORCE_TILEBAR
-#define PC_FORCE_TILEBAR 0      // 1: waits on a per-tile mbarrier (hardware-suspended try_wait) instead of polling which buffer holds the tile
-#endif
-// Per-tile barriers: tile sequence index k completes phase k / kTileBars of
-// tbar[k % kTileBars] (armed by its loader, completed by its bulk copies);
-// bufof[] names the buffer it was staged into.  A warp holding an item of
-// tile k waits with parity (k / kTileBars) & 1, which is right once tile
-// k - kTileBars has completed: items are claimed in order and at most 4
-// tiles are resident, so tile k - 128 still in flight would need ~90 later
-// tiles fully processed through the other buffers during one bulk copy.
-constexpr int kTileBars = 128;
-#ifndef PC_FORCE_GUARD
-#define PC_FORCE_GUARD 1
-#endif
+// (Measured and removed: per-tile mbarrier waits instead of the
+// buffer poll, claiming items one ahead, L2 prefetch of the next items' list
+// heads, a second list group in registers, per-buffer code paths.)
 struct ForceShared {
-#if PC_FORCE_TILEBAR
-  uint64_t tbar[kTileBars];
-  volatile unsigned char bufof[kTileBars];
-#else
   uint64_t bar[kNBuf];
   volatile int seq[kNBuf];   // tile sequence index held by each buffer (-1: none)
   int par[kNBuf];            // mbarrier parity of the current use
   int uses[kNBuf];
-#endif
   int done[kNBuf];           // finished row-warps of the current tile
   int next_item;
   int loaded;                // tickets: next tile sequence index to load
@@ -1313,19 +1260,9 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   const int tail = R & 7;
   f32x2_t su2 = 0ull, s62 = 0ull;   // (+0.0f, +0.0f)
   uint4 nxt = first;
-#if PC_FORCE_LIST2
-  // two list groups in registers ahead of the one in use (the row's list is
-  // allocated for Q8 groups: reading one past the rounds is in bounds)
-  uint4 nxt2 = ld_stream(lp + 32);
-#endif
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
-#if PC_FORCE_LIST2
-    nxt = nxt2;
-    if (gi + 2 < G || (gi + 2 == G && tail)) nxt2 = ld_stream(lp + (gi + 2) * 32);
-#else
     if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
-#endif
     if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -1388,9 +1325,6 @@ __device__ __forceinline__ void tile_row(const char* __restrict__ st_rt,
 }
 
 // whole warp: stage tile sequence k of this CTA into buffer b
-#ifndef PC_FORCE_HEADPF
-#define PC_FORCE_HEADPF 0       // list groups (+ the row indices) of the staged tile's row-warps the loader L2-prefetches (0: none); 1 / 2: no gain (C3 force 1060-1062 vs 1059 us, profiles/r02x)
-#endif
 __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ stage, int b,
                                            int k, const int* __restrict__ plan,
                                            const double* __restrict__ pl, int64_t ps, int lane,
@@ -1399,34 +1333,7 @@ __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ 
   const int tile = tile_at(F.tiles, F.t0, k);
   const int* gp = plan + (int64_t)tile * kPlanInts;
   const int m = gp[0], S = gp[1];
-#if PC_FORCE_HEADPF
-  {
-    // the warps that take this tile's row-warps start each with a list
-    // group and row-index load from HBM (~1 us); into L2 now, while the
-    // tiles in flight are computed
-    constexpr int L = 4 * PC_FORCE_HEADPF + 1;     // 128-B lines per row-warp
-    const int nrw = gp[2], rw0 = gp[3];
-    for (int t = lane; t < nrw * L; t += 32) {
-      const int w = t / L, part = t - L * w;
-      const int64_t rw = rw0 + w;
-      if (part < L - 1)
-        prefetch_l2(reinterpret_cast<const char*>(list + rw * Q8 * 32) + part * 128);
-      else
-        prefetch_l2(rowidx + rw * 32);
-    }
-  }
-#endif
   double* st = stage + (int64_t)b * 3 * kStageStride;
-#if PC_FORCE_TILEBAR
-  uint64_t* bar = &F.tbar[k % kTileBars];
-  if (lane == 0) {
-    F.done[b] = 0;
-    // the previous use of this barrier (tile k - kTileBars) has completed
-    if (PC_FORCE_GUARD && k >= kTileBars) mbar_wait(bar, (uint32_t)((k / kTileBars) - 1) & 1u);
-    F.bufof[k % kTileBars] = (unsigned char)b;
-    mbar_expect_tx(bar, (uint32_t)S * 24u);     // arrive: release (bufof visible to waiters)
-  }
-#else
   uint64_t* bar = &F.bar[b];
   if (lane == 0) {
     F.done[b] = 0;
@@ -1434,7 +1341,6 @@ __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ 
     F.uses[b] += 1;
     mbar_expect_tx(bar, (uint32_t)S * 24u);
   }
-#endif
   __syncwarp();
   for (int e = lane; e < m; e += 32) {
     const int src = gp[4 + 3 * e], len = gp[5 + 3 * e], dst = gp[6 + 3 * e];
@@ -1442,13 +1348,11 @@ __device__ __forceinline__ void force_load(ForceShared& F, double* __restrict__ 
     for (int a = 0; a < 3; ++a)
       bulk_g2s(st + a * kStageStride + dst, pl + a * ps + src, (uint32_t)len * 8u, bar);
   }
-#if !PC_FORCE_TILEBAR
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
     F.seq[b] = k;
   }
-#endif
 }
 
 template <bool UNIT_SIGMA>
@@ -1500,15 +1404,11 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       F.tiles = tiles;
       F.t0 = t0;
       F.next_item = 0;
-#if PC_FORCE_TILEBAR
-      for (int q = 0; q < kTileBars; ++q) mbar_init(&F.tbar[q], 1);
-#else
       for (int q = 0; q < kNBuf; ++q) {
         F.seq[q] = -1;
         F.uses[q] = 0;
         mbar_init(&F.bar[q], 1);
       }
-#endif
       F.loaded = min(K, nbuf);
     }
     __syncwarp();
@@ -1533,34 +1433,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     k = lo;
     return rwbk[lo] + (i - pre[lo]);
   };
-#if PC_FORCE_NEXT
-  // items are claimed one ahead: the next row-warp's row index is loaded
-  // (and its positions / velocities prefetched into L2) while this one runs
-  int i_next = 0;
-  if (lane == 0) i_next = atomicAdd(&F.next_item, 1);
-  i_next = __shfl_sync(0xffffffffu, i_next, 0);
-  int a_next = -1;
-  if (i_next < items) {
-    int kn;
-    a_next = rowidx[(int64_t)locate(i_next, kn) * 32 + lane];
-  }
-#endif
   for (;;) {
-#if PC_FORCE_NEXT
-    const int i = i_next;
-    if (i >= items) break;
-    if (lane == 0) i_next = atomicAdd(&F.next_item, 1);
-    i_next = __shfl_sync(0xffffffffu, i_next, 0);
-    int k;
-    const int rw = locate(i, k);
-    const int a = a_next;
-    int rw_next = -1;
-    if (i_next < items) {
-      int kn;
-      rw_next = locate(i_next, kn);
-      a_next = rowidx[(int64_t)rw_next * 32 + lane];
-    }
-#else
     int i = 0;
     if (lane == 0) i = atomicAdd(&F.next_item, 1);
     i = __shfl_sync(0xffffffffu, i, 0);
@@ -1568,27 +1441,6 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     int k;
     const int rw = locate(i, k);
     const int a = rowidx[(int64_t)rw * 32 + lane];
-#endif
-#if PC_FORCE_AHEAD
-    // the item this warp will most likely take next is ~one item per warp
-    // later (items are claimed in order by kForceWarps warps): its list
-    // head, row indices and round count into L2 now, a full row-warp time
-    // ahead (the first list group of a row-warp otherwise waits on HBM)
-    {
-      const int ia = i + kForceWarps;
-      if (ia < items) {
-        int ka;
-        const int rwa = locate(ia, ka);
-        const uint4* lpa = list + (int64_t)rwa * p.Q8 * 32 + lane;
-        prefetch_l2(lpa);
-        if (PC_FORCE_AHEAD > 1) prefetch_l2(lpa + 32);
-        if (lane == 0) {
-          prefetch_l2(rowidx + (int64_t)rwa * 32);
-          prefetch_l2(rounds + rwa);
-        }
-      }
-    }
-#endif
     // prefetch everything that does not depend on the staged tile
     const int R = rounds[rw];
     const uint4* lp = list + (int64_t)rw * p.Q8 * 32 + lane;
@@ -1606,10 +1458,6 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
       }
     }
     // buffer holding tile k (loaded in ticket order; spin until published)
-#if PC_FORCE_TILEBAR
-    mbar_wait(&F.tbar[k % kTileBars], (uint32_t)(k / kTileBars) & 1u);
-    const int bsel = F.bufof[k % kTileBars];
-#else
     int bsel = -1;
     for (;;) {
 #pragma unroll
@@ -1620,7 +1468,6 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     }
     __threadfence_block();
     mbar_wait(&F.bar[bsel], (uint32_t)F.par[bsel]);
-#endif
     const char* st = reinterpret_cast<const char*>(stage + (int64_t)bsel * 3 * kStageStride);
 
 #if PC_FORCE_MIU
@@ -1657,33 +1504,8 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
   else                                                                                        \
     PC_ROWFN<false, UNIT_SIGMA, BB>(st, lp, first, R, xi, yi, zi, nx, ny, nz, b, p, fx, fy,   \
                                     fz, su, s6, overlap);
-#if PC_FORCE_STATIC_BUF
-    static_assert(kNBuf == 4, "one code path per staging buffer");
-    switch (bsel) {
-      case 0: PC_ROW(0) break;
-      case 1: PC_ROW(1) break;
-      case 2: PC_ROW(2) break;
-      default: PC_ROW(3) break;
-    }
-#else
     PC_ROW(-1)
-#endif
 #undef PC_ROW
-#if PC_FORCE_NEXT
-    if (rw_next >= 0) {      // next row-warp's positions, velocities, first list word -> L2
-      if (a_next >= 0) {
-        prefetch_l2(pl + a_next);
-        prefetch_l2(pl + p.ps + a_next);
-        prefetch_l2(pl + 2 * p.ps + a_next);
-        if (v) {
-          prefetch_l2(v + a_next);
-          prefetch_l2(v + vs + a_next);
-          prefetch_l2(v + 2 * vs + a_next);
-        }
-      }
-      prefetch_l2(list + (int64_t)rw_next * p.Q8 * 32 + lane);
-    }
-#endif
     // release the buffer when this was the tile's last row-warp; refill it
     int last = 0;
     if (lane == 0) last = atomicAdd(&F.done[bsel], 1) + 1 == pre[k + 1] - pre[k];
@@ -1691,9 +1513,7 @@ tile_force_kernel(const double* __restrict__ pl, TileForceParams p, int ntiles,
     if (last) {
       int kn = 0;
       if (lane == 0) {
-#if !PC_FORCE_TILEBAR
         F.seq[bsel] = -1;
-#endif
         kn = atomicAdd(&F.loaded, 1);
       }
       kn = __shfl_sync(0xffffffffu, kn, 0);
