@@ -148,6 +148,17 @@ def static_traffic():
     return float(d["bytes_per_launch_per_atom"]), d.get("source", p)
 
 
+def static_build_capture():
+    """ncu warp instructions and DRAM bytes per atom of one rebuild's build +
+    order kernels (profiles/build_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "build_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def static_inst_per_atom():
     """ncu warp instructions per atom of one force launch (same capture)."""
     d, _ = _force_capture()
@@ -399,6 +410,19 @@ def run_ours(args):
                           "bytes_per_atom": bb, "bytes_model": "SURVEY §8(d) K4/5: 24 + 4k + 8",
                           "avg_launch_us": build_ms * 1e3,
                           "rebuild_us": rebuild_ms * 1e3, "rebuilds": len(rb)}
+        bc = static_build_capture()
+        if bc is not None and mode == "tile":
+            # like the force kernel, the build is not HBM bound: its issue
+            # roofline from the committed ncu instruction count
+            sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+            peak_i = _sm_count() * 4 * sm_clk
+            ach_i = bc["warp_instructions_per_atom"] * n_local / (build_ms * 1e-3)
+            roofline_build["issue"] = {
+                "achieved_warp_inst_per_s": ach_i, "peak_warp_inst_per_s": peak_i,
+                "frac": ach_i / peak_i,
+                "traffic_bytes_per_atom": bc["dram_bytes_per_atom"],
+                "source": "static: ncu smsp__inst_executed.sum of the build + order kernels "
+                          "per atom (profiles/build_traffic.json) x atoms / live build time"}
 
     # the device leg's engine goes back to PyTorch's caching allocator, so the
     # end-to-end leg (a fresh engine through the public API) allocates from a
