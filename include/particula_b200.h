@@ -580,6 +580,12 @@ int pc_p2p_put(const double* d_send, const void* d_dests, int32_t n_dst, int64_t
                int32_t width, int64_t cap_rows, int32_t parity, void* stream);
 int pc_p2p_signal(const void* d_dests, int32_t n_dst, int64_t flag_off, int32_t me,
                   int64_t value, void* stream);
+/* The refresh's pack fused into the put: exported row
+ * d_rows[src0 + k] of the planar x|y|z positions straight into each
+ * destination window (width 3), no send buffer. */
+int pc_p2p_pack_put(const double* d_planar, int64_t planar_stride, const int32_t* d_rows,
+                    const void* d_dests, int32_t n_dst, int64_t max_rows, int64_t cap_rows,
+                    int32_t parity, void* stream);
 int pc_p2p_wait(const void* d_window, int64_t flag_off, const int32_t* d_ranks, int32_t n,
                 int64_t target, int32_t* d_err, int64_t spin_limit, void* stream);
 /* dst[idx[k]] += src[k] over rows of w doubles, idx distinct per call

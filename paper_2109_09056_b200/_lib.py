@@ -194,6 +194,8 @@ SIGNATURES = {
     "pc_p2p_close": (ctypes.c_int, [c_vp]),
     "pc_p2p_put": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp]),
     "pc_p2p_signal": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i32, c_i64, c_vp]),
+    "pc_p2p_pack_put": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i32, c_i64, c_i64, c_i32,
+                                       c_vp]),
     "pc_p2p_wait": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i32, c_i64, c_vp, c_i64, c_vp]),
 }
 

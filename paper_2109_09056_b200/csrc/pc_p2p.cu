@@ -62,6 +62,24 @@ __global__ void p2p_put_kernel(const double* __restrict__ send, const P2PDest* _
   __threadfence_system();
 }
 
+// K11: the refresh's pack fused into the put -- exported row k of
+// destination D is gathered from the planar positions and stored straight
+// into D's window (no send buffer)
+__global__ void p2p_pack_put_kernel(const double* __restrict__ pl, int64_t ps,
+                                    const int* __restrict__ rows,
+                                    const P2PDest* __restrict__ dst, int64_t cap, int parity) {
+  const P2PDest D = dst[blockIdx.y];
+  double* out = D.window + ((int64_t)parity * cap + D.dst0) * 3;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < D.count;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[D.src0 + k];
+    out[3 * k] = pl[r];
+    out[3 * k + 1] = pl[ps + r];
+    out[3 * k + 2] = pl[2 * ps + r];
+  }
+  __threadfence_system();
+}
+
 // flag[me] = value in each window of the table (arrive or ack region)
 __global__ void p2p_signal_kernel(const P2PDest* __restrict__ dst, int n, int64_t flag_off,
                                   int me, long long value) {
@@ -176,6 +194,20 @@ int pc_p2p_put(const double* d_send, const void* d_dests, int32_t n_dst, int64_t
   p2p_put_kernel<<<dim3(bx, (unsigned)n_dst), 256, 0, as_stream(stream)>>>(
       d_send, static_cast<const P2PDest*>(d_dests), width, cap_rows, parity & 1);
   return check_launch("pc_p2p_put");
+}
+
+// Fused pack + put of the ghost refresh: rows[src0 + k] of the planar x|y|z
+// positions to each destination window's parity block (width 3).
+int pc_p2p_pack_put(const double* d_planar, int64_t planar_stride, const int32_t* d_rows,
+                    const void* d_dests, int32_t n_dst, int64_t max_rows, int64_t cap_rows,
+                    int32_t parity, void* stream) {
+  if (n_dst <= 0 || max_rows <= 0) return PC_OK;
+  unsigned bx = (unsigned)((max_rows + 255) / 256);
+  if (bx > 1184) bx = 1184;
+  p2p_pack_put_kernel<<<dim3(bx, (unsigned)n_dst), 256, 0, as_stream(stream)>>>(
+      d_planar, planar_stride, d_rows, static_cast<const P2PDest*>(d_dests), cap_rows,
+      parity & 1);
+  return check_launch("pc_p2p_pack_put");
 }
 
 // flags[me] = value in every window of the table (flag_off: the arrive or

@@ -1269,10 +1269,13 @@ class P2PTransport(NCCLTransport):
         self.channel_send(key, send)
         return self.channel_recv(key)
 
-    def channel_send(self, key, send):
+    def channel_send(self, key, send, rows=None, planar=None):
         """First half of channel_alltoall: acknowledge, wait for the parity
         block, store, raise the arrival flags (the stream does not wait for
-        the sources yet -- work enqueued next overlaps their stores)."""
+        the sources yet -- work enqueued next overlaps their stores).  With
+        `rows` and `planar` = (tensor, stride) instead of `send`: the rows'
+        x, y, z are gathered from the planar positions inside the put
+        (pc_p2p_pack_put, the fused pack of SURVEY §8 K11)."""
         ch = self._chan[key]
         s = stream()
         ch["step"] += 1
@@ -1284,8 +1287,12 @@ class P2PTransport(NCCLTransport):
             call("pc_p2p_wait", ctypes.c_void_p(ch["window"]), ch["ack_off"], ptr(ch["dst_ranks"]),
                  ch["n_dst"], k - 2, ptr(ch["err"]), self.SPIN_LIMIT, s)
         tab = ch["put"][k & 1]
-        call("pc_p2p_put", ptr(send), ptr(tab), ch["n_dst"], ch["max_rows"], ch["width"],
-             0, 0, s)
+        if rows is not None:
+            call("pc_p2p_pack_put", ptr(planar[0]), planar[1], ptr(rows), ptr(tab), ch["n_dst"],
+                 ch["max_rows"], 0, 0, s)
+        else:
+            call("pc_p2p_put", ptr(send), ptr(tab), ch["n_dst"], ch["max_rows"], ch["width"],
+                 0, 0, s)
         call("pc_p2p_signal", ptr(tab), ch["n_dst"], ch["arrive_off"], self.rank, k, s)
 
     def channel_recv(self, key):
@@ -1396,6 +1403,17 @@ class DistMD(_StepLogic):
             if e.half:
                 self.transport.prepare("reverse", e.recv_split, e.send_split, 3, self.device)
 
+    def _p2p_refresh_send(self):
+        """Refresh over the peer-memory channel: the exported rows' x, y, z
+        gathered from the planar positions inside the put (fused pack), or
+        packed first when the engine has no planar copy."""
+        e = self.engine
+        if e.pl is not None:
+            self.transport.channel_send("refresh", None, rows=e.export_all,
+                                        planar=(e.pl, e._ps))
+        else:
+            self.transport.channel_send("refresh", e.refresh_pack())
+
     def _reverse(self):
         """Ghost forces back to their owners: one all-to-all, the transpose of
         the per-step refresh (split sizes swapped)."""
@@ -1411,13 +1429,13 @@ class DistMD(_StepLogic):
         flags), interior force on the compute stream meanwhile, then wait,
         unpack, boundary force."""
         e = self.engine
-        buf = e.refresh_pack()
         if self._p2p:
-            self.transport.channel_send("refresh", buf)
+            self._p2p_refresh_send()
             e.force(self._dtm, part="interior")
             e.refresh_unpack(self.transport.channel_recv("refresh"))
             e.force(self._dtm, part="boundary")
             return
+        buf = e.refresh_pack()
         work, recv = self.transport.alltoall_async(buf, e.send_split, e.recv_split, self.device)
         e.force(self._dtm, part="interior")
         e.refresh_unpack(work())
@@ -1429,10 +1447,11 @@ class DistMD(_StepLogic):
             # per step: one pack, one all-to-all (sizes fixed by the halo plan
             # until the next rebuild), one unpack -- a few host calls per step
             # whatever the number of neighbour ranks
-            buf = e.refresh_pack()
             if self._p2p:
-                e.refresh_unpack(self.transport.channel_alltoall("refresh", buf))
+                self._p2p_refresh_send()
+                e.refresh_unpack(self.transport.channel_recv("refresh"))
                 return
+            buf = e.refresh_pack()
             e.refresh_unpack(self.transport.alltoall(buf, e.send_split, e.recv_split,
                                                       self.device))
             return
