@@ -265,6 +265,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+#ifndef PC_BUILD_POPC
+#define PC_BUILD_POPC 1   // 4-candidate step: hit-row offsets from the hit mask's popcounts
+#endif
 #ifndef PC_BUILD_JOINTSEARCH
 #define PC_BUILD_JOINTSEARCH 1   // a column window's two bisections in one loop (C3 build + order 5.25 vs 5.35 ms, profiles/r02ap)
 #endif
@@ -954,6 +957,20 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
             }
             // absolute shared addresses; one clamp per step (the column's
             // kHitSlack spare rows take o1..o3 past the last row)
+#if PC_BUILD_POPC
+            // offsets from the step's hit mask: the loop-carried chain
+            // through ha is one add and a clamp instead of four adds
+            const uint32_t hm = (h[0] ? 1u : 0u) | (h[1] ? 2u : 0u) | (h[2] ? 4u : 0u) |
+                                (h[3] ? 8u : 0u);
+            const uint32_t o1 = ha + ((hm & 1u) << 6);
+            const uint32_t o2 = ha + ((uint32_t)__popc(hm & 3u) << 6);
+            const uint32_t o3 = ha + ((uint32_t)__popc(hm & 7u) << 6);
+            st_shared_u16(ha, (uint16_t)i);
+            st_shared_u16(o1, (uint16_t)(i + 1));
+            st_shared_u16(o2, (uint16_t)(i + 2));
+            st_shared_u16(o3, (uint16_t)(i + 3));
+            ha = min(ha + ((uint32_t)__popc(hm) << 6), hend);
+#else
             const uint32_t o1 = ha + (h[0] ? 64u : 0u);
             const uint32_t o2 = o1 + (h[1] ? 64u : 0u);
             const uint32_t o3 = o2 + (h[2] ? 64u : 0u);
@@ -962,6 +979,7 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
             st_shared_u16(o2, (uint16_t)(i + 2));
             st_shared_u16(o3, (uint16_t)(i + 3));
             ha = min(o3 + (h[3] ? 64u : 0u), hend);
+#endif
           }
 #if PC_BUILD_MASKTAIL
           if (i < s1) {
