@@ -67,6 +67,9 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_PFDIST
 #define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
 #endif
+#ifndef PC_FORCE_L1PF
+#define PC_FORCE_L1PF 0         // >0: list group gi + L1PF prefetched into L1 and the next group's load may hit L1
+#endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
@@ -265,9 +268,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-#ifndef PC_BUILD_POPC
-#define PC_BUILD_POPC 1   // 4-candidate step: hit-row offsets from the hit mask's popcounts
-#endif
 #ifndef PC_BUILD_JOINTSEARCH
 #define PC_BUILD_JOINTSEARCH 1   // a column window's two bisections in one loop (C3 build + order 5.25 vs 5.35 ms, profiles/r02ap)
 #endif
@@ -333,6 +333,23 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// next list group: from L1 when it was prefetched there (PC_FORCE_L1PF)
+__device__ __forceinline__ uint4 ld_group(const uint4* p) {
+#if PC_FORCE_L1PF
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+#else
+  return ld_stream(p);
+#endif
 }
 
 // ---- two pairs per call: the FP32 LJ magnitude as packed f32x2 ------------
@@ -957,20 +974,6 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
             }
             // absolute shared addresses; one clamp per step (the column's
             // kHitSlack spare rows take o1..o3 past the last row)
-#if PC_BUILD_POPC
-            // offsets from the step's hit mask: the loop-carried chain
-            // through ha is one add and a clamp instead of four adds
-            const uint32_t hm = (h[0] ? 1u : 0u) | (h[1] ? 2u : 0u) | (h[2] ? 4u : 0u) |
-                                (h[3] ? 8u : 0u);
-            const uint32_t o1 = ha + ((hm & 1u) << 6);
-            const uint32_t o2 = ha + ((uint32_t)__popc(hm & 3u) << 6);
-            const uint32_t o3 = ha + ((uint32_t)__popc(hm & 7u) << 6);
-            st_shared_u16(ha, (uint16_t)i);
-            st_shared_u16(o1, (uint16_t)(i + 1));
-            st_shared_u16(o2, (uint16_t)(i + 2));
-            st_shared_u16(o3, (uint16_t)(i + 3));
-            ha = min(ha + ((uint32_t)__popc(hm) << 6), hend);
-#else
             const uint32_t o1 = ha + (h[0] ? 64u : 0u);
             const uint32_t o2 = o1 + (h[1] ? 64u : 0u);
             const uint32_t o3 = o2 + (h[2] ? 64u : 0u);
@@ -979,7 +982,6 @@ tile_build_kernel(const double* __restrict__ pl, const int* __restrict__ cs, pc_
             st_shared_u16(o2, (uint16_t)(i + 2));
             st_shared_u16(o3, (uint16_t)(i + 3));
             ha = min(o3 + (h[3] ? 64u : 0u), hend);
-#endif
           }
 #if PC_BUILD_MASKTAIL
           if (i < s1) {
@@ -1298,7 +1300,8 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   uint4 nxt = first;
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
-    if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
+    if (gi + 1 < G || tail) nxt = ld_group(lp + (gi + 1) * 32);
+    if (PC_FORCE_L1PF && gi + PC_FORCE_L1PF < G + (tail ? 1 : 0)) prefetch_l1(lp + (gi + PC_FORCE_L1PF) * 32);
     if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll

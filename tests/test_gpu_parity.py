@@ -393,6 +393,33 @@ def test_md_verlet_list_bit_exact(pc, oracle, cells, temp):
         assert drv.mode == "tile"
 
 
+@pytest.mark.parametrize("noise", [0.0, 1e-7])
+def test_md_tile_list_pairs_at_search_radius(pc, oracle, noise):
+    """fcc lattice whose fifth neighbour shell lies AT the search radius
+    (a = 2.8 / sqrt(5/2)): 24 pairs per atom sit inside the tile build's FP32
+    band, where the reference's FP64 predicate decides, on both sides of it
+    with the noise.  The tile list equals the oracle's, bit-exact."""
+    cells = 16
+    a = 2.8 / np.sqrt(2.5)
+    x = pc.md.fcc_lattice(cells, a)
+    L = cells * a
+    x = np.mod(x + np.random.default_rng(5).normal(0.0, noise, x.shape), L) if noise else x
+    v = np.zeros_like(x)
+    cfg = pc.md.MDConfig(lattice_cells=cells, density=4.0 / a ** 3, temperature=1.0,
+                         cutoff=2.5, skin=0.3, rebuild_stride=20, seed=3, steps=0)
+    drv = pc.md.MDDriver(cfg, state=(x, v), tile=True)
+    assert drv.mode == "tile"
+    xs, _ = drv.gather_state()
+    counts, offsets, idx = drv.verlet_sets()
+    ref = oracle.build_verlet(xs, drv.box.low, drv.box.high, [True] * 3, drv.search)
+    assert np.array_equal(counts, ref["counts"])
+    assert np.array_equal(idx, ref["indices"])
+    # shells 1-4 (54 neighbours) always in, shell 5 (24) decided at the boundary
+    assert 54 <= counts.min() and counts.max() <= 78
+    if noise:
+        assert 54 < counts.mean() < 78
+
+
 @pytest.mark.parametrize("cells,temp", [(16, 1.44), (6, 3.0)])
 def test_md_sell_path_verlet_bit_exact(pc, oracle, cells, temp):
     """Same check for the SELL fallback path (staged SELL build)."""
