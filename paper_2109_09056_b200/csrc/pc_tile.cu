@@ -67,9 +67,6 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_PFDIST
 #define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
 #endif
-#ifndef PC_FORCE_L1PF
-#define PC_FORCE_L1PF 0         // >0: list group gi + L1PF prefetched into L1 and the next group's load may hit L1
-#endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
@@ -333,23 +330,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
-// next list group: from L1 when it was prefetched there (PC_FORCE_L1PF)
-__device__ __forceinline__ uint4 ld_group(const uint4* p) {
-#if PC_FORCE_L1PF
-  uint4 r;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-#else
-  return ld_stream(p);
-#endif
 }
 
 // ---- two pairs per call: the FP32 LJ magnitude as packed f32x2 ------------
@@ -1300,8 +1280,7 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   uint4 nxt = first;
   for (int gi = 0; gi < G; ++gi) {
     const uint4 q = nxt;
-    if (gi + 1 < G || tail) nxt = ld_group(lp + (gi + 1) * 32);
-    if (PC_FORCE_L1PF && gi + PC_FORCE_L1PF < G + (tail ? 1 : 0)) prefetch_l1(lp + (gi + PC_FORCE_L1PF) * 32);
+    if (gi + 1 < G || tail) nxt = ld_stream(lp + (gi + 1) * 32);
     if (PC_FORCE_PREFETCH && gi + PC_FORCE_PFDIST < G) prefetch_l2(lp + (gi + PC_FORCE_PFDIST) * 32);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
