@@ -222,7 +222,7 @@ def cpu_oracle_rate(kw, cells, steps):
     """Oracle port of the reference MD (numpy, 1 thread) on a bounded sample."""
     from oracle import particula_oracle as orc
     cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=steps))
-    drv = orc.MDOracle(cfg)
+    drv = orc.MDOracle(cfg, cell_loop=True)
     t0 = time.perf_counter()
     for s in range(1, steps + 1):
         drv.step(s)
@@ -244,7 +244,7 @@ def run_reference(args):
     cells = max(6, min(gc[0], 48, int((budget_atoms / 4) ** (1 / 3))))
     from oracle import particula_oracle as orc
     cfg = orc.MDConfig(**dict(kw, lattice_cells=cells, steps=args.steps))
-    drv = orc.MDOracle(cfg)
+    drv = orc.MDOracle(cfg, cell_loop=True)
     for s in range(1, args.warmup + 1):
         drv.step(s)
     t0 = time.perf_counter()
@@ -254,7 +254,8 @@ def run_reference(args):
     value = drv.n * args.steps / dt
     ncpu = os.cpu_count()
     sample = (f"oracle port of the reference MD (numpy, 1 thread: the reference is "
-              f"single-threaded; 1 of {ncpu} host cores) on fcc {cells}^3 = {drv.n} atoms, "
+              f"single-threaded; 1 of {ncpu} host cores; neighbor lists through the "
+              f"reference's per-cell loop) on fcc {cells}^3 = {drv.n} atoms, "
               f"same rho/T/rc/skin/rebuild as the fcc {'x'.join(map(str, gc))} workload")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
@@ -443,7 +444,8 @@ def run_ours(args):
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                "host_cores": os.cpu_count(),
                "sample": f"oracle port (numpy, 1 thread, as the single-threaded reference; "
-                         f"1 of {os.cpu_count()} host cores) 20 MD steps on fcc 16^3 = "
+                         f"1 of {os.cpu_count()} host cores; neighbor lists through the "
+                         f"reference's per-cell loop) 20 MD steps on fcc 16^3 = "
                          f"{natoms} atoms, same rho/T/rc/skin/rebuild ({secs:.1f} s)"}
     if rank == 0:
         shape = "x".join(map(str, gc))

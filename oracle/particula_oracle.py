@@ -240,6 +240,71 @@ def neighbor_pairs(x, low, high, periodic, cutoff, cell_ratio=1.0, chunk=16384, 
     return pi[o], pj[o]
 
 
+def neighbor_sets_cell_loop(x, low, high, periodic, cutoff, cell_ratio=1.0):
+    """Per-row sorted neighbor arrays (full convention, no self), restating the
+    reference's loop structure -- ref neighbors.py:49-97: a Python loop over
+    cells; per cell the union of its stencil cells' members (``np.unique``),
+    one vectorised min-image distance block (mine x candidates), and a Python
+    loop over the cell's rows that slices each row's hits.
+
+    Same sets as ``neighbor_pairs`` (tests/test_oracle_golden.py).  It exists so
+    that ``bench.py --impl reference`` pays the reference's own cost profile
+    (per-cell and per-row interpreter work) rather than the vectorised port's.
+    """
+    x = np.ascontiguousarray(x, np.float64)
+    n, d = x.shape
+    low = np.asarray(low, np.float64)
+    length = np.asarray(high, np.float64) - low
+    per = np.asarray(periodic, bool)
+    nc = np.maximum(1, np.floor(length / (cutoff * cell_ratio)).astype(np.int64))
+    idx = np.clip(np.floor((x - low) / (length / nc)).astype(np.int64), 0, nc - 1)
+    flat = (np.ravel_multi_index(tuple(idx.T), tuple(nc)) if n
+            else np.empty(0, np.int64))
+    ncells = int(np.prod(nc))
+    order = np.argsort(flat, kind="stable")
+    counts = np.bincount(flat, minlength=ncells)
+    start = np.concatenate(([0], np.cumsum(counts)))
+    members = [order[start[c]:start[c + 1]] for c in range(ncells)]
+    stencil = list(itertools.product(*[(-1, 0, 1)] * d))
+    rc2 = cutoff * cutoff
+    out = [np.empty(0, np.int64)] * n
+    for c in range(ncells):
+        mine = members[c]
+        if mine.size == 0:
+            continue
+        cc = np.array(np.unravel_index(c, tuple(nc)))
+        cells = set()
+        for off in stencil:
+            cell = cc + np.array(off)
+            ok = True
+            for a in range(d):
+                if per[a]:
+                    cell[a] %= nc[a]
+                elif not 0 <= cell[a] < nc[a]:
+                    ok = False
+                    break
+            if ok:
+                cells.add(int(np.ravel_multi_index(tuple(cell), tuple(nc))))
+        cand = np.unique(np.concatenate([members[k] for k in sorted(cells)]))
+        dx = box_min_image(x[cand][None, :, :] - x[mine][:, None, :], length, per)
+        hit = sqnorm(dx) < rc2
+        for row, i in enumerate(mine):
+            js = cand[hit[row]]
+            out[int(i)] = js[js != i]
+    return out
+
+
+def neighbor_pairs_cell_loop(x, low, high, periodic, cutoff, cell_ratio=1.0):
+    """``neighbor_pairs`` through the per-cell loop: the sets concatenated into
+    CSR rows and expanded to (i, j) as ref neighbors.py:119-127 and
+    VerletList.pairs (neighbors.py:39-46) do."""
+    sets = neighbor_sets_cell_loop(x, low, high, periodic, cutoff, cell_ratio)
+    cnt = np.array([js.size for js in sets], np.int64)
+    pj = np.concatenate(sets) if sets else np.empty(0, np.int64)
+    pi = np.repeat(np.arange(len(sets), dtype=np.int64), cnt)
+    return pi, pj.astype(np.int64)
+
+
 def validate_verlet_args(low, high, periodic, cutoff, layout, half_or_full,
                          cell_ratio):
     """Argument checks of ref neighbors.py:107-118 (ValueError)."""
@@ -679,9 +744,12 @@ class MDConfig:
 class MDOracle:
     """Velocity-Verlet LJ NVE on a simulated rank fabric -- ref md.py:129-292."""
 
-    def __init__(self, cfg: MDConfig):
+    def __init__(self, cfg: MDConfig, cell_loop: bool = False):
         cfg.validate()
         self.cfg = cfg
+        # cell_loop: neighbor lists through the reference's per-cell loop
+        # (neighbor_pairs_cell_loop; same pairs, the reference's cost profile)
+        self._pairs_fn = neighbor_pairs_cell_loop if cell_loop else neighbor_pairs
         a = (4.0 / cfg.density) ** (1.0 / 3.0)
         L = cfg.lattice_cells * a
         self.low = np.zeros(3)
@@ -726,7 +794,7 @@ class MDOracle:
         self.timings["halo"] += time.perf_counter() - t0
         t0 = time.perf_counter()
         search = (self.cfg.cutoff + self.cfg.skin) * CUTOFF_MARGIN
-        self.pairs = [neighbor_pairs(st.f["x0"], self.low, self.high,
+        self.pairs = [self._pairs_fn(st.f["x0"], self.low, self.high,
                                      self.periodic, search) for st in self.ranks]
         self.timings["neighbor"] += time.perf_counter() - t0
         self._forces()
