@@ -427,9 +427,10 @@ def run_ours(args):
 
     # the device leg's engine goes back to PyTorch's caching allocator, so the
     # end-to-end leg (a fresh engine through the public API) allocates from a
-    # warm pool, as a process calling run_md repeatedly does
+    # warm pool, as a process calling run_md repeatedly does (after an
+    # empty_cache the leg's setup paid ~20 ms of fresh cudaMallocs and varied
+    # run to run: profiles/r02aw/e2e_probe.txt)
     del drv, eng
-    torch.cuda.empty_cache()
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(pc, kw, args.e2e_steps or max(K, 200),
