@@ -74,7 +74,10 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #define PC_BUILD_WARPS 10       // build warps per CTA (2 CTAs per SM); 8 / 6: build +23 / +36 % (profiles/r02ad)
 #endif
 constexpr int kBuildWarps = PC_BUILD_WARPS;
-constexpr int kHitCap = 112;
+#ifndef PC_HIT_CAP
+#define PC_HIT_CAP 112          // build hit rows per lane (the row's list capacity)
+#endif
+constexpr int kHitCap = PC_HIT_CAP;
 constexpr int kHitSlack = 3;   // spare rows per hit column (unclamped 4-candidate stores)
 // force-kernel staging capacity (slots) and per-coordinate stride in shared
 // memory: compile-time so every LDS is [slot*8 + immediate]
