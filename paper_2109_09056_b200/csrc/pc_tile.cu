@@ -67,6 +67,9 @@ constexpr int kForceWarps = PC_FORCE_WARPS;
 #ifndef PC_FORCE_PFDIST
 #define PC_FORCE_PFDIST 2       // list groups ahead of the one in use that are L2-prefetched (3 / 4 / 6: 1063 / 1067 / 1070 vs 1052 us at C3, profiles/r02x)
 #endif
+#ifndef PC_FORCE_HALFU
+#define PC_FORCE_HALFU 1        // accumulate u / 2 and fm / 2 (bit-identical results, one instruction less per pair pair)
+#endif
 #ifndef PC_FORCE_PREFETCH
 #define PC_FORCE_PREFETCH 1     // L2 prefetch of list groups two ahead + epilogue velocities
 #endif
@@ -1247,8 +1250,16 @@ __device__ __forceinline__ void tile_pair2(const char* __restrict__ st, uint32_t
   const f32x2_t inv = pk2(rcp_approx(ra), rcp_approx(rb));
   const f32x2_t sr2 = UNIT_SIGMA ? inv : mul2(pk2(p.sig2, p.sig2), inv);
   const f32x2_t sr6 = mul2(mul2(sr2, sr2), sr2);
+#if PC_FORCE_HALFU
+  // h = u / 2 = sr6 (sr6 - 1/2), fm / 2 = h / r^2: the halves of the r01
+  // terms bit for bit (fl(2 sr6 - 1) = 2 fl(sr6 - 1/2); scaling by 2 is
+  // exact), one FADD2 with an immediate instead of a materialised 2.0 and an
+  // FFMA2; tile_row2 doubles the row's sums and force (exact)
+  const f32x2_t u = mul2(sr6, add2(sr6, pk2(-0.5f, -0.5f)));
+#else
   // u = 2 sr12 - sr6 = sr6 (2 sr6 - 1) (pair virial); fm = u / r^2
   const f32x2_t u = mul2(sr6, fma2(pk2(2.0f, 2.0f), sr6, pk2(-1.0f, -1.0f)));
+#endif
   const f32x2_t fm = mul2(u, inv);
   su2 = add2(su2, u);
   s62 = add2(s62, sr6);
@@ -1303,6 +1314,12 @@ __device__ __forceinline__ void tile_row2(const char* __restrict__ st_rt,
   upk2(s62, c0, c1);
   su = a0 + a1;
   s6 = c0 + c1;
+#if PC_FORCE_HALFU
+  su *= 2.0f;
+  fx *= 2.0;
+  fy *= 2.0;
+  fz *= 2.0;
+#endif
 }
 
 template <bool MI, bool UNIT_SIGMA, int B>
